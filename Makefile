@@ -1,0 +1,25 @@
+# Builds the C-ABI library in-tree (it travels to the GPU box with the repo).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --cudart static -Iinclude
+PKG := paper_2512_20777_b200
+SRC := $(PKG)/csrc/api.cu
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/expmb.h
+
+all: $(PKG)/libexpmb.so
+
+tools: tools/peaks
+
+tools/peaks: tools/peaks.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+$(PKG)/libexpmb.so: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
+
+ptxas: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/expmb_api.o $(SRC) 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" | paste - - - | sed 's/ptxas info    ://g'
+
+clean:
+	rm -f $(PKG)/libexpmb.so
+
+.PHONY: all clean ptxas tools

@@ -1,0 +1,101 @@
+/*
+ * expmb.h -- C ABI of libexpmb.so, the B200 (sm_100a) batched matrix
+ * exponential behind `paper_2512_20777_b200.expm`.
+ *
+ * Drop-in boundary for the reference hot path
+ *   expmkit.expm(W: Matrix, eps: float, scheme: str = "sastre") -> ExpmResult
+ *   (/root/reference/pkg/src/expmkit/engine.py:119-152,
+ *    re-exported at __init__.py:61-70)
+ * batched: one call exponentiates B independent n x n matrices.
+ *
+ * Conventions
+ *  - Every pointer argument of expmb_expm is DEVICE memory owned by the caller
+ *    (the library never allocates; scratch comes from `workspace`).
+ *  - Matrices are row-major, contiguous, [batch][n][n], dtype fp32 or fp64.
+ *  - All work is enqueued on `stream` (a cudaStream_t passed as void*); the
+ *    call does not synchronise the device except where noted (large-n
+ *    path: one small device->host copy of the per-matrix plans).
+ *  - Errors in arguments are returned synchronously as negative codes
+ *    (mapped by the Python layer to ToleranceError / MatrixError, exactly
+ *    like select.py:72-79, matrix.py:52-55, engine.py:137).  Numerical
+ *    failure is reported per matrix in `nonfinite[]` (NonFiniteError,
+ *    matrix.py:56-57,95-102).
+ *  - Stateless and re-entrant; constant tables live in __constant__ memory.
+ */
+#ifndef EXPMB_H_
+#define EXPMB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes */
+#define EXPMB_F32 0
+#define EXPMB_F64 1
+/* scheme codes: select.py:58-61 SCHEME_SASTRE / SCHEME_PS */
+#define EXPMB_SASTRE 0
+#define EXPMB_PS 1
+
+/* return codes */
+#define EXPMB_OK 0
+#define EXPMB_ERR_TOLERANCE (-1)   /* ToleranceError  (select.py:72-79)            */
+#define EXPMB_ERR_SHAPE (-2)       /* MatrixError: n < 1 / batch < 0 (matrix.py:52-55) */
+#define EXPMB_ERR_SCHEME (-3)      /* MatrixError: unknown scheme (engine.py:137)  */
+#define EXPMB_ERR_DTYPE (-4)       /* MatrixError: dtype not fp32/fp64             */
+#define EXPMB_ERR_WORKSPACE (-5)   /* workspace missing or too small               */
+#define EXPMB_ERR_CUDA (-6)        /* a CUDA launch/copy failed                    */
+#define EXPMB_ERR_ALIGN (-7)       /* W/X not 16-byte aligned                      */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int expmb_version(void);
+
+/* Human-readable text for a return code. */
+const char* expmb_strerror(int code);
+
+/* Smallest admissible tolerance for a dtype: 2^-53 for fp64 (select.py:55),
+ * 2^-24 for fp32 (the same rule at the working precision). */
+double expmb_unit_roundoff(int dtype);
+
+/* Scratch bytes expmb_expm needs for this problem (0 for the fused small-n
+ * path).  Replaces nothing in the reference (numpy allocates per op). */
+size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme);
+
+/*
+ * Batched expm.  Replaces engine.py:119-152 (expm), which the reference
+ * calls once per matrix (bench.py:266-269, cli.py:40-43).
+ *
+ *   W          [batch,n,n] input (read only)
+ *   X          [batch,n,n] output e^W (may not alias W)
+ *   eps        tolerance (>= expmb_unit_roundoff(dtype), not NaN)
+ *   scheme     EXPMB_SASTRE (orders 1,2,4,8,15+) or EXPMB_PS (1..16)
+ *   m, s       [batch] selected order / scaling          (EvalPlan.m/.s)
+ *   e1, e2     [batch] two-term remainder bounds         (EvalPlan.e1/.e2)
+ *   norms      [batch,2] ||W||_1 and ||W^2||_1 (NaN if W^2 never formed)
+ *   mults      [batch] n x n products charged (ExpmResult.mults)
+ *   nonfinite  [batch] 1 where the input or any produced value was NaN/Inf
+ *   Any of m..nonfinite may be NULL (not written).
+ */
+int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype,
+               double eps, int scheme,
+               int8_t* m, int8_t* s, double* e1, double* e2, double* norms,
+               int32_t* mults, uint8_t* nonfinite,
+               void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Host-side evaluation of the SAME selector the kernels run (one
+ * __host__ __device__ function), for testing without a GPU.  Replaces
+ * select.py:164-220 given the power norms: norms[p-1] = ||W^p||_1 for
+ * p = 1..4 (entries beyond what the ladder touches are ignored).
+ * Returns the highest power the ladder needed (1..4) and writes the plan.
+ */
+int expmb_select_host(const double* norms, double eps, int scheme,
+                      int* m, int* s, double* e1, double* e2);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXPMB_H_ */

@@ -1,0 +1,85 @@
+"""ctypes binding of libexpmb.so (the C ABI in include/expmb.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``).  There
+is no fallback: if it is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libexpmb.so")
+
+EXPMB_F32, EXPMB_F64 = 0, 1
+EXPMB_SASTRE, EXPMB_PS = 0, 1
+
+ERR_TOLERANCE = -1
+ERR_SHAPE = -2
+ERR_SCHEME = -3
+ERR_DTYPE = -4
+ERR_WORKSPACE = -5
+ERR_CUDA = -6
+ERR_ALIGN = -7
+
+# Every symbol include/expmb.h declares (tests check the .so exports them all).
+EXPORTS = (
+    "expmb_version",
+    "expmb_strerror",
+    "expmb_unit_roundoff",
+    "expmb_workspace_bytes",
+    "expmb_expm",
+    "expmb_select_host",
+)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libexpmb.so once; raise loudly if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build the CUDA library first (`make` or "
+            "`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback."
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    L.expmb_version.restype = c.c_int
+    L.expmb_strerror.restype = c.c_char_p
+    L.expmb_strerror.argtypes = [c.c_int]
+    L.expmb_unit_roundoff.restype = c.c_double
+    L.expmb_unit_roundoff.argtypes = [c.c_int]
+    L.expmb_workspace_bytes.restype = c.c_size_t
+    L.expmb_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int, c.c_int]
+    L.expmb_expm.restype = c.c_int
+    L.expmb_expm.argtypes = [
+        c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+        c.c_void_p, c.c_size_t, c.c_void_p,
+    ]
+    L.expmb_select_host.restype = c.c_int
+    L.expmb_select_host.argtypes = [
+        c.POINTER(c.c_double), c.c_double, c.c_int,
+        c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
+    ]
+    _lib = L
+    return L
+
+
+def strerror(code: int) -> str:
+    return lib().expmb_strerror(code).decode()
+
+
+def select_host(norms, eps: float, scheme: int):
+    """Run the kernels' selector on the host: returns (m, s, e1, e2, max_power)."""
+    L = lib()
+    arr = (ctypes.c_double * 4)(*(list(norms) + [float("nan")] * (4 - len(norms))))
+    m, s = ctypes.c_int(), ctypes.c_int()
+    e1, e2 = ctypes.c_double(), ctypes.c_double()
+    have = L.expmb_select_host(arr, float(eps), int(scheme), ctypes.byref(m), ctypes.byref(s),
+                               ctypes.byref(e1), ctypes.byref(e2))
+    return m.value, s.value, e1.value, e2.value, have

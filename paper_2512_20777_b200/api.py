@@ -1,0 +1,189 @@
+"""Batched drop-in for ``expmkit.expm`` (engine.py:119-152) on B200.
+
+    res = expm(W, eps, scheme="sastre")      # W: cuda tensor [..., n, n] fp32/fp64
+    res.value   -> tensor [..., n, n]        (ExpmResult.value)
+    res.plan.m / .s / .e1 / .e2              (EvalPlan, select.py:144-161)
+    res.mults   -> int32 tensor [...]        (ExpmResult.mults = budget(m) + s)
+    res.wall_time                            (seconds, host clock around the call)
+
+Error behaviour follows the reference: ToleranceError for eps NaN or below
+the dtype's unit roundoff (select.py:72-79), MatrixError for non-square /
+empty input and unknown schemes (matrix.py:52-55, engine.py:137),
+NonFiniteError when an input or any produced matrix is not finite
+(matrix.py:56-57, 95-102) -- raised after the batch completes, listing the
+offending batch indices.  CPU tensors raise: there is no CPU fallback.
+
+The compute is the registered custom op ``expmkit_b200::expm`` over the C ABI
+of libexpmb.so (include/expmb.h).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .tables import (MatrixError, NonFiniteError, SCHEME_PS, SCHEME_SASTRE, ToleranceError,
+                     UNIT_ROUNDOFF, UNIT_ROUNDOFF_F32)
+
+_SCHEMES = {SCHEME_SASTRE: _lib.EXPMB_SASTRE, SCHEME_PS: _lib.EXPMB_PS}
+
+
+@dataclass
+class EvalPlan:
+    """Batched select.py:144-161 (tensors instead of scalars)."""
+    m: torch.Tensor       # int8 [...]
+    s: torch.Tensor       # int8 [...]
+    scheme: str
+    e1: torch.Tensor      # float64 [...]
+    e2: torch.Tensor      # float64 [...]
+    norms: torch.Tensor   # float64 [..., 2]: ||W||_1, ||W^2||_1 (NaN if W^2 never formed)
+
+
+@dataclass
+class ExpmResult:
+    """Batched engine.py:64-77."""
+    value: torch.Tensor
+    plan: EvalPlan
+    mults: torch.Tensor   # int32 [...]
+    wall_time: float
+    nonfinite: torch.Tensor  # bool [...]
+
+
+def unit_roundoff(dtype: torch.dtype) -> float:
+    return UNIT_ROUNDOFF_F32 if dtype == torch.float32 else UNIT_ROUNDOFF
+
+
+def check_tolerance(eps: float, dtype: torch.dtype = torch.float64) -> float:
+    """select.py:72-79, with the fp32 floor for fp32 inputs."""
+    eps = float(eps)
+    floor = unit_roundoff(dtype)
+    if math.isnan(eps) or eps < floor:
+        raise ToleranceError(
+            f"tolerance {eps!r} below unit roundoff {floor:.3e}; "
+            f"sub-roundoff accuracy cannot be guaranteed in {str(dtype).replace('torch.', '')}")
+    return eps
+
+
+def _raise_rc(rc: int):
+    if rc == _lib.ERR_TOLERANCE:
+        raise ToleranceError(_lib.strerror(rc))
+    if rc in (_lib.ERR_SHAPE, _lib.ERR_SCHEME, _lib.ERR_DTYPE):
+        raise MatrixError(_lib.strerror(rc))
+    raise RuntimeError(f"libexpmb: {_lib.strerror(rc)} (code {rc})")
+
+
+def _launch(W: torch.Tensor, X: torch.Tensor, eps: float, scheme_code: int,
+            m, s, e1, e2, norms, mults, nonfinite) -> None:
+    """One C-ABI call on the current stream (all pointers device memory)."""
+    L = _lib.lib()
+    B = W.shape[0]
+    n = W.shape[-1]
+    dt = _lib.EXPMB_F32 if W.dtype == torch.float32 else _lib.EXPMB_F64
+    wsb = L.expmb_workspace_bytes(B, n, dt, scheme_code)
+    ws = torch.empty(max(int(wsb), 1), dtype=torch.uint8, device=W.device) if wsb else None
+    stream = torch.cuda.current_stream(W.device).cuda_stream
+
+    def p(t):
+        return None if t is None else t.data_ptr()
+
+    rc = L.expmb_expm(W.data_ptr(), X.data_ptr(), B, n, dt, float(eps), scheme_code,
+                      p(m), p(s), p(e1), p(e2), p(norms), p(mults), p(nonfinite),
+                      p(ws), int(wsb), stream)
+    if rc != 0:
+        _raise_rc(rc)
+
+
+@torch.library.custom_op("expmkit_b200::expm", mutates_args=())
+def _expm_op(W: torch.Tensor, eps: float, scheme: int) -> tuple[
+        torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor,
+        torch.Tensor, torch.Tensor]:
+    B = W.shape[0]
+    dev = W.device
+    X = torch.empty_like(W)
+    m = torch.empty(B, dtype=torch.int8, device=dev)
+    s = torch.empty(B, dtype=torch.int8, device=dev)
+    e1 = torch.empty(B, dtype=torch.float64, device=dev)
+    e2 = torch.empty(B, dtype=torch.float64, device=dev)
+    norms = torch.empty(B, 2, dtype=torch.float64, device=dev)
+    mults = torch.empty(B, dtype=torch.int32, device=dev)
+    nonfinite = torch.empty(B, dtype=torch.uint8, device=dev)
+    _launch(W, X, eps, scheme, m, s, e1, e2, norms, mults, nonfinite)
+    return X, m, s, e1, e2, norms, mults, nonfinite
+
+
+@_expm_op.register_fake
+def _(W, eps, scheme):
+    B = W.shape[0]
+    return (torch.empty_like(W), W.new_empty(B, dtype=torch.int8), W.new_empty(B, dtype=torch.int8),
+            W.new_empty(B, dtype=torch.float64), W.new_empty(B, dtype=torch.float64),
+            W.new_empty(B, 2, dtype=torch.float64), W.new_empty(B, dtype=torch.int32),
+            W.new_empty(B, dtype=torch.uint8))
+
+
+def _validate(W: torch.Tensor, eps: float, scheme: str) -> tuple[torch.Tensor, int]:
+    if not isinstance(W, torch.Tensor):
+        raise MatrixError(f"expected a torch.Tensor, got {type(W).__name__}")
+    if W.dim() < 2 or W.shape[-1] != W.shape[-2]:
+        raise MatrixError(f"expected [..., n, n] square matrices, got shape {tuple(W.shape)}")
+    if W.shape[-1] < 1:
+        raise MatrixError("matrix order must be at least 1")
+    if scheme not in _SCHEMES:
+        raise MatrixError(f"unknown scheme {scheme!r}; expected 'ps' or 'sastre'")
+    if W.dtype not in (torch.float32, torch.float64):
+        raise MatrixError(f"dtype must be float32 or float64, got {W.dtype}")
+    if W.device.type != "cuda":
+        raise RuntimeError("expmkit_b200.expm runs on CUDA tensors only (no CPU fallback)")
+    check_tolerance(eps, W.dtype)
+    Wc = W.reshape(-1, W.shape[-1], W.shape[-1])
+    if not Wc.is_contiguous() or Wc.data_ptr() % 16:
+        Wc = Wc.contiguous().clone()
+    return Wc, _SCHEMES[scheme]
+
+
+def expm(W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, check_finite: bool = True) -> ExpmResult:
+    """Selected-order scaled-Taylor exponential of every matrix in ``W``.
+
+    Mirrors engine.py:119-152 per matrix; ``scheme`` selects the Sastre
+    evaluation formulas (orders 1,2,4,8,15+) or Paterson-Stockmeyer (1..16).
+    """
+    t0 = time.perf_counter()
+    Wc, code = _validate(W, eps, scheme)
+    lead = W.shape[:-2]
+    n = W.shape[-1]
+    X, m, s, e1, e2, norms, mults, nonfinite = torch.ops.expmkit_b200.expm(Wc, float(eps), code)
+    bad = nonfinite.bool()
+    if check_finite and Wc.shape[0] > 0 and bool(bad.any()):
+        idx = torch.nonzero(bad).flatten()[:8].tolist()
+        raise NonFiniteError(f"operation produced non-finite entries (batch indices {idx}...)")
+    plan = EvalPlan(m.reshape(lead), s.reshape(lead), scheme, e1.reshape(lead), e2.reshape(lead),
+                    norms.reshape(*lead, 2))
+    return ExpmResult(X.reshape(*lead, n, n), plan, mults.reshape(lead), time.perf_counter() - t0,
+                      bad.reshape(lead))
+
+
+def expm_into(W: torch.Tensor, X: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE,
+              plan: dict | None = None) -> None:
+    """Allocation-free variant for steady-state loops and CUDA graphs:
+    writes e^W into the preallocated ``X`` (same shape/dtype) and, if given,
+    into the plan tensors of ``plan`` (keys m, s, e1, e2, norms, mults, nonfinite).
+    No host synchronisation for n <= 64."""
+    Wc, code = _validate(W, eps, scheme)
+    if X.shape != W.shape or X.dtype != W.dtype or not X.is_contiguous():
+        raise MatrixError("X must be a contiguous tensor shaped and typed like W")
+    plan = plan or {}
+    _launch(Wc, X.view(Wc.shape), eps, code, plan.get("m"), plan.get("s"), plan.get("e1"),
+            plan.get("e2"), plan.get("norms"), plan.get("mults"), plan.get("nonfinite"))
+
+
+def select_sastre(W: torch.Tensor, eps: float) -> EvalPlan:
+    """select.py:228-234, batched (runs the full op; the plan is its by-product)."""
+    return expm(W, eps, SCHEME_SASTRE, check_finite=False).plan
+
+
+def select_ps(W: torch.Tensor, eps: float) -> EvalPlan:
+    """select.py:223-225, batched."""
+    return expm(W, eps, SCHEME_PS, check_finite=False).plan

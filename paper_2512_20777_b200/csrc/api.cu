@@ -1,0 +1,128 @@
+// api.cu -- the C ABI of libexpmb.so (declared in include/expmb.h).
+//
+// Validation mirrors the reference's error behaviour (select.py:72-79
+// check_tolerance, matrix.py:52-55 shape checks, engine.py:137 unknown
+// scheme); dispatch picks the fused small-n kernel (n <= 64) or the large-n
+// GEMM pipeline (n > 64).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/expmb.h"
+#include "fused_small.cuh"
+#include "large.cuh"
+
+namespace expmb {
+
+static int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
+static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, cudaStream_t st) {
+  using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
+  auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME>;
+  static int occ = -1;  // per instantiation; identical on every B200
+  if (occ < 0) {
+    if (F::kSmem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::kSmem) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, F::NT, F::kSmem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t ctas_needed = (batch + GROUPS - 1) / GROUPS;
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(ctas_needed < persistent ? ctas_needed : persistent);
+  if (grid <= 0) return EXPMB_OK;
+  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, eps, po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
+template <typename T, int SCHEME>
+static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, cudaStream_t st) {
+  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, st);
+  if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, st);
+  return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, st);
+}
+
+}  // namespace expmb
+
+using namespace expmb;
+
+extern "C" {
+
+int expmb_version(void) { return 100; }
+
+const char* expmb_strerror(int code) {
+  switch (code) {
+    case EXPMB_OK: return "ok";
+    case EXPMB_ERR_TOLERANCE: return "tolerance NaN or below the unit roundoff of the dtype";
+    case EXPMB_ERR_SHAPE: return "matrix order must be at least 1 and batch non-negative";
+    case EXPMB_ERR_SCHEME: return "unknown scheme; expected sastre (0) or ps (1)";
+    case EXPMB_ERR_DTYPE: return "dtype must be fp32 (0) or fp64 (1)";
+    case EXPMB_ERR_WORKSPACE: return "workspace missing or smaller than expmb_workspace_bytes()";
+    case EXPMB_ERR_CUDA: return "CUDA launch or copy failed";
+    case EXPMB_ERR_ALIGN: return "W and X must be 16-byte aligned";
+    default: return "unknown error";
+  }
+}
+
+double expmb_unit_roundoff(int dtype) { return dtype == EXPMB_F32 ? 0x1p-24 : 0x1p-53; }
+
+size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme) {
+  if (n <= 64 || batch <= 0) return 0;
+  return large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
+}
+
+int expmb_select_host(const double* norms, double eps, int scheme, int* m, int* s, double* e1, double* e2) {
+  Plan p{};
+  int have = 1;
+  for (;;) {
+    int need = select_walk(norms, have, eps, scheme, &p);
+    if (need == 0) break;
+    have = need;
+  }
+  if (m) *m = p.m;
+  if (s) *s = p.s;
+  if (e1) *e1 = p.e1;
+  if (e2) *e2 = p.e2;
+  return have;
+}
+
+int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, double eps, int scheme, int8_t* m,
+               int8_t* s, double* e1, double* e2, double* norms, int32_t* mults, uint8_t* nonfinite, void* workspace,
+               size_t workspace_bytes, void* stream) {
+  if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
+  if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS) return EXPMB_ERR_SCHEME;
+  if (n < 1 || batch < 0) return EXPMB_ERR_SHAPE;
+  if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
+  if (((uintptr_t)W | (uintptr_t)X) & 15u) return EXPMB_ERR_ALIGN;
+  if (batch == 0) return EXPMB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  PlanOut po{m, s, e1, e2, norms, mults, nonfinite};
+  if (n <= 64) {
+    if (dtype == EXPMB_F32) {
+      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>((const float*)W, (float*)X, batch, n, eps, po, st)
+                                    : dispatch_small<float, 1>((const float*)W, (float*)X, batch, n, eps, po, st);
+    }
+    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>((const double*)W, (double*)X, batch, n, eps, po, st)
+                                  : dispatch_small<double, 1>((const double*)W, (double*)X, batch, n, eps, po, st);
+  }
+  const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
+  if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
+  return large_expm(W, X, batch, n, dtype, eps, scheme, po, workspace, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// large.cuh -- batched expm for n > 64: bucketed GEMM pipeline.
+//
+// Same algorithm as engine.py:119-152, re-scheduled for a batch:
+//   K_norm    ||W||_1 per matrix + the m=1 rung (select.py:169-188); decides
+//             which matrices need W^2 (device flag, no host sync).
+//   G stage0  W^2 = W W for flagged matrices, epilogue writes per-tile column
+//             abs-sum partials (select.py:192-193).  PS: W^3, W^4 likewise.
+//   K_select  ||W^2||_1 (fixed-order reduction of the partials) and the
+//             ladder (select.py:164-220) -> m, s, e1, e2, mults.
+//   -- one device->host copy of (m, s): the host buckets the batch --
+//   K_elem    T0/T1/T2 results, T4's inner factor, R1 = c1 A^2 + c2 A
+//   G stage1..3  the products of poly.py:189-230, each epilogue emitting the
+//             next linear combinations (y02/L2/R2, y12/L3/R3, X) so no
+//             separate elementwise pass runs between products
+//   G square  s squarings (engine.py:80-87), bucket = prefix of the batch
+//             sorted by s descending.
+// The 2^-s, 2^-2s scalings (engine.py:139-140) are folded into epilogue
+// coefficients; they are powers of two so the folding is exact.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "fused_small.cuh"
+#include "gemm_simt.cuh"
+#include "select.cuh"
+
+namespace expmb {
+
+// ---------------------------------------------------------------------------
+// workspace layout (per chunk of `chunk` matrices)
+// ---------------------------------------------------------------------------
+constexpr int kLargeBufsSastre = 7;  // W2 Y0 Y1 La Ra Lb Rb   (Tmp aliases Lb)
+constexpr int kLargeBufsPS = 6;      // W2 W3 W4 Q0 Q1 Tmp
+constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers
+
+struct LargeLayout {
+  int64_t chunk;
+  size_t mat_bytes;
+  int nbufs;
+  int tiles_m;
+  size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_m, off_s, off_e1, off_e2, off_list, total;
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static inline LargeLayout large_layout(int64_t batch, int n, int esize, int scheme) {
+  LargeLayout L{};
+  L.mat_bytes = align256((size_t)n * n * esize);
+  L.nbufs = scheme == 1 ? kLargeBufsPS : kLargeBufsSastre;
+  const size_t per = L.mat_bytes * L.nbufs;
+  int64_t chunk = (int64_t)(kLargeWsCap / per);
+  if (chunk < 1) chunk = 1;
+  if (chunk > 65535) chunk = 65535;  // gridDim.z
+  if (chunk > batch) chunk = batch;
+  L.chunk = chunk;
+  L.tiles_m = (n + kGemmBM - 1) / kGemmBM;
+  size_t off = 0;
+  L.off_bufs = off; off += per * chunk;
+  L.off_part = off; off += align256((size_t)chunk * L.tiles_m * n * sizeof(double));
+  L.off_norm1 = off; off += align256((size_t)chunk * 4 * sizeof(double));
+  L.off_norm2 = off; off += 0;  // norms for powers 1..4 live in the same [chunk][4] array
+  L.off_need = off; off += align256((size_t)chunk * sizeof(int));
+  L.off_m = off; off += align256((size_t)chunk);
+  L.off_s = off; off += align256((size_t)chunk);
+  L.off_e1 = off; off += align256((size_t)chunk * sizeof(double));
+  L.off_e2 = off; off += align256((size_t)chunk * sizeof(double));
+  L.off_list = off; off += align256((size_t)chunk * 8 * sizeof(int));
+  L.total = off;
+  return L;
+}
+
+static inline size_t large_workspace_bytes(int64_t batch, int n, int esize, int scheme) {
+  return large_layout(batch, n, esize, scheme).total;
+}
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+
+// ||W||_1 (column abs-sums in binary64, fixed order) + the first ladder rung.
+template <typename T>
+__global__ void __launch_bounds__(256) k_norm1(const T* __restrict__ W, int n, double eps, int scheme,
+                                               double* __restrict__ nrm4, int* __restrict__ need,
+                                               int8_t* __restrict__ pm, int8_t* __restrict__ ps,
+                                               double* __restrict__ pe1, double* __restrict__ pe2) {
+  const int z = blockIdx.x;
+  const T* w = W + (size_t)z * n * n;
+  __shared__ double red[256];
+  double mx = -INFINITY;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < n; ++r) a += fabs((double)w[(size_t)r * n + c]);
+    mx = nanmax(mx, a);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] = nanmax(red[threadIdx.x], red[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double nr[4] = {red[0], NAN, NAN, NAN};
+    nrm4[4 * z + 0] = nr[0];
+    nrm4[4 * z + 1] = NAN;
+    Plan p{};
+    const int nd = select_walk(nr, 1, eps, scheme, &p);
+    need[z] = nd;
+    if (nd == 0) {
+      pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
+    }
+  }
+}
+
+// Reduce the per-tile column partials of W^p and walk the ladder again.
+__global__ void __launch_bounds__(256) k_select(const double* __restrict__ part, int tiles_m, int n, int have,
+                                                double eps, int scheme, double* __restrict__ nrm4,
+                                                int* __restrict__ need, int8_t* __restrict__ pm,
+                                                int8_t* __restrict__ ps, double* __restrict__ pe1,
+                                                double* __restrict__ pe2) {
+  const int z = blockIdx.x;
+  if (need[z] != have) return;  // this matrix did not form W^have
+  __shared__ double red[256];
+  const double* pz = part + (size_t)z * tiles_m * n;
+  double mx = -INFINITY;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double a = 0.0;
+    for (int t = 0; t < tiles_m; ++t) a += pz[(size_t)t * n + c];
+    mx = nanmax(mx, a);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] = nanmax(red[threadIdx.x], red[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    nrm4[4 * z + have - 1] = red[0];
+    double nr[4];
+    for (int q = 0; q < 4; ++q) nr[q] = nrm4[4 * z + q];
+    Plan p{};
+    const int nd = select_walk(nr, have, eps, scheme, &p);
+    need[z] = nd;
+    if (nd == 0) {
+      pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
+    }
+  }
+}
+
+// Per-matrix outputs + non-finite scan of the final X (and of W).
+template <typename T>
+__global__ void __launch_bounds__(256) k_finish(const T* __restrict__ W, const T* __restrict__ X, int n, int scheme,
+                                                const double* __restrict__ nrm4, const int8_t* __restrict__ pm,
+                                                const int8_t* __restrict__ ps, const double* __restrict__ pe1,
+                                                const double* __restrict__ pe2, int64_t base, PlanOut po) {
+  const int z = blockIdx.x;
+  const size_t nn = (size_t)n * n;
+  const T* x = X + (size_t)z * nn;
+  const T* w = W + (size_t)z * nn;
+  int bad = 0;
+  for (size_t i = threadIdx.x; i < nn; i += blockDim.x) bad |= !(isfinite(x[i]) && isfinite(w[i]));
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    const int64_t g = base + z;
+    const int m = pm[z], s = ps[z];
+    const double n1 = nrm4[4 * z], n2 = nrm4[4 * z + 1];
+    if (po.m) po.m[g] = (int8_t)m;
+    if (po.s) po.s[g] = (int8_t)s;
+    if (po.e1) po.e1[g] = pe1[z];
+    if (po.e2) po.e2[g] = pe2[z];
+    if (po.norms) { po.norms[2 * g] = n1; po.norms[2 * g + 1] = n2; }
+    if (po.mults) po.mults[g] = budget(m, scheme) + s;
+    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || !(n1 <= INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+template <typename T>
+static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int scheme, int64_t base, PlanOut po,
+                           unsigned char* ws, const LargeLayout& L, cudaStream_t st) {
+  const size_t nn = (size_t)n * n;
+  auto buf = [&](int b) { return reinterpret_cast<T*>(ws + L.off_bufs + (size_t)b * L.mat_bytes * L.chunk); };
+  // buffers are [buffer][matrix] with stride mat_bytes
+  const int64_t mstride = (int64_t)(L.mat_bytes / sizeof(T));
+  double* part = reinterpret_cast<double*>(ws + L.off_part);
+  double* nrm4 = reinterpret_cast<double*>(ws + L.off_norm1);
+  int* need = reinterpret_cast<int*>(ws + L.off_need);
+  int8_t* dm = reinterpret_cast<int8_t*>(ws + L.off_m);
+  int8_t* ds = reinterpret_cast<int8_t*>(ws + L.off_s);
+  double* de1 = reinterpret_cast<double*>(ws + L.off_e1);
+  double* de2 = reinterpret_cast<double*>(ws + L.off_e2);
+  int* dlist = reinterpret_cast<int*>(ws + L.off_list);
+  const int ic = (int)cnt;
+
+  k_norm1<T><<<ic, 256, 0, st>>>(W, n, eps, scheme, nrm4, need, dm, ds, de1, de2);
+
+  GemmCtx<T> g{};
+  g.n = n;
+  g.W = W;
+  g.X = X;
+  g.mstride = mstride;
+  g.wstride = (int64_t)nn;
+  g.m = dm;
+  g.s = ds;
+  g.need = need;
+  g.part = part;
+  g.tiles_m = L.tiles_m;
+  g.scheme = scheme;
+  if (scheme == 0) {
+    g.W2 = buf(0); g.Y0 = buf(1); g.Y1 = buf(2); g.La = buf(3); g.Ra = buf(4); g.Lb = buf(5); g.Rb = buf(6);
+    g.Tmp = g.Lb;
+  } else {
+    g.W2 = buf(0); g.W3 = buf(1); g.W4 = buf(2); g.La = buf(3); g.Ra = buf(4); g.Tmp = buf(5);
+  }
+
+  // powers + ladder, gated on device flags (no host round trip)
+  const int maxp = scheme == 1 ? 4 : 2;
+  for (int p = 2; p <= maxp; ++p) {
+    if (gemm_launch<T>(g, p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic, st)) return EXPMB_ERR_CUDA;
+    k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, eps, scheme, nrm4, need, dm, ds, de1, de2);
+  }
+
+  // one small device->host copy of the plans
+  std::vector<int8_t> hm(cnt), hs(cnt);
+  if (cudaMemcpyAsync(hm.data(), dm, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  if (cudaMemcpyAsync(hs.data(), ds, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return EXPMB_ERR_CUDA;
+
+  // bucket scheduler: stage lists; every list is sorted by s descending so
+  // the squaring buckets are prefixes of one list.
+  std::vector<int> order(cnt);
+  for (int i = 0; i < ic; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return hs[a] > hs[b]; });
+  std::vector<int> lists;
+  lists.reserve(cnt * 4);
+  std::vector<int> l_elem(order), l_s1, l_s2, l_s3, l_sq(order);
+  int maxs = 0;
+  for (int i : order) {
+    const int m = hm[i], s = hs[i];
+    if (s > maxs) maxs = s;
+    if (scheme == 0) {
+      if (m >= 4) l_s1.push_back(i);
+      if (m >= 8) l_s2.push_back(i);
+      if (m >= 15) l_s3.push_back(i);
+    } else if (m >= 1) {
+      const int k = ps_k_of(m);
+      if (k >= 2) l_s1.push_back(i);
+      if (k >= 3) l_s2.push_back(i);
+      if (k >= 4) l_s3.push_back(i);
+    }
+  }
+  // upload: [elem | s1 | s2 | s3 | sq]
+  std::vector<int> hl;
+  hl.insert(hl.end(), l_elem.begin(), l_elem.end());
+  const size_t o1 = hl.size(); hl.insert(hl.end(), l_s1.begin(), l_s1.end());
+  const size_t o2 = hl.size(); hl.insert(hl.end(), l_s2.begin(), l_s2.end());
+  const size_t o3 = hl.size(); hl.insert(hl.end(), l_s3.begin(), l_s3.end());
+  const size_t o4 = hl.size(); hl.insert(hl.end(), l_sq.begin(), l_sq.end());
+  if (cudaMemcpyAsync(dlist, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return EXPMB_ERR_CUDA;
+
+  if (elem_launch<T>(g, dlist, ic, st)) return EXPMB_ERR_CUDA;
+  if (!l_s1.empty() && gemm_launch<T>(g, STAGE_E1, dlist + o1, (int)l_s1.size(), st)) return EXPMB_ERR_CUDA;
+  if (!l_s2.empty() && gemm_launch<T>(g, STAGE_E2, dlist + o2, (int)l_s2.size(), st)) return EXPMB_ERR_CUDA;
+  if (!l_s3.empty() && gemm_launch<T>(g, STAGE_E3, dlist + o3, (int)l_s3.size(), st)) return EXPMB_ERR_CUDA;
+  for (int q = 0; q < maxs; ++q) {
+    int c = 0;
+    while (c < ic && hs[l_sq[c]] > q) ++c;
+    g.sq_step = q;
+    if (gemm_launch<T>(g, STAGE_SQ, dlist + o4, c, st)) return EXPMB_ERR_CUDA;
+  }
+  k_finish<T><<<ic, 256, 0, st>>>(W, X, n, scheme, nrm4, dm, ds, de1, de2, base, po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
+static inline int large_expm(const void* W, void* X, int64_t batch, int n, int dtype, double eps, int scheme,
+                             PlanOut po, void* workspace, cudaStream_t st) {
+  const int es = dtype == 0 ? 4 : 8;
+  const LargeLayout L = large_layout(batch, n, es, scheme);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  for (int64_t b0 = 0; b0 < batch; b0 += L.chunk) {
+    const int64_t cnt = std::min<int64_t>(L.chunk, batch - b0);
+    const size_t off = (size_t)b0 * n * n;
+    int rc;
+    if (dtype == 0)
+      rc = large_run_chunk<float>(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n,
+                                  eps, scheme, b0, po, ws, L, st);
+    else
+      rc = large_run_chunk<double>(reinterpret_cast<const double*>(W) + off, reinterpret_cast<double*>(X) + off, cnt,
+                                   n, eps, scheme, b0, po, ws, L, st);
+    if (rc != EXPMB_OK) return rc;
+  }
+  return EXPMB_OK;
+}
+
+}  // namespace expmb

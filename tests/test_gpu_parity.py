@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the public op / C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): identical (m, s) per matrix except where the
+reference's own norms sit within 1e-4 log2 units of a ladder/scaling
+threshold, and relative 1-norm difference <= 1e-12 (fp64) / <= 1e-5 (fp32).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_20777_b200 as X
+from paper_2512_20777_b200 import workloads as WL
+from oracle import expm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float64: 1e-12, torch.float32: 1e-5}
+
+
+def _rel1(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    d = np.abs(a - b).sum(axis=-2).max(axis=-1)
+    r = np.abs(b).sum(axis=-2).max(axis=-1)
+    return d / r
+
+
+def _run(Wnp, eps, scheme="sastre", dtype=torch.float64, check_finite=True):
+    W = torch.as_tensor(Wnp).to(device="cuda", dtype=dtype)
+    res = X.expm(W, eps, scheme, check_finite=check_finite)
+    torch.cuda.synchronize()
+    return res
+
+
+def _oracle_batch(Wnp, eps, scheme="sastre"):
+    return O.expm_batch(np.asarray(Wnp, np.float64), eps, scheme)
+
+
+def _check_batch(Wnp, eps, scheme, dtype, label=""):
+    """Full parity check of one batch; returns (#exempt, worst rel err)."""
+    res = _run(Wnp, eps, scheme, dtype, check_finite=False)
+    val, m, s, e1, e2, mults, bad = _oracle_batch(Wnp, eps, scheme)
+    gm = res.plan.m.cpu().numpy().astype(int)
+    gs = res.plan.s.cpu().numpy().astype(int)
+    gmu = res.mults.cpu().numpy()
+    gbad = res.nonfinite.cpu().numpy()
+    assert np.array_equal(gbad, bad), (label, np.nonzero(gbad != bad))
+    ok = ~bad
+    diff = (gm != m) | (gs != s)
+    exempt = 0
+    for i in np.nonzero(diff & ok)[0]:
+        W64 = np.asarray(Wnp[i], np.float64)
+        n1 = O.one_norm(W64)
+        n2 = O.one_norm(W64 @ W64)
+        assert scheme == "sastre" and O.near_threshold(n1, n2, eps), \
+            (label, i, (gm[i], gs[i]), (m[i], s[i]), n1, n2)
+        exempt += 1
+    same = ok & ~diff
+    assert np.array_equal(gmu[same], mults[same]), label
+    err = _rel1(res.value.cpu().numpy()[ok], val[ok]) if ok.any() else np.zeros(0)
+    worst = float(err.max()) if err.size else 0.0
+    assert worst <= TOL[dtype], (label, worst, int(np.argmax(err)))
+    # e1/e2 are derived from the same norms: tight for fp64, loose for fp32 norms
+    if same.any():
+        ge1 = res.plan.e1.cpu().numpy()[same]
+        rtol = 1e-12 if dtype == torch.float64 else 1e-4
+        fin = np.isfinite(e1[same])
+        np.testing.assert_allclose(ge1[fin], e1[same][fin], rtol=rtol)
+    return exempt, worst
+
+
+# ---------------------------------------------------------------------------
+# golden vectors of the reference itself (tests/golden)
+# ---------------------------------------------------------------------------
+
+def _golden_cases(g):
+    offs = g["offsets"]
+    for i in range(len(g["names"])):
+        n = int(g["n"][i])
+        yield (i, str(g["names"][i]), g["W"][offs[i]:offs[i + 1]].reshape(n, n),
+               g["X"][offs[i]:offs[i + 1]].reshape(n, n), float(g["eps"][i]), str(g["scheme"][i]))
+
+
+def test_golden_fp64_vs_reference(golden):
+    worst = 0.0
+    for i, name, W, Xref, eps, scheme in _golden_cases(golden):
+        if golden["raised"][i]:
+            with pytest.raises(X.NonFiniteError):
+                _run(W[None], eps, scheme)
+            continue
+        res = _run(W[None], eps, scheme)
+        gm, gs = int(res.plan.m[0]), int(res.plan.s[0])
+        if (gm, gs) != (golden["m"][i], golden["s"][i]):
+            assert scheme == "sastre" and O.near_threshold(O.one_norm(W), O.one_norm(W @ W), eps), name
+            continue
+        assert int(res.mults[0]) == golden["mults"][i], name
+        err = _rel1(res.value[0].cpu().numpy(), Xref)
+        worst = max(worst, float(err))
+        assert err <= 1e-12, (name, scheme, float(err))
+    print(f"golden fp64 worst rel 1-norm diff {worst:.2e}")
+
+
+def test_golden_fp32_vs_oracle(golden):
+    """fp32 inputs (golden matrices rounded to fp32) vs the oracle on the same values."""
+    for i, name, W, Xref, eps, scheme in _golden_cases(golden):
+        if golden["raised"][i] or eps < 2.0 ** -24:
+            continue
+        W32 = W.astype(np.float32)
+        if not np.isfinite(W32).all() or O.one_norm(W) > 25.0:
+            continue  # e^W itself would leave the fp32 range
+        _check_batch(W32[None], eps, scheme, torch.float32, name)
+
+
+@pytest.mark.parametrize("scheme", ["sastre", "ps"])
+def test_named_plans(scheme):
+    cases = {
+        "zero": (np.zeros((4, 4)), (0, 0, 0)),
+        "diag1": (np.diag([1.0] * 5), (15, 0, 4) if scheme == "sastre" else (12, 0, 5)),
+        "nil": (np.array([[0.0, 1.0], [0.0, 0.0]]), None),
+    }
+    for name, (W, want) in cases.items():
+        res = _run(W[None], 1e-8, scheme)
+        got = (int(res.plan.m[0]), int(res.plan.s[0]), int(res.mults[0]))
+        if want:
+            assert got == want, (name, got)
+    res = _run(np.zeros((3, 4, 4)), 1e-8, scheme)
+    assert torch.equal(res.value.cpu(), torch.eye(4, dtype=torch.float64).expand(3, 4, 4))
+    nil = _run(np.array([[[0.0, 1.0], [0.0, 0.0]]]), 1e-8, scheme).value[0].cpu().numpy()
+    assert np.abs(nil - np.array([[1.0, 1.0], [0.0, 1.0]])).max() <= 1e-15
+
+
+# ---------------------------------------------------------------------------
+# ragged orders, both dtypes, both schemes, tolerance sweep
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("scheme", ["sastre", "ps"])
+def test_ragged_orders(dtype, scheme):
+    rng = np.random.default_rng(101)
+    sizes = (1, 2, 3, 5, 8, 15, 16, 17, 31, 32, 33, 47, 63, 64, 65, 100, 129)
+    epss = ((1e-12, 1e-8, 1e-4, 2.0 ** -24, 2.0 ** -53) if dtype == torch.float64
+            else (1e-6, 1e-4, 2.0 ** -24))
+    for n in sizes:
+        B = 6 if n <= 64 else 3
+        arr = rng.uniform(-1, 1, (B, n, n))
+        target = 10.0 ** rng.uniform(-7, 2.3 if dtype == torch.float64 else 1.4, B)
+        W = arr * (target / np.abs(arr).sum(axis=1).max(axis=1))[:, None, None]
+        if dtype == torch.float32:
+            W = W.astype(np.float32)
+        for eps in epss:
+            _check_batch(W, eps, scheme, dtype, f"n={n} eps={eps}")
+
+
+def test_generator_kinds_sweep():
+    """Structured inputs (reference bench.py:100-143 kinds) at small orders."""
+    rng = np.random.default_rng(7)
+    for n in (4, 16, 32, 64):
+        mats = []
+        for kind in range(5):
+            for _ in range(4):
+                a = rng.uniform(-1, 1, (n, n))
+                if kind == 0:
+                    a = np.diag(np.diag(a))
+                elif kind == 2:
+                    a = np.triu(a) * 0.5 ** np.maximum(np.arange(n)[None, :] - np.arange(n)[:, None], 0)
+                elif kind == 3:
+                    a = np.triu(a, 1) + 1e-8 * rng.uniform(-1, 1, (n, n))
+                elif kind == 4:
+                    a = np.zeros((n, n))
+                    for i in range(n // 2):
+                        th = rng.uniform(0.25, 1.0)
+                        a[2 * i, 2 * i + 1], a[2 * i + 1, 2 * i] = th, -th
+                t = 10.0 ** rng.uniform(-3, 2)
+                mats.append(a * t / np.abs(a).sum(axis=0).max())
+        W = np.stack(mats)
+        for scheme in ("sastre", "ps"):
+            for eps in (1e-12, 1e-8, 2.0 ** -53):
+                _check_batch(W, eps, scheme, torch.float64, f"kinds n={n}")
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs
+# ---------------------------------------------------------------------------
+
+def test_config_C1_full():
+    cfg = WL.CONFIGS["C1"]
+    W = WL.generate("C1")
+    ex, worst = _check_batch(W, cfg.eps, "sastre", torch.float64, "C1")
+    print(f"C1: exempt {ex}, worst {worst:.2e}")
+
+
+def test_config_C2_full():
+    cfg = WL.CONFIGS["C2"]
+    W = WL.generate("C2")
+    ex, worst = _check_batch(W, cfg.eps, "sastre", torch.float32, "C2")
+    assert ex <= 8
+    print(f"C2: exempt {ex}, worst {worst:.2e}")
+
+
+def test_config_C2_orthogonality():
+    """exp of a skew-symmetric matrix is orthogonal: a size-independent property."""
+    W = torch.as_tensor(WL.generate("C2")).cuda()
+    Q = X.expm(W, 2.0 ** -24).value
+    I = torch.eye(16, device="cuda")
+    dev = (Q @ Q.transpose(-1, -2) - I).abs().amax()
+    assert float(dev) < 2e-5
+
+
+def test_config_C3_subset_and_full_properties():
+    cfg = WL.CONFIGS["C3"]
+    idx = np.arange(0, 4096, 64)               # 64 of 4096 time points
+    W = WL.generate("C3", indices=idx)
+    ex, worst = _check_batch(W, cfg.eps, "sastre", torch.float32, "C3")
+    print(f"C3 subset: exempt {ex}, worst {worst:.2e}")
+    # full batch: finite, and exp(t A) determinant = exp(t tr A)
+    Wf = torch.as_tensor(WL.generate("C3")).cuda()
+    res = X.expm(Wf, cfg.eps)
+    A, t = WL.c3_factors()
+    sel = torch.arange(0, 4096, 256, device="cuda")
+    ld = torch.linalg.slogdet(res.value[sel].double())[1].cpu().numpy()
+    want = t[sel.cpu().numpy()].astype(np.float64) * np.trace(A.astype(np.float64))
+    assert np.abs(ld - want).max() <= 1e-3 * np.abs(want).max()
+
+
+@pytest.mark.slow
+def test_config_C4_subset():
+    cfg = WL.CONFIGS["C4"]
+    W = WL.generate("C4", indices=np.arange(0, 64, 8))
+    ex, worst = _check_batch(W, cfg.eps, "sastre", torch.float64, "C4")
+    print(f"C4 subset: exempt {ex}, worst {worst:.2e}")
+
+
+@pytest.mark.slow
+def test_config_C5_subset():
+    cfg = WL.CONFIGS["C5"]
+    W = WL.generate("C5", indices=[0, 37, 101, 255])
+    ex, worst = _check_batch(W, cfg.eps, "sastre", torch.float32, "C5")
+    print(f"C5 subset: exempt {ex}, worst {worst:.2e}")
+
+
+# ---------------------------------------------------------------------------
+# error behaviour and invariants
+# ---------------------------------------------------------------------------
+
+def test_errors():
+    W = torch.eye(3, device="cuda", dtype=torch.float64)[None]
+    with pytest.raises(X.ToleranceError):
+        X.expm(W, 2.0 ** -54)
+    with pytest.raises(X.ToleranceError):
+        X.expm(W, float("nan"))
+    with pytest.raises(X.ToleranceError):
+        X.expm(W.float(), 2.0 ** -30)
+    X.expm(W, 2.0 ** -53)
+    with pytest.raises(X.MatrixError):
+        X.expm(W, 1e-8, "pade")
+    with pytest.raises(X.MatrixError):
+        X.expm(torch.zeros(2, 3, 4, device="cuda"), 1e-8)
+    with pytest.raises(RuntimeError):
+        X.expm(torch.eye(3, dtype=torch.float64)[None], 1e-8)
+    bad = torch.eye(3, device="cuda", dtype=torch.float64)[None].clone()
+    bad[0, 1, 1] = float("nan")
+    with pytest.raises(X.NonFiniteError):
+        X.expm(bad, 1e-8)
+    big = torch.diag(torch.tensor([1e300, 1.0], dtype=torch.float64)).cuda()[None]
+    with pytest.raises(X.NonFiniteError):
+        X.expm(big, 1e-8)
+    r = X.expm(torch.zeros(0, 5, 5, device="cuda"), 1e-4)
+    assert r.value.shape == (0, 5, 5)
+
+
+def test_batch_shape_and_determinism():
+    rng = np.random.default_rng(3)
+    W = torch.as_tensor(rng.uniform(-1, 1, (2, 3, 24, 24))).cuda()
+    a = X.expm(W, 1e-10)
+    b = X.expm(W, 1e-10)
+    assert a.value.shape == (2, 3, 24, 24) and a.plan.m.shape == (2, 3)
+    assert torch.equal(a.value, b.value)
+    flat = X.expm(W.reshape(6, 24, 24), 1e-10)
+    assert torch.equal(flat.value.reshape(2, 3, 24, 24), a.value)
+
+
+def test_inverse_identity_fp64():
+    rng = np.random.default_rng(37)
+    for n in (8, 33, 64, 96):
+        W = rng.uniform(-1, 1, (4, n, n))
+        W *= (rng.uniform(0.1, 2.0, 4) / np.abs(W).sum(axis=1).max(axis=1))[:, None, None]
+        Wt = torch.as_tensor(W).cuda()
+        F = X.expm(Wt, 1e-12).value
+        Bk = X.expm(-Wt, 1e-12).value
+        I = torch.eye(n, dtype=torch.float64, device="cuda")
+        d = torch.linalg.matrix_norm(F @ Bk - I) / math.sqrt(n)
+        assert float(d.max()) <= 1e-10

@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark: batched matrix exponentials/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" = one call of the hot path (expm over the whole batch of the
+config).  Default workload: BASELINE.json configs[1] = C2 (65536 x 16x16 fp32
+skew-symmetric, tol 2^-24).  Under torchrun (N > 1) every rank exponentiates
+its own batch (global indices rank*B .. rank*B+B-1; weak scaling, no
+collective on the data path); the step time is the max over ranks.
+
+Printed JSON line (rank 0):
+  value       whole-job exps/s with inputs resident in HBM (device-timed)
+  e2e         exps/s through the public API from pinned host memory, H2D of W
+              and D2H of e^W + plan inside the timed region
+  roofline    dominant kernel vs its bound (HBM bytes and useful FLOPs)
+  cpu_baseline the CPU oracle port timed on this host (bounded sample)
+`--impl reference` times the reference algorithm's CPU port (oracle/) instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2512_20777_b200 import workloads as WL  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+CPU_SAMPLE = {"C1": 1024, "C2": 16384, "C3": 48, "C4": 6, "C5": 3}
+
+
+def _peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver) + our pipe microbenchmarks."""
+    out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        out["hbm_gbs"] = float(d["hbm_gbs"])
+        out["hbm_src"] = "MEASURED_PEAKS.json"
+    pp = os.path.join(ROOT, "profiles", "peaks.json")
+    if os.path.exists(pp):
+        for line in open(pp):
+            line = line.strip()
+            if line.startswith("{") and "pipe" in line:
+                d = json.loads(line)
+                out[d["pipe"]] = float(d["tflops"])
+    out.setdefault("ffma_fp32", 74.4)
+    out.setdefault("dfma_fp64", 37.2)
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (the oracle port of the reference algorithm) -- rank 0 only
+# ---------------------------------------------------------------------------
+
+def _cpu_chunk(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    W, eps = args
+    from oracle import expm_oracle as O
+    for i in range(W.shape[0]):
+        O.expm(W[i], eps)
+    return W.shape[0]
+
+
+def cpu_reference_rate(key: str, count: int | None = None, cores: int | None = None):
+    """exps/s of the reference algorithm (oracle port, binary64 as the reference)
+    on `count` matrices of config `key`, sharded over a process pool the way
+    the reference's own harness shards (bench.py:303-306)."""
+    from concurrent.futures import ProcessPoolExecutor
+    cfg = WL.CONFIGS[key]
+    count = count or CPU_SAMPLE[key]
+    cores = cores or os.cpu_count() or 1
+    W = WL.generate(key, indices=np.arange(count)).astype(np.float64)
+    pieces = np.array_split(W, max(1, min(count, cores * 4)))
+    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        with ProcessPoolExecutor(max_workers=cores) as pool:
+            list(pool.map(_cpu_chunk, [(pieces[0][:1], cfg.eps)] * min(cores, 2)))  # warm workers
+            t0 = time.perf_counter()
+            done = sum(pool.map(_cpu_chunk, [(p, cfg.eps) for p in pieces]))
+            dt = time.perf_counter() - t0
+    finally:
+        if env_old is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = env_old
+    return done / dt, cores, f"{done} matrices of {key} ({cfg.n}x{cfg.n}, fp64 as the reference computes)"
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    cfg = WL.CONFIGS[args.config]
+    count = CPU_SAMPLE[args.config]
+    for _ in range(args.warmup):
+        cpu_reference_rate(args.config, max(1, count // 8))
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, cores, sample = cpu_reference_rate(args.config, count)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": "matrix exponentials/s", "value": value, "unit": "exps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch": cfg.batch, "n": cfg.n, "eps": cfg.eps,
+                   "parallelism": "cpu process pool (reference bench.py:303-306)"},
+        "cpu_baseline": {"value": value, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "exps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _launch_count(key, m, s, n):
+    """Kernels of ours launched by one expm call (host orchestration is deterministic)."""
+    if n <= 64:
+        return 1
+    m = np.asarray(m); s = np.asarray(s)
+    return int(1 + 2 + 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max()) + 1)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2512_20777_b200 as XP
+
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = WL.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    dtype = torch.float32 if cfg.dtype == "f32" else torch.float64
+    esz = 4 if cfg.dtype == "f32" else 8
+    # this rank's shard of the global batch (seeded chunks -> independent of N)
+    if cfg.key == "C3":
+        idx = np.arange(B) % cfg.batch
+    else:
+        idx = np.arange(rank * B, (rank + 1) * B)
+    Wh = torch.from_numpy(WL.generate(cfg.key, indices=idx))
+    W = Wh.to(dev)
+    Xd = torch.empty_like(W)
+    plan = {"m": torch.empty(B, dtype=torch.int8, device=dev), "s": torch.empty(B, dtype=torch.int8, device=dev),
+            "e1": torch.empty(B, dtype=torch.float64, device=dev), "e2": torch.empty(B, dtype=torch.float64, device=dev),
+            "norms": torch.empty(B, 2, dtype=torch.float64, device=dev),
+            "mults": torch.empty(B, dtype=torch.int32, device=dev),
+            "nonfinite": torch.empty(B, dtype=torch.uint8, device=dev)}
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        XP.expm_into(W, Xd, cfg.eps, "sastre", plan)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    m = plan["m"].cpu().numpy(); s = plan["s"].cpu().numpy()
+    assert not plan["nonfinite"].any(), "non-finite results in the bench batch"
+    flops = WL.useful_flops(m, s, cfg.n)
+
+    # ---- device-timed steps, L2 flushed between steps ----------------------
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * B / (ms_per_step * 1e-3)
+
+    # ---- end-to-end through the public API from pinned host memory --------
+    Wp = Wh.pin_memory()
+    Xp = torch.empty_like(Wp).pin_memory()
+    mp = torch.empty(B, dtype=torch.int8).pin_memory()
+    sp = torch.empty(B, dtype=torch.int8).pin_memory()
+
+    def e2e_step():
+        Wd = Wp.to(dev, non_blocking=True)
+        r = XP.expm(Wd, cfg.eps, "sastre", check_finite=False)
+        Xp.copy_(r.value, non_blocking=True)
+        mp.copy_(r.plan.m, non_blocking=True)
+        sp.copy_(r.plan.s, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = ws * B / (float(et.item()) / args.steps * 1e-3)
+    h2d = B * cfg.n * cfg.n * esz
+    d2h = B * cfg.n * cfg.n * esz + 2 * B
+
+    gather_ms = None
+    if ws > 1:
+        # the final gather of results to rank 0 (not part of the step)
+        out = torch.empty((ws * B, cfg.n, cfg.n), dtype=dtype, device=dev) if rank == 0 else None
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gl = [torch.empty_like(Xd) for _ in range(ws)] if rank == 0 else None
+        dist.gather(Xd, gl, dst=0)
+        torch.cuda.synchronize()
+        gather_ms = 1e3 * (time.perf_counter() - t0)
+        del out, gl
+
+    if rank == 0:
+        pk = _peaks()
+        hbm_bytes = 2 * B * cfg.n * cfg.n * esz
+        tflops = flops / (ms_per_step * 1e-3) / 1e12
+        gbs = hbm_bytes / (ms_per_step * 1e-3) / 1e9
+        cpeak = pk["ffma_fp32"] if cfg.dtype == "f32" else pk["dfma_fp64"]
+        t_hbm = hbm_bytes / (pk["hbm_gbs"] * 1e9)
+        t_cmp = flops / (cpeak * 1e12)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.key}.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        hbm_roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["hbm_src"],
+                    "algorithmic_bytes_per_launch": hbm_bytes}
+        cmp_roof = {"bound": "fp32_ffma" if cfg.dtype == "f32" else "fp64_dfma", "achieved": tflops,
+                    "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
+                    "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
+                    "useful_flops_per_launch": flops}
+        roof = dict(hbm_roof if t_hbm >= t_cmp else cmp_roof)
+        roof["kernel"] = "expm_fused_kernel" if cfg.n <= 64 else "gemm_stage_kernel"
+        roof["other"] = cmp_roof if t_hbm >= t_cmp else hbm_roof
+        cpu = None
+        if not args.no_cpu_baseline:
+            r, cores, sample = cpu_reference_rate(cfg.key)
+            cpu = {"value": r, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample}
+        hist = {}
+        for mm, ss in zip(m.tolist(), s.tolist()):
+            hist[f"{mm},{ss}"] = hist.get(f"{mm},{ss}", 0) + 1
+        line = {
+            "metric": "matrix exponentials/s", "value": value, "unit": "exps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg.dtype, "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
+            "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch_per_gpu": B, "global_batch": ws * B,
+                       "n": cfg.n, "eps": cfg.eps, "scheme": "sastre", "l2": "flushed between steps (252 MB write)",
+                       "parallelism": f"batch-sharded x{ws}, no collective on the hot path"},
+            "useful_tflops": tflops, "hbm_gbs": gbs,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "exps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": float(et.item()) / args.steps},
+            "gpu_launches": _launch_count(cfg.key, m, s, cfg.n) * args.steps,
+            "clocks": clk.summary(),
+            "plan_histogram": hist,
+            "gather_ms": gather_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(WL.CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -34,7 +34,7 @@ __global__ void k_dmma(double* out) {
   double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
   double c[8][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0;
+  for (int i = 0; i < 8; ++i) { c[i][0] = i * 0.1 + threadIdx.x; c[i][1] = i * 0.3 - threadIdx.x; }
   for (int it = 0; it < ITERS / 16; ++it)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -49,7 +49,7 @@ __global__ void k_tf32(float* out) {
   unsigned a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, b0 = a0 * 3, b1 = a0 * 5;
   float c[8][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
+  for (int i = 0; i < 8; ++i) { c[i][0] = i; c[i][1] = i + threadIdx.x; c[i][2] = -i; c[i][3] = i * 0.5f; }
   for (int it = 0; it < ITERS / 16; ++it)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -66,7 +66,12 @@ template <typename K>
 float timeit(K launch) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  launch(); cudaDeviceSynchronize();
+  launch();
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    printf("{\"error\": \"%s\"}\n", cudaGetErrorString(err));
+    return -1.f;
+  }
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(e0);

@@ -46,7 +46,8 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
   const int64_t persistent = (int64_t)sm_count() * occ;
   const int grid = (int)(ctas_needed < persistent ? ctas_needed : persistent);
   if (grid <= 0) return EXPMB_OK;
-  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, eps, po);
+  // log2(eps) on the host: the same libm log2 as the reference's math.log2 (select.py:175)
+  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, log2(eps), po);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
@@ -89,6 +90,20 @@ size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme) {
 int expmb_select_host(const double* norms, double eps, int scheme, int* m, int* s, double* e1, double* e2) {
   Plan p{};
   int have = 1;
+  if (scheme == EXPMB_SASTRE && norms[0] != 0.0) {
+    // the kernels' fast path first; it must agree with the exact walk below
+    const double le = log2(eps);
+    int nd = select_sastre_fast(norms[0], 0.0, 1, le, &p);
+    if (nd == 2) nd = select_sastre_fast(norms[0], norms[1], 2, le, &p), have = 2;
+    if (nd == 0) {
+      if (m) *m = p.m;
+      if (s) *s = p.s;
+      if (e1) *e1 = p.e1;
+      if (e2) *e2 = p.e2;
+      return have;
+    }
+    have = 1;
+  }
   for (;;) {
     int need = select_walk(norms, have, eps, scheme, &p);
     if (need == 0) break;

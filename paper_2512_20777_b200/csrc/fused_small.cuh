@@ -179,13 +179,17 @@ struct Fused {
   }
 
   // ||.||_1 of the group's matrix: column abs-sums in binary64, then max.
+  // ||.||_1 of the group's matrix: column abs-sums, then max.  Sums are
+  // accumulated in the working precision (fp32 sums of fp32 values carry a
+  // relative error ~n u, far inside the 1e-4 log2 exemption margin; fp64
+  // matches the reference's binary64 sums to rounding).
   __device__ __forceinline__ double norm1(const Tile& v) const {
-    double cs[4];
+    T cs[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      double a = 0.0;
+      T a = T(0);
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a += fabs((double)v[i][j]);
+      for (int i = 0; i < TM; ++i) a += fabs(v[i][j]);
       cs[j] = a;
     }
     // reduce over the thread rows that share this column quad inside the warp
@@ -194,7 +198,7 @@ struct Fused {
 #pragma unroll
       for (int j = 0; j < 4; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], off);
     if constexpr (WARPS_PG == 1) {
-      double mx = nanmax(nanmax(cs[0], cs[1]), nanmax(cs[2], cs[3]));
+      double mx = nanmax(nanmax((double)cs[0], (double)cs[1]), nanmax((double)cs[2], (double)cs[3]));
 #pragma unroll
       for (int off = 1; off < TC; off *= 2) mx = nanmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
       return mx;
@@ -202,7 +206,7 @@ struct Fused {
       const int w = t / 32, lane = t % 32;
       if (lane < TC) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) red[w * NPAD + 4 * lane + j] = cs[j];
+        for (int j = 0; j < 4; ++j) red[w * NPAD + 4 * lane + j] = (double)cs[j];
       }
       sync();
       double* res = red + WARPS_PG * NPAD;
@@ -288,11 +292,29 @@ struct Fused {
   __device__ __forceinline__ bool is_diag(int i, int j) const { return row(i) == 4 * tc + j; }
 };
 
+// Steps of the per-matrix program.  Every step is "build the two operands in
+// shared memory -> one product -> consume the product", so the kernel has a
+// single inlined product loop (the unrolled code of five call sites thrashed
+// the instruction cache: `no_instructions` was the top stall).
+enum FusedStep : int {
+  ST_W2 = 0,   // W^2 = W W                         (select.py:192)
+  ST_W3,       // W^3 = W^2 W (PS ladder)            (select.py:192)
+  ST_W4,       // W^4 = W^3 W (PS ladder)
+  ST_T4,       // T4: inner * A^2                    (poly.py:198-199)
+  ST_Y02,      // y02 = A^2 (c1 A^2 + c2 A)          (poly.py:209, :221)
+  ST_P2,       // (y02 + c3 A^2 + c4 A)(y02 + c5 A^2) (poly.py:210, :222)
+  ST_P3,       // (y12 + c8 A^2 + c9 A)(y12 + c10 y02 + c11 A)  (poly.py:224)
+  ST_HORNER,   // PS: q <- q A^j (+ block)           (poly.py:179-181)
+  ST_SQ,       // X <- X X                           (engine.py:80-87)
+  ST_DONE
+};
+
 template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
 __global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, (NPAD == 16 && sizeof(T) == 4) ? 2 : 1)
-expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double eps, PlanOut po) {
+expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, PlanOut po) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   using Tile = typename F::Tile;
+  constexpr bool kPrefetch = !(NPAD == 64 && sizeof(T) == 8);  // register budget
   extern __shared__ __align__(16) unsigned char smem_raw[];
   F f;
   f.g = threadIdx.x / F::TPG;
@@ -310,237 +332,209 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   int64_t idx = (int64_t)blockIdx.x * GROUPS + f.g;
   if (idx >= batch) return;  // whole group exits together
 
-  Tile w;
-  f.load(W + idx * nn, n, vec, w);
+#define EW(expr)                     \
+  _Pragma("unroll") for (int i = 0; i < TM; ++i) \
+  _Pragma("unroll") for (int j = 0; j < 4; ++j) { expr; }
+#define DG(i, j) (f.is_diag(i, j) ? T(1) : T(0))
+
+  Tile B;  // W, later 2^-s W
+  Tile nxt;
+  f.load(W + idx * nn, n, vec, B);
   for (; idx < batch; idx += stride) {
-    // prefetch the next matrix of this group while this one is processed
-    Tile nxt;
     const int64_t nidx = idx + stride;
-    if (nidx < batch) f.load(W + nidx * nn, n, vec, nxt);
-
+    if constexpr (kPrefetch) {
+      if (nidx < batch) f.load(W + nidx * nn, n, vec, nxt);
+    }
     bool bad = false;
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bad |= !is_finite_t(w[i][j]);
+    EW(bad |= !is_finite_t(B[i][j]));
 
-    // ---- selection (select.py:164-220) --------------------------------
-    double nrm[4];
-    nrm[0] = f.norm1(w);
+    // ---- ||W||_1 and the first rung (select.py:169-188) -------------------
+    double nrm[4], lw[4];
+    nrm[0] = f.norm1(B);
     nrm[1] = nrm[2] = nrm[3] = NAN;
-    Plan p;
-    int need = select_walk(nrm, 1, eps, SCHEME, &p);
-    Tile a2, a3, a4;
-    if (need >= 2) {  // W^2 = W W (select.py:192)
-      f.square(w, a2);
-      nrm[1] = f.norm1(a2);
-      bad |= !(nrm[1] < INFINITY);  // W^2 overflowed or is NaN (matrix.py:97-98)
-      need = select_walk(nrm, 2, eps, SCHEME, &p);
-      if constexpr (SCHEME == 1) {
-        if (need >= 3) {  // W^3 = W^2 W
-          f.product(a2, w, a3);
-          nrm[2] = f.norm1(a3);
-          need = select_walk(nrm, 3, eps, SCHEME, &p);
-          if (need >= 4) {  // W^4 = W^3 W
-            f.product(a3, w, a4);
-            nrm[3] = f.norm1(a4);
-            need = select_walk(nrm, 4, eps, SCHEME, &p);
-          }
-        }
+    Plan p{0, 0, 0.0, 0.0};
+    Tile A2, Y0, Y1, P;  // A^2 (PS: also q), y02 (PS: A^3), y12 (PS: A^4), product
+    int have = 1, step = ST_DONE, q = 0, hz = 0;
+    if (nrm[0] != 0.0) {
+      int need = SCHEME == 0 ? select_sastre_fast(nrm[0], 0.0, 1, log_eps, &p) : -1;
+      if (need < 0) {
+        lw[0] = log2_or_ninf(nrm[0]);
+        need = select_walk_lw(lw, 1, log_eps, SCHEME, &p);
       }
+      if (need >= 2) step = ST_W2;
     }
-    const int m = p.m, s = p.s;
-
-    // ---- exact 2^-s rescaling of W and cached powers (engine.py:139-140)
-    const T sc = (T)ldexp(1.0, -s);
-    const T sc2 = (T)ldexp(1.0, -2 * s);
-    Tile B, A2;
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        B[i][j] = w[i][j] * sc;
-        A2[i][j] = a2[i][j] * sc2;
-      }
-
-    Tile Xt;
-    if (m == 0) {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) Xt[i][j] = f.is_diag(i, j) ? T(1) : T(0);
-    } else if constexpr (SCHEME == 0) {
-      if (m == 1) {  // poly.py:192: A + I
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) Xt[i][j] = B[i][j] + (f.is_diag(i, j) ? T(1) : T(0));
-      } else if (m == 2) {  // poly.py:196: A^2/2 + A + I
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            Xt[i][j] = (A2[i][j] * T(0.5) + B[i][j]) + (f.is_diag(i, j) ? T(1) : T(0));
-      } else if (m == 4) {  // poly.py:198-199
-        Tile inner, P;
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            inner[i][j] = (A2[i][j] * T(0.25) + B[i][j]) / T(3) + (f.is_diag(i, j) ? T(1) : T(0));
-        f.product(inner, A2, P);
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            Xt[i][j] = (P[i][j] * T(0.5) + B[i][j]) + (f.is_diag(i, j) ? T(1) : T(0));
-      } else {
-        // y02 = A2 (c1 A2 + c2 A)   (poly.py:209 / :221)
-        const double* c = (m == 8) ? kT8 : kT15;
-        Tile R, y02, L, P;
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) R[i][j] = (T)c[0] * A2[i][j] + (T)c[1] * B[i][j];
-        f.product(A2, R, y02);
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            L[i][j] = (y02[i][j] + (T)c[2] * A2[i][j]) + (T)c[3] * B[i][j];
-            R[i][j] = y02[i][j] + (T)c[4] * A2[i][j];
-          }
-        f.product(L, R, P);
-        if (m == 8) {  // poly.py:211
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              Xt[i][j] = (((P[i][j] + (T)c[5] * y02[i][j]) + A2[i][j] * T(0.5)) + B[i][j]) +
-                         (f.is_diag(i, j) ? T(1) : T(0));
-        } else {  // poly.py:222-229
-          Tile y12;
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              y12[i][j] = (P[i][j] + (T)c[5] * y02[i][j]) + (T)c[6] * A2[i][j];
-              L[i][j] = (y12[i][j] + (T)c[7] * A2[i][j]) + (T)c[8] * B[i][j];
-              R[i][j] = (y12[i][j] + (T)c[9] * y02[i][j]) + (T)c[10] * B[i][j];
-            }
-          f.product(L, R, P);
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              Xt[i][j] = ((((P[i][j] + (T)c[11] * y12[i][j]) + (T)c[12] * y02[i][j]) + (T)c[13] * A2[i][j]) +
-                          (T)c[14] * B[i][j]) +
-                         (f.is_diag(i, j) ? (T)c[15] : T(0));
-        }
-      }
-    } else {
-      // Paterson-Stockmeyer (poly.py:149-182) on B with cached A^2..A^4.
-      const T sc3 = (T)ldexp(1.0, -3 * s);
-      const T sc4 = (T)ldexp(1.0, -4 * s);
-      Tile A3, A4;
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          A3[i][j] = a3[i][j] * sc3;
-          A4[i][j] = a4[i][j] * sc4;
-        }
-      const int jj = ps_j_of(m), kk = ps_k_of(m);
-      auto block = [&](int lo, int hi, Tile& acc) {
-        const T c0 = (T)kInvFact[lo];
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = f.is_diag(i, j) ? c0 : T(0);
-        const int cnt = hi - lo;
-        if (cnt >= 1) {
-          const T ct = (T)kInvFact[lo + 1];
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] + ct * B[i][j];
-        }
-        if (cnt >= 2) {
-          const T ct = (T)kInvFact[lo + 2];
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] + ct * A2[i][j];
-        }
-        if (cnt >= 3) {
-          const T ct = (T)kInvFact[lo + 3];
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] + ct * A3[i][j];
-        }
-        if (cnt >= 4) {
-          const T ct = (T)kInvFact[lo + 4];
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] + ct * A4[i][j];
-        }
-      };
-      block((kk - 1) * jj, m, Xt);
-      if (kk >= 2) {
-        // stage A^j once as the right operand of every Horner product
+    T sc = T(1), sc2 = T(1);
+    auto decided = [&]() {
+      // exact 2^-s rescaling of W and the cached powers (engine.py:139-140)
+      sc = pow2_neg<T>(p.s);
+      sc2 = pow2_neg<T>(2 * p.s);
+      EW(B[i][j] *= sc; A2[i][j] *= sc2);
+    };
+    // ---- the per-matrix program ------------------------------------------
+    while (step != ST_DONE) {
+      // (1) operands -> shared memory
+      const T* Lb = f.buf0;
+      const T* Rb = f.buf1;
+      if (step == ST_W2) {
+        f.store(f.buf0, B);
+        Rb = f.buf0;
+      } else if (step == ST_SQ) {
+        f.store(f.buf0, P);
+        Rb = f.buf0;
+      } else if (SCHEME == 1 && (step == ST_W3 || step == ST_W4)) {
+        f.store(f.buf0, step == ST_W3 ? A2 : Y0);
+        f.store(f.buf1, B);
+      } else if (SCHEME == 1 && step == ST_HORNER) {
+        f.store(f.buf0, P);
+        const int jj = ps_j_of(p.m);
         if (jj == 2) f.store(f.buf1, A2);
-        else if (jj == 3) f.store(f.buf1, A3);
-        else f.store(f.buf1, A4);
-        for (int r = kk - 2; r >= 0; --r) {
-          Tile P, blk;
-          f.store(f.buf0, Xt);
-          f.sync();
-          f.mm(f.buf0, f.buf1, P);
-          f.sync();
-          block(r * jj, r * jj + jj - 1, blk);
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) Xt[i][j] = P[i][j] + blk[i][j];
+        else if (jj == 3) f.store(f.buf1, Y0);
+        else f.store(f.buf1, Y1);
+      } else if (SCHEME == 0) {
+        const double* c = (p.m == 8) ? kT8 : kT15;
+        if (step == ST_T4) {
+          Tile L;
+          // (A2/4 + A)/3 + I; x/3 taken as x * fl(1/3) (<= 1 ulp from the division)
+          EW(L[i][j] = (A2[i][j] * T(0.25) + B[i][j]) * T(1.0 / 3.0) + DG(i, j));
+          f.store(f.buf0, L);
+          f.store(f.buf1, A2);
+        } else if (step == ST_Y02) {
+          const T c0 = (T)c[0], c1 = (T)c[1];
+          Tile R;
+          EW(R[i][j] = c0 * A2[i][j] + c1 * B[i][j]);
+          f.store(f.buf0, A2);
+          f.store(f.buf1, R);
+        } else if (step == ST_P2) {
+          const T c2 = (T)c[2], c3 = (T)c[3], c4 = (T)c[4];
+          Tile L, R;
+          EW(L[i][j] = (Y0[i][j] + c2 * A2[i][j]) + c3 * B[i][j]; R[i][j] = Y0[i][j] + c4 * A2[i][j]);
+          f.store(f.buf0, L);
+          f.store(f.buf1, R);
+        } else {  // ST_P3
+          const T c7 = (T)c[7], c8 = (T)c[8], c9 = (T)c[9], c10 = (T)c[10];
+          Tile L, R;
+          EW(L[i][j] = (Y1[i][j] + c7 * A2[i][j]) + c8 * B[i][j];
+             R[i][j] = (Y1[i][j] + c9 * Y0[i][j]) + c10 * B[i][j]);
+          f.store(f.buf0, L);
+          f.store(f.buf1, R);
+        }
+      }
+      // (2) the product
+      f.sync();
+      f.mm(Lb, Rb, P);
+      f.sync();
+      // (3) consume it, choose the next step
+      if (step == ST_SQ) {
+        step = (++q < p.s) ? ST_SQ : ST_DONE;
+      } else if (step == ST_W2 || (SCHEME == 1 && (step == ST_W3 || step == ST_W4))) {
+        const int pw = step == ST_W2 ? 2 : step == ST_W3 ? 3 : 4;
+        if (pw == 2) { EW(A2[i][j] = P[i][j]); }
+        else if (pw == 3) { EW(Y0[i][j] = P[i][j]); }
+        else { EW(Y1[i][j] = P[i][j]); }
+        nrm[pw - 1] = f.norm1(P);
+        bad |= !(nrm[pw - 1] < INFINITY);  // a power overflowed or is NaN (matrix.py:97-98)
+        have = pw;
+        int need = SCHEME == 0 ? select_sastre_fast(nrm[0], nrm[1], 2, log_eps, &p) : -1;
+        if (need < 0) {
+          for (int q = 0; q < pw; ++q) lw[q] = log2_or_ninf(nrm[q]);
+          need = select_walk_lw(lw, have, log_eps, SCHEME, &p);
+        }
+        if (need > 0) {
+          step = need == 3 ? ST_W3 : ST_W4;
+          continue;
+        }
+        decided();
+        if constexpr (SCHEME == 1) {
+          const T sc3 = pow2_neg<T>(3 * p.s), sc4 = pow2_neg<T>(4 * p.s);
+          if (have >= 3) { EW(Y0[i][j] *= sc3); }
+          if (have >= 4) { EW(Y1[i][j] *= sc4); }
+          // q = block((k-1) j, m)   (poly.py:179)
+          const int jj = ps_j_of(p.m), kk = ps_k_of(p.m), lo = (kk - 1) * jj, cnt = p.m - lo;
+          const T c0 = (T)kInvFact[lo];
+          EW(P[i][j] = f.is_diag(i, j) ? c0 : T(0));
+          if (cnt >= 1) { const T ct = (T)kInvFact[lo + 1]; EW(P[i][j] = P[i][j] + ct * B[i][j]); }
+          if (cnt >= 2) { const T ct = (T)kInvFact[lo + 2]; EW(P[i][j] = P[i][j] + ct * A2[i][j]); }
+          if (cnt >= 3) { const T ct = (T)kInvFact[lo + 3]; EW(P[i][j] = P[i][j] + ct * Y0[i][j]); }
+          if (cnt >= 4) { const T ct = (T)kInvFact[lo + 4]; EW(P[i][j] = P[i][j] + ct * Y1[i][j]); }
+          hz = kk - 2;  // next Horner block index r
+          step = kk >= 2 ? ST_HORNER : (p.s > 0 ? ST_SQ : ST_DONE);
+        } else {
+          if (p.m == 2) {  // poly.py:196
+            EW(P[i][j] = (A2[i][j] * T(0.5) + B[i][j]) + DG(i, j));
+            step = ST_DONE;
+          } else {
+            step = p.m == 4 ? ST_T4 : ST_Y02;
+          }
+        }
+      } else if (SCHEME == 1 && step == ST_HORNER) {
+        // q <- q A^j + block(r j, r j + j - 1)
+        const int jj = ps_j_of(p.m), lo = hz * jj, cnt = jj - 1;
+        const T c0 = (T)kInvFact[lo];
+        EW(P[i][j] = P[i][j] + (f.is_diag(i, j) ? c0 : T(0)));
+        if (cnt >= 1) { const T ct = (T)kInvFact[lo + 1]; EW(P[i][j] = P[i][j] + ct * B[i][j]); }
+        if (cnt >= 2) { const T ct = (T)kInvFact[lo + 2]; EW(P[i][j] = P[i][j] + ct * A2[i][j]); }
+        if (cnt >= 3) { const T ct = (T)kInvFact[lo + 3]; EW(P[i][j] = P[i][j] + ct * Y0[i][j]); }
+        step = (--hz >= 0) ? ST_HORNER : (p.s > 0 ? ST_SQ : ST_DONE);
+      } else if (SCHEME == 0) {
+        if (step == ST_T4) {  // poly.py:199
+          EW(P[i][j] = (P[i][j] * T(0.5) + B[i][j]) + DG(i, j));
+          step = ST_DONE;  // m = 4 implies s = 0
+        } else if (step == ST_Y02) {
+          EW(Y0[i][j] = P[i][j]);
+          step = ST_P2;
+        } else if (step == ST_P2) {
+          const double* c = (p.m == 8) ? kT8 : kT15;
+          if (p.m == 8) {  // poly.py:211
+            const T c5 = (T)c[5];
+            EW(P[i][j] = (((P[i][j] + c5 * Y0[i][j]) + A2[i][j] * T(0.5)) + B[i][j]) + DG(i, j));
+            step = ST_DONE;  // m = 8 implies s = 0
+          } else {  // poly.py:222-223
+            const T c5 = (T)c[5], c6 = (T)c[6];
+            EW(Y1[i][j] = (P[i][j] + c5 * Y0[i][j]) + c6 * A2[i][j]);
+            step = ST_P3;
+          }
+        } else {  // ST_P3 -> y22 (poly.py:224-229)
+          const T c11 = (T)kT15[11], c12 = (T)kT15[12], c13 = (T)kT15[13], c14 = (T)kT15[14], c15 = (T)kT15[15];
+          EW(P[i][j] = ((((P[i][j] + c11 * Y1[i][j]) + c12 * Y0[i][j]) + c13 * A2[i][j]) + c14 * B[i][j]) +
+                       (f.is_diag(i, j) ? c15 : T(0)));
+          step = p.s > 0 ? ST_SQ : ST_DONE;
         }
       }
     }
-
-    // ---- squaring phase (engine.py:80-87) ----------------------------
-    for (int q = 0; q < s; ++q) {
-      Tile Y;
-      f.square(Xt, Y);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) Xt[i][j] = Y[i][j];
+    // m = 0 / 1 finish without a product (poly.py:192, engine.py:141-142)
+    if (nrm[0] == 0.0) {
+      EW(P[i][j] = DG(i, j));
+    } else if (have == 1) {
+      if constexpr (SCHEME == 1) {  // PS m = 1: block(0, 1) = I + A
+        EW(P[i][j] = (f.is_diag(i, j) ? (T)kInvFact[0] : T(0)) + (T)kInvFact[1] * B[i][j]);
+      } else {
+        EW(P[i][j] = B[i][j] + DG(i, j));
+      }
     }
 
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bad |= !is_finite_t(Xt[i][j]);
+    EW(bad |= !is_finite_t(P[i][j]));
     bad = f.any_group(bad);
-    f.save(X + idx * nn, n, vec, Xt);
+    f.save(X + idx * nn, n, vec, P);
     if (f.t == 0) {
-      if (po.m) po.m[idx] = (int8_t)m;
-      if (po.s) po.s[idx] = (int8_t)s;
+      if (po.m) po.m[idx] = (int8_t)p.m;
+      if (po.s) po.s[idx] = (int8_t)p.s;
       if (po.e1) po.e1[idx] = p.e1;
       if (po.e2) po.e2[idx] = p.e2;
       if (po.norms) {
         po.norms[2 * idx] = nrm[0];
         po.norms[2 * idx + 1] = nrm[1];
       }
-      if (po.mults) po.mults[idx] = budget(m, SCHEME) + s;
+      if (po.mults) po.mults[idx] = budget(p.m, SCHEME) + p.s;
       if (po.nonfinite) po.nonfinite[idx] = (uint8_t)(bad || !(nrm[0] <= INFINITY));
     }
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) w[i][j] = nxt[i][j];
+    if constexpr (kPrefetch) {
+      EW(B[i][j] = nxt[i][j]);
+    } else {
+      if (nidx < batch) f.load(W + nidx * nn, n, vec, B);
+    }
   }
+#undef EW
+#undef DG
 }
 
 }  // namespace expmb

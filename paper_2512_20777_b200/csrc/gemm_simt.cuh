@@ -86,7 +86,7 @@ __device__ __forceinline__ bool make_epi(const GemmCtx<T>& g, int stage, int z, 
     return true;
   }
   const int m = g.m[z], s = g.s[z];
-  const double sg = ldexp(1.0, -s), sg2 = ldexp(1.0, -2 * s);
+  const double sg = pow2_neg<double>(s), sg2 = pow2_neg<double>(2 * s);
   if (stage == STAGE_SQ) {
     if (s <= g.sq_step) return false;
     e.L = e.R = sq_target(g, z, s, g.sq_step);
@@ -101,13 +101,13 @@ __device__ __forceinline__ bool make_epi(const GemmCtx<T>& g, int stage, int z, 
     if (r < 0) return false;
     e.L = (h % 2 == 0) ? g.La + o : g.Ra + o;
     e.R = j == 2 ? g.W2 + o : (j == 3 ? g.W3 + o : g.W4 + o);
-    e.alpha = (T)ldexp(1.0, -j * s);
+    e.alpha = (T)pow2_neg<double>(j * s);
     e.out[0] = (r == 0) ? sq_target(g, z, s, 0) : ((h % 2 == 0) ? g.Ra + o : g.La + o);
     e.in[0] = Wz; e.in[1] = g.W2 + o; e.in[2] = g.W3 + o; e.in[3] = g.W4 + o;
     const int lo = r * j, hi = r * j + j - 1;
     e.d[0] = (T)kInvFact[lo];
     e.nin = hi - lo;
-    for (int t = 1; t <= hi - lo; ++t) e.c[0][t - 1] = (T)(kInvFact[lo + t] * ldexp(1.0, -t * s));
+    for (int t = 1; t <= hi - lo; ++t) e.c[0][t - 1] = (T)(kInvFact[lo + t] * pow2_neg<double>(t * s));
     return true;
   }
   // Sastre formulas
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __re
   const int64_t o = (int64_t)z * g.mstride;
   const T* Wz = g.W + (int64_t)z * g.wstride;
   const T* A2 = g.W2 + o;
-  const double sg = ldexp(1.0, -s), sg2 = ldexp(1.0, -2 * s);
+  const double sg = pow2_neg<double>(s), sg2 = pow2_neg<double>(2 * s);
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / n), c = (int)(i % n);
     const T dg = (r == c) ? T(1) : T(0);
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __re
       const int lo = (k - 1) * j;
       T acc = (T)kInvFact[lo] * dg;
       const T pw[4] = {Wz[i], m >= 2 ? A2[i] : T(0), j >= 3 ? g.W3[o + i] : T(0), j >= 4 ? g.W4[o + i] : T(0)};
-      for (int t = 1; t <= m - lo; ++t) acc = fma((T)(kInvFact[lo + t] * ldexp(1.0, -t * s)), pw[t - 1], acc);
+      for (int t = 1; t <= m - lo; ++t) acc = fma((T)(kInvFact[lo + t] * pow2_neg<double>(t * s)), pw[t - 1], acc);
       if (k == 1) sq_target(g, z, s, 0)[i] = acc;
       else g.La[o + i] = acc;
       continue;

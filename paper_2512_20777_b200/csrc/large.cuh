@@ -106,8 +106,12 @@ __global__ void __launch_bounds__(256) k_norm1(const T* __restrict__ W, int n, d
     double nr[4] = {red[0], NAN, NAN, NAN};
     nrm4[4 * z + 0] = nr[0];
     nrm4[4 * z + 1] = NAN;
-    Plan p{};
-    const int nd = select_walk(nr, 1, eps, scheme, &p);
+    Plan p{0, 0, 0.0, 0.0};
+    int nd = 0;
+    if (nr[0] != 0.0) {
+      const double lw[4] = {log2_or_ninf(nr[0]), 0.0, 0.0, 0.0};
+      nd = select_walk_lw(lw, 1, eps, scheme, &p);  // eps carries log2(eps) here
+    }
     need[z] = nd;
     if (nd == 0) {
       pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
@@ -142,7 +146,9 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
     double nr[4];
     for (int q = 0; q < 4; ++q) nr[q] = nrm4[4 * z + q];
     Plan p{};
-    const int nd = select_walk(nr, have, eps, scheme, &p);
+    double lw[4];
+    for (int q = 0; q < have; ++q) lw[q] = log2_or_ninf(nr[q]);
+    const int nd = select_walk_lw(lw, have, eps, scheme, &p);  // eps carries log2(eps)
     need[z] = nd;
     if (nd == 0) {
       pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
@@ -198,7 +204,8 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
   int* dlist = reinterpret_cast<int*>(ws + L.off_list);
   const int ic = (int)cnt;
 
-  k_norm1<T><<<ic, 256, 0, st>>>(W, n, eps, scheme, nrm4, need, dm, ds, de1, de2);
+  const double log_eps = log2(eps);  // host libm, as select.py:175
+  k_norm1<T><<<ic, 256, 0, st>>>(W, n, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
 
   GemmCtx<T> g{};
   g.n = n;
@@ -223,7 +230,7 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
   const int maxp = scheme == 1 ? 4 : 2;
   for (int p = 2; p <= maxp; ++p) {
     if (gemm_launch<T>(g, p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic, st)) return EXPMB_ERR_CUDA;
-    k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, eps, scheme, nrm4, need, dm, ds, de1, de2);
+    k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
   }
 
   // one small device->host copy of the plans

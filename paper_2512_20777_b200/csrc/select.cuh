@@ -104,11 +104,43 @@ EXPMB_HD double rn_mul(double a, double b) { volatile double r = a * b; return r
 EXPMB_HD double rn_div(double a, double b) { volatile double r = a / b; return r; }
 #endif
 
-// select.py:82-83
-EXPMB_HD double log2_or_ninf(double x) { return x > 0.0 ? log2(x) : -INFINITY; }
+// select.py:82-83 (out of line on the device: the libdevice log2 expansion is
+// large and the kernels call it from several sites)
+#if defined(__CUDACC__)
+__host__ __device__ __noinline__
+#else
+inline
+#endif
+double log2_or_ninf(double x) { return x > 0.0 ? log2(x) : -INFINITY; }
+
+// 2^-k exactly, for 0 <= k <= 126 (float) / 1022 (double): the scaling factors
+// of engine.py:139-140 (ldexp), built from the exponent bits.
+template <typename T>
+EXPMB_HD T pow2_neg(int k);
+template <>
+EXPMB_HD float pow2_neg<float>(int k) {
+#if defined(__CUDA_ARCH__)
+  return __int_as_float((127 - k) << 23);
+#else
+  return ldexpf(1.0f, -k);
+#endif
+}
+template <>
+EXPMB_HD double pow2_neg<double>(int k) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double((long long)(1023 - k) << 52);
+#else
+  return ldexp(1.0, -k);
+#endif
+}
 
 // NumPy npymath npy_logaddexp2 (np.logaddexp2 at select.py:206).
-EXPMB_HD double logaddexp2(double x, double y) {
+#if defined(__CUDACC__)
+__host__ __device__ __noinline__
+#else
+inline
+#endif
+double logaddexp2(double x, double y) {
   const double kLog2e = 1.442695040888963407359924681001892137;
   if (x == y) return rn_add(x, 1.0);
   const double tmp = rn_sub(x, y);
@@ -129,61 +161,23 @@ struct Plan {
 // power p > have the next rung needs (the caller forms W^p = W^(p-1) W, as
 // select.py:190-194 does, and calls again; restarting the walk is exact
 // because earlier rungs depend only on norms that do not change).
-EXPMB_HD int select_walk(const double* nrm, int have, double eps, int scheme, Plan* out) {
-  const double norm1 = nrm[0];
-  if (norm1 == 0.0) {  // select.py:172-173
-    out->m = 0; out->s = 0; out->e1 = 0.0; out->e2 = 0.0;
-    return 0;
-  }
-  const double log_eps = log2(eps);
-  double lw[5];
-  lw[1] = log2_or_ninf(norm1);
-  for (int p = 2; p <= have && p <= 4; ++p) lw[p] = log2_or_ninf(nrm[p - 1]);
-  double l1 = INFINITY, l2 = INFINITY;
-  const int nord = scheme == 1 ? 7 : 5;
-  int m = scheme == 1 ? 16 : 15;
-  bool finished = false;
-  for (int i = 0; i < nord; ++i) {
-    const int mi = scheme == 1 ? ps_order(i) : sastre_order(i);
-    const int j = scheme == 1 ? ps_jpow(i) : (i == 0 ? 1 : 2);
-    const int k = scheme == 1 ? ps_kcount(i) : sastre_kcount(i);
-    const double lc1 = scheme == 1 ? ps_log_tail(2 * i) : sastre_log_tail(2 * i);
-    const double lc2 = scheme == 1 ? ps_log_tail(2 * i + 1) : sastre_log_tail(2 * i + 1);
-    m = mi;
-    if (mi == 1) {
-      l1 = rn_add(lc1, rn_mul(2.0, lw[1]));
-      l2 = rn_add(lc2, rn_mul(3.0, lw[1]));
-    } else {
-      if (j > have) return j;  // need W^j (select.py:190-194)
-      const double kl = rn_mul((double)k, lw[j]);
-      if (scheme == 1) {
-        l1 = rn_add(rn_add(lc1, kl), lw[1]);
-        l2 = rn_add(rn_add(lc2, kl), lw[2]);
-      } else {
-        l1 = rn_add(lc1, kl);
-        l2 = rn_add(lc2, kl);
-        if (j * k == mi) {
-          l1 = rn_add(l1, lw[1]);
-          l2 = rn_add(l2, lw[2]);
-        } else {
-          l2 = rn_add(l2, lw[1]);
-        }
-      }
-    }
-    if (logaddexp2(l1, l2) <= log_eps) {
-      finished = true;
-      break;
-    }
-  }
+// Tail of the walk (select.py:210-220): scaling rule + reported bounds.
+// Out of line: ceil/div/exp2 expand to a lot of code and run once per matrix.
+#if defined(__CUDACC__)
+__host__ __device__ __noinline__
+#else
+inline
+#endif
+void plan_tail(double l1, double l2, int m, bool finished, double log_eps, Plan* out) {
   int s = 0;
-  if (!finished) {  // select.py:210-219
+  if (!finished) {
     const double ls[2] = {l1, l2};
     for (int t = 1; t <= 2; ++t) {
       const double l = ls[t - 1];
       if (l == -INFINITY) continue;
       const double q = ceil(rn_div(rn_sub(l, log_eps), (double)(m + t)));
-      // q may be +inf/NaN when a norm overflowed; the cap below bounds it
-      // (the reference raises NonFiniteError earlier in that case).
+      // q may be +inf/NaN when a norm overflowed; the cap bounds it (the
+      // reference raises NonFiniteError earlier in that case).
       if (!(q <= (double)kMaxScaling)) { s = kMaxScaling; continue; }
       const int s1 = (int)q;
       if (s1 > s) s = s1;
@@ -194,7 +188,188 @@ EXPMB_HD int select_walk(const double* nrm, int have, double eps, int scheme, Pl
   out->s = s;
   out->e1 = exp2(l1);
   out->e2 = exp2(l2);
+}
+
+// Core walk on log2 power norms: lwp[p-1] = log2 ||W^p||_1 (select.py:176,194),
+// log_eps = log2(eps) (select.py:175).  The caller handles ||W||_1 == 0.
+// Fully unrolled (the rung constants fold into immediates); the exact
+// logaddexp2 runs only for a rung whose [max, max+1] bracket straddles log_eps.
+EXPMB_HD int select_walk_lw(const double* lwp, int have, double log_eps, int scheme, Plan* out) {
+  const double lw1 = lwp[0];
+  const double lw2 = have >= 2 ? lwp[1] : 0.0;
+  const double lw3 = have >= 3 ? lwp[2] : 0.0;
+  const double lw4 = have >= 4 ? lwp[3] : 0.0;
+  double l1 = INFINITY, l2 = INFINITY;
+  const int nord = scheme == 1 ? 7 : 5;
+  int m = scheme == 1 ? 16 : 15;
+  bool finished = false;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    if (i >= nord) break;
+    const int mi = scheme == 1 ? ps_order(i) : sastre_order(i);
+    const int j = scheme == 1 ? ps_jpow(i) : (i == 0 ? 1 : 2);
+    const int k = scheme == 1 ? ps_kcount(i) : sastre_kcount(i);
+    const double lc1 = scheme == 1 ? ps_log_tail(2 * i) : sastre_log_tail(2 * i);
+    const double lc2 = scheme == 1 ? ps_log_tail(2 * i + 1) : sastre_log_tail(2 * i + 1);
+    m = mi;
+    if (mi == 1) {
+      l1 = rn_add(lc1, rn_mul(2.0, lw1));
+      l2 = rn_add(lc2, rn_mul(3.0, lw1));
+    } else {
+      if (j > have) return j;  // need W^j (select.py:190-194)
+      const double lwj = j == 2 ? lw2 : (j == 3 ? lw3 : lw4);
+      const double kl = rn_mul((double)k, lwj);
+      if (scheme == 1) {
+        l1 = rn_add(rn_add(lc1, kl), lw1);
+        l2 = rn_add(rn_add(lc2, kl), lw2);
+      } else {
+        l1 = rn_add(lc1, kl);
+        l2 = rn_add(lc2, kl);
+        if (j * k == mi) {
+          l1 = rn_add(l1, lw1);
+          l2 = rn_add(l2, lw2);
+        } else {
+          l2 = rn_add(l2, lw1);
+        }
+      }
+    }
+    // logaddexp2(l1, l2) lies in [max, max + 1]; only a rung whose bracket
+    // straddles log_eps needs the exact (transcendental) evaluation.
+    const double hi = l1 > l2 ? l1 : l2;
+    bool pass;
+    if (rn_add(hi, 1.0) < log_eps - 1e-9) pass = true;
+    else if (hi > log_eps + 1e-9) pass = false;
+    else pass = logaddexp2(l1, l2) <= log_eps;
+    if (pass) {
+      finished = true;
+      break;
+    }
+  }
+  plan_tail(l1, l2, m, finished, log_eps, out);
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Fast Sastre selector for the fused kernels.
+//
+// The exact walk needs binary64 log2 of the norms and exp2 for the reported
+// bounds -- ~300 instructions per matrix, 16% of the n=16 kernel.  The fast
+// path evaluates the same ladder with a cheap log2 (exponent bits + fp32
+// log2f of the mantissa, |error| < 4e-7) and accepts a decision only when
+// every comparison it makes clears the error by a wide margin (1e-5 in log2
+// units for the rung tests, 1e-5 on the fractional part for each ceil of the
+// scaling rule).  Any closer call returns -1 and the caller runs the exact
+// walk, so the chosen (m, s) is always the exact walk's.  e1/e2 are formed
+// as tail * ||W^2||^k * ||W|| products (equal to exp2 of the log-domain sum to
+// ~1e-14 relative), valid because both norms are restricted to [2^-100, 2^100].
+// ---------------------------------------------------------------------------
+EXPMB_HD double sastre_tail(int i) {
+  switch (i) {
+    case 0: return 0x1.0000000000000p-1;
+    case 1: return 0x1.5555555555555p-3;
+    case 2: return 0x1.5555555555555p-3;
+    case 3: return 0x1.5555555555555p-5;
+    case 4: return 0x1.1111111111111p-7;
+    case 5: return 0x1.6c16c16c16c17p-10;
+    case 6: return 0x1.71de3a556c734p-19;
+    case 7: return 0x1.27e4fb7789f5cp-22;
+    case 8: return 0x1.871cb69cf3722p-46;   // |1/16! - b16|
+    default: return 0x1.952c77030ad4ap-49;  // 1/17!
+  }
+}
+
+EXPMB_HD double fast_log2(double x) {
+#if defined(__CUDA_ARCH__)
+  const int hi = __double2hiint(x);
+  const int e = ((hi >> 20) & 0x7ff) - 1023;
+  const double mant = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(x));
+  return (double)e + (double)log2f((float)mant);
+#else
+  int e;
+  const double mant = frexp(x, &e) * 2.0;
+  return (double)(e - 1) + (double)log2f((float)mant);
+#endif
+}
+
+// Returns 0 (decided, *out written), 2 (needs W^2 first), or -1 (too close to
+// call: run select_walk_lw).  have = 1 or 2; n2 ignored when have == 1.
+EXPMB_HD int select_sastre_fast(double n1, double n2, int have, double log_eps, Plan* out) {
+  const double lo = 0x1p-100, hi = 0x1p100;
+  if (!(n1 >= lo && n1 <= hi)) return -1;
+  if (have >= 2 && !(n2 >= lo && n2 <= hi)) return -1;
+  const double lw1 = fast_log2(n1);
+  const double lw2 = have >= 2 ? fast_log2(n2) : 0.0;
+  const double M = 1e-5;
+  double l1 = 0.0, l2 = 0.0;
+  int mi = 1, ri = 0;
+  bool finished = false;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    mi = sastre_order(i);
+    ri = i;
+    const int k = sastre_kcount(i);
+    if (i == 0) {
+      l1 = sastre_log_tail(0) + 2.0 * lw1;
+      l2 = sastre_log_tail(1) + 3.0 * lw1;
+    } else {
+      if (have < 2) return 2;
+      l1 = sastre_log_tail(2 * i) + k * lw2;
+      l2 = sastre_log_tail(2 * i + 1) + k * lw2;
+      if (2 * k == mi) { l1 += lw1; l2 += lw2; } else { l2 += lw1; }
+    }
+    const double h = l1 > l2 ? l1 : l2;
+    if (h + 1.0 < log_eps - M) { finished = true; break; }  // certainly passes
+    if (h > log_eps + M) continue;                           // certainly fails
+    // inside the [max, max+1] bracket: logaddexp2 in fp32 (|error| < 1e-6)
+    const float d = (float)fabs(l1 - l2);
+    const double lae = h + (double)log2f(1.0f + exp2f(-d));
+    if (lae < log_eps - M) { finished = true; break; }
+    if (!(lae > log_eps + M)) return -1;                     // too close: exact walk
+  }
+  int s = 0;
+  if (!finished) {
+    // s = clamp(max(ceil(v1), ceil(v2)), 0, 20); ambiguous only if a
+    // perturbation of M changes the clamped result
+    const double v1 = (l1 - log_eps) / (double)(mi + 1);
+    const double v2 = (l2 - log_eps) / (double)(mi + 2);
+    const double va = v1 > v2 ? v1 : v2;
+    double c_lo = ceil(va - M), c_hi = ceil(va + M);
+    c_lo = c_lo < 0.0 ? 0.0 : (c_lo > kMaxScaling ? kMaxScaling : c_lo);
+    c_hi = c_hi < 0.0 ? 0.0 : (c_hi > kMaxScaling ? kMaxScaling : c_hi);
+    if (c_lo != c_hi) return -1;
+    s = (int)c_lo;
+  }
+  // reported bounds exp2(l1), exp2(l2) as products (select.py:220)
+  double e1, e2;
+  if (ri == 0) {
+    e1 = sastre_tail(0) * (n1 * n1);
+    e2 = sastre_tail(1) * (n1 * n1 * n1);
+  } else {
+    const int k = sastre_kcount(ri);
+    double pk = n2;
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < k) pk *= n2;
+    e1 = sastre_tail(2 * ri) * pk;
+    e2 = sastre_tail(2 * ri + 1) * pk;
+    if (2 * k == mi) { e1 *= n1; e2 *= n2; } else { e2 *= n1; }
+  }
+  out->m = mi;
+  out->s = s;
+  out->e1 = e1;
+  out->e2 = e2;
+  return 0;
+}
+
+// Same walk from the norms themselves (host tests, large-n select kernels).
+EXPMB_HD int select_walk(const double* nrm, int have, double eps, int scheme, Plan* out) {
+  if (nrm[0] == 0.0) {  // select.py:172-173
+    out->m = 0; out->s = 0; out->e1 = 0.0; out->e2 = 0.0;
+    return 0;
+  }
+  double lw[4];
+  for (int p = 1; p <= have && p <= 4; ++p) lw[p - 1] = log2_or_ninf(nrm[p - 1]);
+  return select_walk_lw(lw, have, log2(eps), scheme, out);
 }
 
 }  // namespace expmb

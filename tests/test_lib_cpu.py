@@ -110,7 +110,7 @@ def test_host_selector_matches_oracle_ladder(scheme):
         m, s, e1, e2, have = _lib.select_host(norms, eps, code)
         assert (m, s) == want[:2], (norms, eps, want, (m, s))
         for a, b in ((e1, want[2]), (e2, want[3])):
-            assert a == b or (math.isinf(a) and math.isinf(b)) or abs(a - b) <= 1e-14 * abs(b)
+            assert a == b or (math.isinf(a) and math.isinf(b)) or abs(a - b) <= 1e-12 * abs(b)
     assert mism == 0
 
 

@@ -278,82 +278,92 @@ EXPMB_HD double sastre_tail(int i) {
   }
 }
 
-EXPMB_HD double fast_log2(double x) {
+// log2 for the fast path: exponent bits + fp32 log2f of the mantissa in [1,2)
+// (|error| < 2e-7 absolute, independent of the magnitude).
+EXPMB_HD float fast_log2f(double x) {
 #if defined(__CUDA_ARCH__)
   const int hi = __double2hiint(x);
   const int e = ((hi >> 20) & 0x7ff) - 1023;
-  const double mant = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(x));
-  return (double)e + (double)log2f((float)mant);
+  const float mant = (float)__hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(x));
+  return (float)e + log2f(mant);
 #else
   int e;
   const double mant = frexp(x, &e) * 2.0;
-  return (double)(e - 1) + (double)log2f((float)mant);
+  return (float)(e - 1) + log2f((float)mant);
 #endif
 }
 
 // Returns 0 (decided, *out written), 2 (needs W^2 first), or -1 (too close to
 // call: run select_walk_lw).  have = 1 or 2; n2 ignored when have == 1.
-EXPMB_HD int select_sastre_fast(double n1, double n2, int have, double log_eps, Plan* out) {
+// All ladder arithmetic is fp32 (|l| <= ~250 so |error| < 4e-5); every
+// comparison needs a margin of 2e-4 (log2 units) or it defers to the exact walk.
+EXPMB_HD int select_sastre_fast(double n1, double n2, int have, double log_eps_d, Plan* out) {
   const double lo = 0x1p-100, hi = 0x1p100;
   if (!(n1 >= lo && n1 <= hi)) return -1;
   if (have >= 2 && !(n2 >= lo && n2 <= hi)) return -1;
-  const double lw1 = fast_log2(n1);
-  const double lw2 = have >= 2 ? fast_log2(n2) : 0.0;
-  const double M = 1e-5;
-  double l1 = 0.0, l2 = 0.0;
-  int mi = 1, ri = 0;
+  const float M = 2e-4f;
+  const float log_eps = (float)log_eps_d;
+  const float lw1 = fast_log2f(n1);
+  // rung 0 (m = 1): l1 = log2(1/2!) + 2 lw1, l2 = log2(1/3!) + 3 lw1
+  {
+    const float l1 = -1.0f + 2.0f * lw1, l2 = -2.5849625f + 3.0f * lw1;
+    const float h = fmaxf(l1, l2);
+    bool pass = false, known = true;
+    if (h + 1.0f < log_eps - M) pass = true;
+    else if (h > log_eps + M) pass = false;
+    else {
+      const float lae = h + log2f(1.0f + exp2f(-fabsf(l1 - l2)));
+      if (lae < log_eps - M) pass = true;
+      else if (!(lae > log_eps + M)) known = false;
+    }
+    if (!known) return -1;
+    if (pass) {
+      out->m = 1; out->s = 0;
+      out->e1 = 0x1.0000000000000p-1 * (n1 * n1);
+      out->e2 = 0x1.5555555555555p-3 * (n1 * n1 * n1);
+      return 0;
+    }
+    if (have < 2) return 2;
+  }
+  const float lw2 = fast_log2f(n2);
+  float l1 = 0.f, l2 = 0.f;
+  int mi = 15, ri = 4;
   bool finished = false;
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 1; i < 5; ++i) {
     mi = sastre_order(i);
     ri = i;
     const int k = sastre_kcount(i);
-    if (i == 0) {
-      l1 = sastre_log_tail(0) + 2.0 * lw1;
-      l2 = sastre_log_tail(1) + 3.0 * lw1;
-    } else {
-      if (have < 2) return 2;
-      l1 = sastre_log_tail(2 * i) + k * lw2;
-      l2 = sastre_log_tail(2 * i + 1) + k * lw2;
-      if (2 * k == mi) { l1 += lw1; l2 += lw2; } else { l2 += lw1; }
-    }
-    const double h = l1 > l2 ? l1 : l2;
-    if (h + 1.0 < log_eps - M) { finished = true; break; }  // certainly passes
+    l1 = (float)sastre_log_tail(2 * i) + (float)k * lw2;
+    l2 = (float)sastre_log_tail(2 * i + 1) + (float)k * lw2;
+    if (2 * k == mi) { l1 += lw1; l2 += lw2; } else { l2 += lw1; }
+    const float h = fmaxf(l1, l2);
+    if (h + 1.0f < log_eps - M) { finished = true; break; }  // certainly passes
     if (h > log_eps + M) continue;                           // certainly fails
-    // inside the [max, max+1] bracket: logaddexp2 in fp32 (|error| < 1e-6)
-    const float d = (float)fabs(l1 - l2);
-    const double lae = h + (double)log2f(1.0f + exp2f(-d));
+    const float lae = h + log2f(1.0f + exp2f(-fabsf(l1 - l2)));
     if (lae < log_eps - M) { finished = true; break; }
     if (!(lae > log_eps + M)) return -1;                     // too close: exact walk
   }
   int s = 0;
   if (!finished) {
-    // s = clamp(max(ceil(v1), ceil(v2)), 0, 20); ambiguous only if a
-    // perturbation of M changes the clamped result
-    const double v1 = (l1 - log_eps) / (double)(mi + 1);
-    const double v2 = (l2 - log_eps) / (double)(mi + 2);
-    const double va = v1 > v2 ? v1 : v2;
-    double c_lo = ceil(va - M), c_hi = ceil(va + M);
-    c_lo = c_lo < 0.0 ? 0.0 : (c_lo > kMaxScaling ? kMaxScaling : c_lo);
-    c_hi = c_hi < 0.0 ? 0.0 : (c_hi > kMaxScaling ? kMaxScaling : c_hi);
+    // s = clamp(max(ceil(v1), ceil(v2)), 0, 20) (select.py:210-219)
+    const float v1 = (l1 - log_eps) * (1.0f / 16.0f);
+    const float v2 = (l2 - log_eps) * (1.0f / 17.0f);
+    const float va = fmaxf(v1, v2);
+    float c_lo = ceilf(va - M), c_hi = ceilf(va + M);
+    c_lo = fminf(fmaxf(c_lo, 0.f), (float)kMaxScaling);
+    c_hi = fminf(fmaxf(c_hi, 0.f), (float)kMaxScaling);
     if (c_lo != c_hi) return -1;
     s = (int)c_lo;
   }
   // reported bounds exp2(l1), exp2(l2) as products (select.py:220)
-  double e1, e2;
-  if (ri == 0) {
-    e1 = sastre_tail(0) * (n1 * n1);
-    e2 = sastre_tail(1) * (n1 * n1 * n1);
-  } else {
-    const int k = sastre_kcount(ri);
-    double pk = n2;
+  const int k = sastre_kcount(ri);
+  double pk = n2;
 #pragma unroll
-    for (int q = 1; q < 8; ++q)
-      if (q < k) pk *= n2;
-    e1 = sastre_tail(2 * ri) * pk;
-    e2 = sastre_tail(2 * ri + 1) * pk;
-    if (2 * k == mi) { e1 *= n1; e2 *= n2; } else { e2 *= n1; }
-  }
+  for (int q = 1; q < 8; ++q)
+    if (q < k) pk *= n2;
+  double e1 = sastre_tail(2 * ri) * pk, e2 = sastre_tail(2 * ri + 1) * pk;
+  if (2 * k == mi) { e1 *= n1; e2 *= n2; } else { e2 *= n1; }
   out->m = mi;
   out->s = s;
   out->e1 = e1;

@@ -288,16 +288,18 @@ def run_ours(args):
 
     gather_ms = None
     if ws > 1:
-        # the final gather of results to rank 0 (not part of the step)
-        out = torch.empty((ws * B, cfg.n, cfg.n), dtype=dtype, device=dev) if rank == 0 else None
+        # the final rank-ordered gather of results to rank 0 (reported, not in the step)
+        from paper_2512_20777_b200.shard import gather_to_rank0
         dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        gl = [torch.empty_like(Xd) for _ in range(ws)] if rank == 0 else None
-        dist.gather(Xd, gl, dst=0)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = gather_to_rank0(Xd, ws * B)
+        g1.record(stream)
         torch.cuda.synchronize()
-        gather_ms = 1e3 * (time.perf_counter() - t0)
-        del out, gl
+        from paper_2512_20777_b200.shard import max_over_ranks
+        gather_ms = max_over_ranks(g0.elapsed_time(g1), dev)
+        del full
 
     if rank == 0:
         pk = _peaks()

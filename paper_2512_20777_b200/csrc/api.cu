@@ -55,7 +55,7 @@ template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, cudaStream_t st) {
   if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, st);
   if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, st);
-  return launch_fused<T, 64, (sizeof(T) == 8 ? 2 : 4), 1, SCHEME>(W, X, batch, n, eps, po, st);
+  return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, st);
 }
 
 }  // namespace expmb

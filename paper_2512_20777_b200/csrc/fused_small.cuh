@@ -123,43 +123,53 @@ struct Fused {
     }
   }
 
-  // acc = L * R with L, R row-major NPAD x NPAD in shared memory.
+  // acc = L * R with L, R row-major NPAD x NPAD in shared memory.  The
+  // operands of k-chunk kb+KV are loaded into registers while chunk kb is
+  // multiplied (the kernel was shared-load latency bound: short_scoreboard).
+  __device__ __forceinline__ void ld_chunk(const T* __restrict__ L, const T* __restrict__ R, int kb, T (&a)[TM][KV],
+                                           T (&b)[KV][4]) const {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const T* p = L + row(i) * LD + kb;
+      if constexpr (sizeof(T) == 4) {
+        float4 v = *reinterpret_cast<const float4*>(p);
+        a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+      } else {
+        double2 v = *reinterpret_cast<const double2*>(p);
+        a[i][0] = v.x; a[i][1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KV; ++kk) {
+      const T* q = R + (kb + kk) * LD + 4 * tc;
+      if constexpr (sizeof(T) == 4) {
+        float4 v = *reinterpret_cast<const float4*>(q);
+        b[kk][0] = v.x; b[kk][1] = v.y; b[kk][2] = v.z; b[kk][3] = v.w;
+      } else {
+        double2 v0 = reinterpret_cast<const double2*>(q)[0];
+        double2 v1 = reinterpret_cast<const double2*>(q)[1];
+        b[kk][0] = v0.x; b[kk][1] = v0.y; b[kk][2] = v1.x; b[kk][3] = v1.y;
+      }
+    }
+  }
+
   __device__ __forceinline__ void mm(const T* __restrict__ L, const T* __restrict__ R, Tile& acc) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    T a[2][TM][KV], b[2][KV][4];
+    ld_chunk(L, R, 0, a[0], b[0]);
 #pragma unroll(NPAD <= 16 ? NPAD / KV : 4)
     for (int kb = 0; kb < NPAD; kb += KV) {
-      T a[TM][KV];
+      const int cur = (kb / KV) & 1;
+      if (kb + KV < NPAD) ld_chunk(L, R, kb + KV, a[cur ^ 1], b[cur ^ 1]);
 #pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const T* p = L + row(i) * LD + kb;
-        if constexpr (sizeof(T) == 4) {
-          float4 v = *reinterpret_cast<const float4*>(p);
-          a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
-        } else {
-          double2 v = *reinterpret_cast<const double2*>(p);
-          a[i][0] = v.x; a[i][1] = v.y;
-        }
-      }
-#pragma unroll
-      for (int kk = 0; kk < KV; ++kk) {
-        T b[4];
-        const T* q = R + (kb + kk) * LD + 4 * tc;
-        if constexpr (sizeof(T) == 4) {
-          float4 v = *reinterpret_cast<const float4*>(q);
-          b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
-        } else {
-          double2 v0 = reinterpret_cast<const double2*>(q)[0];
-          double2 v1 = reinterpret_cast<const double2*>(q)[1];
-          b[0] = v0.x; b[1] = v0.y; b[2] = v1.x; b[3] = v1.y;
-        }
+      for (int kk = 0; kk < KV; ++kk)
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i][kk], b[j], acc[i][j]);
-      }
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[cur][i][kk], b[cur][kk][j], acc[i][j]);
     }
   }
 

@@ -29,7 +29,7 @@ static int sm_count() {
 }
 
 template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
-static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, cudaStream_t st) {
+static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME>;
   static int occ = -1;  // per instantiation; identical on every B200
@@ -47,15 +47,16 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
   const int grid = (int)(ctas_needed < persistent ? ctas_needed : persistent);
   if (grid <= 0) return EXPMB_OK;
   // log2(eps) on the host: the same libm log2 as the reference's math.log2 (select.py:175)
-  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, log2(eps), po);
+  if (ctr != nullptr && cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, log2(eps), po, ctr);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
 template <typename T, int SCHEME>
-static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, cudaStream_t st) {
-  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, st);
-  if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, st);
-  return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, st);
+static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
+  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, ctr, st);
+  if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
+  return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, ctr, st);
 }
 
 }  // namespace expmb
@@ -83,7 +84,8 @@ const char* expmb_strerror(int code) {
 double expmb_unit_roundoff(int dtype) { return dtype == EXPMB_F32 ? 0x1p-24 : 0x1p-53; }
 
 size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme) {
-  if (n <= 64 || batch <= 0) return 0;
+  if (batch <= 0) return 0;
+  if (n <= 64) return 256;  // work counter of the persistent fused kernel
   return large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
 }
 
@@ -128,12 +130,14 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
   cudaStream_t st = (cudaStream_t)stream;
   PlanOut po{m, s, e1, e2, norms, mults, nonfinite};
   if (n <= 64) {
+    // optional: with a workspace the kernel claims matrices dynamically
+    int* ctr = (workspace != nullptr && workspace_bytes >= sizeof(int)) ? (int*)workspace : nullptr;
     if (dtype == EXPMB_F32) {
-      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>((const float*)W, (float*)X, batch, n, eps, po, st)
-                                    : dispatch_small<float, 1>((const float*)W, (float*)X, batch, n, eps, po, st);
+      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>((const float*)W, (float*)X, batch, n, eps, po, ctr, st)
+                                    : dispatch_small<float, 1>((const float*)W, (float*)X, batch, n, eps, po, ctr, st);
     }
-    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>((const double*)W, (double*)X, batch, n, eps, po, st)
-                                  : dispatch_small<double, 1>((const double*)W, (double*)X, batch, n, eps, po, st);
+    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>((const double*)W, (double*)X, batch, n, eps, po, ctr, st)
+                                  : dispatch_small<double, 1>((const double*)W, (double*)X, batch, n, eps, po, ctr, st);
   }
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;

@@ -89,6 +89,7 @@ struct Fused {
   static constexpr int BUF = NPAD * LD;          // one operand buffer (elements)
   // dynamic smem per CTA: two operand buffers per group + reduction scratch
   static constexpr size_t kSmemGroup = 2 * BUF * sizeof(T) + (WARPS_PG > 1 ? WARPS_PG * NPAD * sizeof(double) + 64 : 0);
+  static_assert(BUF * sizeof(T) % 16 == 0, "operand buffers must stay 16-byte aligned");
   static constexpr size_t kSmem = GROUPS * kSmemGroup;
 
   using Tile = T[TM][4];
@@ -109,16 +110,24 @@ struct Fused {
   }
 
   __device__ __forceinline__ int row(int i) const { return tr + i * TR; }
+  // Column of register j.  fp32: 4 consecutive columns (one 16-byte vector).
+  // fp64: two 16-byte pairs, one in each half of the row, so the 16 lanes of
+  // a row read/write 256 contiguous bytes per instruction (a 4-column double
+  // quad per lane strided the lanes 32 B apart: 2x shared-memory wavefronts).
+  __device__ __forceinline__ int col(int j) const {
+    if constexpr (sizeof(T) == 4) return 4 * tc + j;
+    else return (j >> 1) * (NPAD / 2) + 2 * tc + (j & 1);
+  }
 
   __device__ __forceinline__ void store(T* buf, const Tile& v) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      T* p = buf + row(i) * LD + 4 * tc;
+      T* p = buf + row(i) * LD;
       if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+        *reinterpret_cast<float4*>(p + col(0)) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
       } else {
-        reinterpret_cast<double2*>(p)[0] = make_double2(v[i][0], v[i][1]);
-        reinterpret_cast<double2*>(p)[1] = make_double2(v[i][2], v[i][3]);
+        *reinterpret_cast<double2*>(p + col(0)) = make_double2(v[i][0], v[i][1]);
+        *reinterpret_cast<double2*>(p + col(2)) = make_double2(v[i][2], v[i][3]);
       }
     }
   }
@@ -141,13 +150,13 @@ struct Fused {
     }
 #pragma unroll
     for (int kk = 0; kk < KV; ++kk) {
-      const T* q = R + (kb + kk) * LD + 4 * tc;
+      const T* q = R + (kb + kk) * LD;
       if constexpr (sizeof(T) == 4) {
-        float4 v = *reinterpret_cast<const float4*>(q);
+        float4 v = *reinterpret_cast<const float4*>(q + col(0));
         b[kk][0] = v.x; b[kk][1] = v.y; b[kk][2] = v.z; b[kk][3] = v.w;
       } else {
-        double2 v0 = reinterpret_cast<const double2*>(q)[0];
-        double2 v1 = reinterpret_cast<const double2*>(q)[1];
+        double2 v0 = *reinterpret_cast<const double2*>(q + col(0));
+        double2 v1 = *reinterpret_cast<const double2*>(q + col(2));
         b[kk][0] = v0.x; b[kk][1] = v0.y; b[kk][2] = v1.x; b[kk][3] = v1.y;
       }
     }
@@ -214,9 +223,9 @@ struct Fused {
       return mx;
     } else {
       const int w = t / 32, lane = t % 32;
-      if (lane < TC) {
+      if (lane < TC) {  // lanes 0..TC-1 hold tr = first row phase of this warp, tc = lane
 #pragma unroll
-        for (int j = 0; j < 4; ++j) red[w * NPAD + 4 * lane + j] = (double)cs[j];
+        for (int j = 0; j < 4; ++j) red[w * NPAD + col(j)] = (double)cs[j];
       }
       sync();
       double* res = red + WARPS_PG * NPAD;
@@ -258,19 +267,19 @@ struct Fused {
     for (int i = 0; i < TM; ++i) {
       const int r = row(i);
       if (vec) {
-        const T* p = src + r * NPAD + 4 * tc;
+        const T* p = src + r * NPAD;
         if constexpr (sizeof(T) == 4) {
-          float4 q = __ldg(reinterpret_cast<const float4*>(p));
+          float4 q = __ldg(reinterpret_cast<const float4*>(p + col(0)));
           v[i][0] = q.x; v[i][1] = q.y; v[i][2] = q.z; v[i][3] = q.w;
         } else {
-          double2 q0 = __ldg(reinterpret_cast<const double2*>(p));
-          double2 q1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+          double2 q0 = __ldg(reinterpret_cast<const double2*>(p + col(0)));
+          double2 q1 = __ldg(reinterpret_cast<const double2*>(p + col(2)));
           v[i][0] = q0.x; v[i][1] = q0.y; v[i][2] = q1.x; v[i][3] = q1.y;
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int c = 4 * tc + j;
+          const int c = col(j);
           v[i][j] = (r < n && c < n) ? __ldg(src + (size_t)r * n + c) : T(0);
         }
       }
@@ -282,24 +291,43 @@ struct Fused {
     for (int i = 0; i < TM; ++i) {
       const int r = row(i);
       if (vec) {
-        T* p = dst + r * NPAD + 4 * tc;
+        T* p = dst + r * NPAD;
         if constexpr (sizeof(T) == 4) {
-          __stcs(reinterpret_cast<float4*>(p), make_float4(v[i][0], v[i][1], v[i][2], v[i][3]));
+          __stcs(reinterpret_cast<float4*>(p + col(0)), make_float4(v[i][0], v[i][1], v[i][2], v[i][3]));
         } else {
-          __stcs(reinterpret_cast<double2*>(p), make_double2(v[i][0], v[i][1]));
-          __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[i][2], v[i][3]));
+          __stcs(reinterpret_cast<double2*>(p + col(0)), make_double2(v[i][0], v[i][1]));
+          __stcs(reinterpret_cast<double2*>(p + col(2)), make_double2(v[i][2], v[i][3]));
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int c = 4 * tc + j;
+          const int c = col(j);
           if (r < n && c < n) dst[(size_t)r * n + c] = v[i][j];
         }
       }
     }
   }
 
-  __device__ __forceinline__ bool is_diag(int i, int j) const { return row(i) == 4 * tc + j; }
+  __device__ __forceinline__ bool is_diag(int i, int j) const { return row(i) == col(j); }
+
+  // Next matrix of this group: static stride, or (with a work counter) the
+  // next unclaimed index after the first wave -- matrices cost 0..11
+  // products, so dynamic claiming removes the tail of unlucky groups.
+  __device__ __forceinline__ int64_t next_index(int64_t idx, int* ctr, int64_t first_wave) const {
+    if (ctr == nullptr) return idx + first_wave;
+    int64_t v = 0;
+    if (t == 0) v = first_wave + atomicAdd(ctr, 1);
+    if constexpr (TPG == 32) {
+      return __shfl_sync(0xffffffffu, v, 0);
+    } else {
+      int64_t* slot = reinterpret_cast<int64_t*>(red + WARPS_PG * NPAD) + 2;
+      if (t == 0) *slot = v;
+      sync();
+      v = *slot;
+      sync();
+      return v;
+    }
+  }
 };
 
 // Steps of the per-matrix program.  Every step is "build the two operands in
@@ -321,7 +349,8 @@ enum FusedStep : int {
 
 template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
 __global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, (NPAD == 16 && sizeof(T) == 4) ? 2 : 1)
-expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, PlanOut po) {
+expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, PlanOut po,
+                  int* __restrict__ ctr) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   using Tile = typename F::Tile;
   constexpr bool kPrefetch = !(NPAD == 64 && sizeof(T) == 8);  // register budget
@@ -350,8 +379,8 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   Tile B;  // W, later 2^-s W
   Tile nxt;
   f.load(W + idx * nn, n, vec, B);
-  for (; idx < batch; idx += stride) {
-    const int64_t nidx = idx + stride;
+  for (int64_t nidx; idx < batch; idx = nidx) {
+    nidx = f.next_index(idx, ctr, stride);
     if constexpr (kPrefetch) {
       if (nidx < batch) f.load(W + nidx * nn, n, vec, nxt);
     }

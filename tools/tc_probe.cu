@@ -1,0 +1,205 @@
+// tc_probe.cu -- validates the tcgen05 building blocks used by the large-n
+// fp32 path: TMA 2D loads with 128B swizzle, UMMA smem descriptors (A K-major,
+// B MN-major), kind::tf32 MMA with M=128 N=128, commit -> mbarrier, TMEM
+// loads, and the hardware's fp32 -> tf32 input conversion (truncate or round).
+// One CTA, C[128x128] = A[128xK] * B[Kx128], K = 64 (two 32-wide k-tiles).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <math.h>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t make_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(smem) >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+constexpr int M = 128, N = 128, K = 128, BK = 32, KT = K / BK;
+
+__global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap mapA,
+                                                const __grid_constant__ CUtensorMap mapB, float* C, int mode,
+                                                float* dbg) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  // layout: A tiles [2][128 rows][128 B] (16 KB each), B tiles [2][4 col-blocks][32 rows][128 B] (16 KB each)
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem + 1023) & ~(uintptr_t)1023);
+  float* sA = (float*)base;
+  float* sB = (float*)(base + KT * 16384);
+  __shared__ uint64_t bar_tma, bar_mma;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_tma, 1);
+    mbar_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar_tma, KT * 16384 * 2);
+    for (int kt = 0; kt < KT; ++kt) {
+      tma_load_2d(sA + kt * 4096, &mapA, &bar_tma, kt * BK, 0);  // A box {32 k, 128 m}
+      if (mode == 0) {
+        tma_load_2d(sB + kt * 4096, &mapB, &bar_tma, kt * BK, 0);  // B^T box {32 k, 128 n}
+      } else {
+        for (int nb = 0; nb < 4; ++nb)                               // B boxes {32 n, 32 k}
+          tma_load_2d(sB + kt * 4096 + nb * 1024, &mapB, &bar_tma, nb * 32, kt * BK);
+      }
+    }
+    mbar_wait(&bar_tma, 0);
+    for (int q = 0; q < 8; ++q) { dbg[q] = sA[q]; dbg[8 + q] = sB[q]; }
+    dbg[16] = __uint_as_float(tmem);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // kind::tf32, D f32, A K-major, B MN-major, N=128, M=128
+    const uint32_t bmaj = mode == 0 ? 0u : 1u;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (bmaj << 16) | ((uint32_t)(N >> 3) << 17) |
+                           ((uint32_t)(M >> 4) << 24);
+    for (int kt = 0; kt < KT; ++kt) {
+      for (int k = 0; k < BK / 8; ++k) {
+        const uint64_t ad = make_desc((unsigned char*)(sA + kt * 4096) + k * 32, 16, 1024);
+        const uint64_t bd = mode == 0 ? make_desc((unsigned char*)(sB + kt * 4096) + k * 32, 16, 1024)
+                          : mode == 1 ? make_desc((unsigned char*)(sB + kt * 4096) + k * 1024, 4096, 1024)
+                                      : make_desc((unsigned char*)(sB + kt * 4096) + k * 1024, 1024, 4096);
+        const uint32_t acc = (kt | k) ? 1u : 0u;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar_mma))
+                 : "memory");
+  }
+  __syncwarp();
+  mbar_wait(&bar_mma, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (= rows), 32 columns per load
+  const int row = warp * 32 + lane;
+  for (int cb = 0; cb < N / 32; ++cb) {
+    uint32_t r[32];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb * 32;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int j = 0; j < 32; ++j) C[row * N + cb * 32 + j] = __uint_as_float(r[j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  return (EncodeFn)fn;
+}
+
+static CUtensorMap make_map(EncodeFn enc, float* ptr, int cols, int rows, int box_cols, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); exit(1); }
+  return m;
+}
+
+int main() {
+  std::vector<float> A(M * K), B(K * N), Bt(N * K), C(M * N);
+  srand(1);
+  for (auto& x : A) x = (float)(rand() / (double)RAND_MAX - 0.5);
+  for (auto& x : B) x = (float)(rand() / (double)RAND_MAX - 0.5);
+  for (int k = 0; k < K; ++k) A[k] = 0.f;
+  A[0] = 1.0f + ldexpf(1.f, -11) + ldexpf(1.f, -12);
+  for (int k = 0; k < K; ++k) B[k * N] = (k == 0) ? 1.f : 0.f;
+  for (int k = 0; k < K; ++k) for (int j = 0; j < N; ++j) Bt[j * K + k] = B[k * N + j];
+  float *dA, *dB, *dBt, *dC, *dD;
+  CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, B.size() * 4)); CK(cudaMalloc(&dBt, Bt.size() * 4));
+  CK(cudaMalloc(&dC, C.size() * 4)); CK(cudaMalloc(&dD, 64 * 4));
+  CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dBt, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice));
+  EncodeFn enc = get_encode();
+  CUtensorMap mA = make_map(enc, dA, K, M, 32, 128);
+  CUtensorMap mB = make_map(enc, dB, N, K, 32, 32);
+  CUtensorMap mBt = make_map(enc, dBt, K, N, 32, 128);
+  const int smem = 2 * KT * 16384 + 1024;
+  CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (int mode = 0; mode < 3; ++mode) {
+    CK(cudaMemset(dC, 0, C.size() * 4));
+    probe<<<1, 128, smem>>>(mA, mode == 0 ? mBt : mB, dC, mode, dD);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost));
+    float dbg[17];
+    CK(cudaMemcpy(dbg, dD, sizeof(dbg), cudaMemcpyDeviceToHost));
+    double maxabs = 0, maxref = 0, maxabsT = 0;
+    int zeros = 0;
+    for (int i = 1; i < M; ++i)
+      for (int j = 0; j < N; ++j) {
+        double ref = 0, refT = 0;
+        for (int k = 0; k < K; ++k) { ref += (double)A[i * K + k] * B[k * N + j]; refT += (double)A[i * K + k] * Bt[j * K + k] * 0 + (double)A[i*K+k] * B[j * N + k % N] * 0; }
+        maxabs = fmax(maxabs, fabs(C[i * N + j] - ref));
+        maxref = fmax(maxref, fabs(ref));
+        zeros += C[i * N + j] == 0.f;
+      }
+    double x = C[0];
+    printf("{\"mode\": %d, \"max_abs_err\": %.3e, \"max_ref\": %.3f, \"zeros\": %d, \"c00\": %.10f, \"c01\": %.6f, \"c10\": %.6f, "
+           "\"conv\": \"%s\", \"tmem\": %u, \"sA0\": %.4f, \"sB0\": %.4f}\n",
+           mode, maxabs, maxref, zeros, x, C[1], C[N], x == 1.0 ? "truncate" : (x == 1.0 + ldexp(1.0, -10) ? "round" : "other"),
+           *(unsigned*)&dbg[16], dbg[0], dbg[8]);
+  }
+  return 0;
+}

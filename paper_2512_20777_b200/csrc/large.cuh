@@ -21,11 +21,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
 #include "fused_small.cuh"
 #include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
 #include "select.cuh"
 
 namespace expmb {
@@ -35,6 +38,12 @@ namespace expmb {
 // ---------------------------------------------------------------------------
 constexpr int kLargeBufsSastre = 7;  // W2 Y0 Y1 La Ra Lb Rb   (Tmp aliases Lb)
 constexpr int kLargeBufsPS = 6;      // W2 W3 W4 Q0 Q1 Tmp
+constexpr int kLargeBufsTC = 16;     // tensor-core path: see tc::Ctx
+
+// fp32 Sastre with 16-byte rows runs on the tcgen05 path (gemm_tc.cuh)
+static inline bool use_tc_path(int n, int esize, int scheme) {
+  return esize == 4 && scheme == 0 && (n % 4) == 0 && getenv("EXPMB_NO_TC") == nullptr;
+}
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers
 
 struct LargeLayout {
@@ -50,7 +59,7 @@ static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static inline LargeLayout large_layout(int64_t batch, int n, int esize, int scheme) {
   LargeLayout L{};
   L.mat_bytes = align256((size_t)n * n * esize);
-  L.nbufs = scheme == 1 ? kLargeBufsPS : kLargeBufsSastre;
+  L.nbufs = use_tc_path(n, esize, scheme) ? kLargeBufsTC : (scheme == 1 ? kLargeBufsPS : kLargeBufsSastre);
   const size_t per = L.mat_bytes * L.nbufs;
   int64_t chunk = (int64_t)(kLargeWsCap / per);
   if (chunk < 1) chunk = 1;
@@ -286,6 +295,138 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
+// ---------------------------------------------------------------------------
+// tensor-core path (fp32, Sastre)
+// ---------------------------------------------------------------------------
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static TensorMapEncodeFn tensor_map_encoder() {
+  static TensorMapEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (TensorMapEncodeFn)p;
+  }
+  return fn;
+}
+
+// [cnt][n][n] fp32 with `mstride_bytes` between matrices; box 32 (k) x 128 rows x 1, 128B swizzle
+static bool encode_map(CUtensorMap* m, const float* base, int n, int64_t cnt, size_t mstride_bytes) {
+  TensorMapEncodeFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)cnt};
+  cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)mstride_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int tc_launch(const tc::Maps& maps, const tc::Ctx& g, int stage, const int* list, int count, cudaStream_t st) {
+  if (count <= 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc::tc_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES) !=
+        cudaSuccess)
+      return 1;
+    attr = true;
+  }
+  const int t = (g.n + tc::BM - 1) / tc::BM;
+  dim3 grid(t, t, count);
+  tc::tc_stage_kernel<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(maps, g, stage, list);
+  return cudaGetLastError() != cudaSuccess;
+}
+
+static int large_run_chunk_tc(const float* W, float* X, int64_t cnt, int n, double eps, int64_t base, PlanOut po,
+                              unsigned char* ws, const LargeLayout& L, cudaStream_t st) {
+  const int ic = (int)cnt;
+  auto buf = [&](int b) { return reinterpret_cast<float*>(ws + L.off_bufs + (size_t)b * L.mat_bytes * L.chunk); };
+  double* part = reinterpret_cast<double*>(ws + L.off_part);
+  double* nrm4 = reinterpret_cast<double*>(ws + L.off_norm1);
+  int* need = reinterpret_cast<int*>(ws + L.off_need);
+  int8_t* dm = reinterpret_cast<int8_t*>(ws + L.off_m);
+  int8_t* ds = reinterpret_cast<int8_t*>(ws + L.off_s);
+  double* de1 = reinterpret_cast<double*>(ws + L.off_e1);
+  double* de2 = reinterpret_cast<double*>(ws + L.off_e2);
+  int* dlist = reinterpret_cast<int*>(ws + L.off_list);
+
+  tc::Ctx g{};
+  g.n = n;
+  g.tiles_m = L.tiles_m;
+  g.ms = (int64_t)(L.mat_bytes / 4);
+  g.ws = (int64_t)n * n;
+  g.W = W;
+  g.X = X;
+  float** slots[16] = {&g.Wlo, &g.Wt, &g.Wtlo, &g.W2, &g.W2lo, &g.W2t, &g.Y0, &g.Y1,
+                       &g.La, &g.Lalo, &g.Ra, &g.Ralo, &g.Lb, &g.Lblo, &g.Rb, &g.Rblo};
+  for (int b = 0; b < 16; ++b) *slots[b] = buf(b);
+  g.m = dm;
+  g.s = ds;
+  g.need = need;
+  g.part = part;
+
+  tc::Maps maps;
+  const size_t wsb = (size_t)n * n * 4, msb = L.mat_bytes;
+  const float* mp[tc::M_COUNT] = {W, g.Wlo, g.Wt, g.Wtlo, g.W2, g.W2lo, g.La, g.Lalo, g.Ra, g.Ralo, g.Lb, g.Lblo, g.Rb, g.Rblo};
+  for (int i = 0; i < tc::M_COUNT; ++i)
+    if (!encode_map(&maps.m[i], mp[i], n, cnt, i == tc::M_W ? wsb : msb)) return EXPMB_ERR_CUDA;
+
+  const double log_eps = log2(eps);
+  k_norm1<float><<<ic, 256, 0, st>>>(W, n, log_eps, 0, nrm4, need, dm, ds, de1, de2);
+  {
+    dim3 grid((n + 31) / 32, (n + 31) / 32, ic);
+    tc::tc_prep_kernel<<<grid, 256, 0, st>>>(g, ic);
+  }
+  if (tc_launch(maps, g, STAGE_W2, nullptr, ic, st)) return EXPMB_ERR_CUDA;
+  k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, 2, log_eps, 0, nrm4, need, dm, ds, de1, de2);
+
+  std::vector<int8_t> hm(cnt), hs(cnt);
+  if (cudaMemcpyAsync(hm.data(), dm, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  if (cudaMemcpyAsync(hs.data(), ds, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return EXPMB_ERR_CUDA;
+
+  std::vector<int> order(cnt);
+  for (int i = 0; i < ic; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return hs[a] > hs[b]; });
+  std::vector<int> l_s1, l_s2, l_s3;
+  int maxs = 0;
+  for (int i : order) {
+    const int m = hm[i];
+    if (hs[i] > maxs) maxs = hs[i];
+    if (m >= 4) l_s1.push_back(i);
+    if (m >= 8) l_s2.push_back(i);
+    if (m >= 15) l_s3.push_back(i);
+  }
+  std::vector<int> hl(order);
+  const size_t o1 = hl.size(); hl.insert(hl.end(), l_s1.begin(), l_s1.end());
+  const size_t o2 = hl.size(); hl.insert(hl.end(), l_s2.begin(), l_s2.end());
+  const size_t o3 = hl.size(); hl.insert(hl.end(), l_s3.begin(), l_s3.end());
+  if (cudaMemcpyAsync(dlist, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return EXPMB_ERR_CUDA;
+  {
+    const size_t nn = (size_t)n * n;
+    int bx = (int)((nn + 255) / 256);
+    if (bx > 64) bx = 64;
+    tc::tc_elem_kernel<<<dim3(bx, ic), 256, 0, st>>>(g, dlist);
+  }
+  if (tc_launch(maps, g, STAGE_E1, dlist + o1, (int)l_s1.size(), st)) return EXPMB_ERR_CUDA;
+  if (tc_launch(maps, g, STAGE_E2, dlist + o2, (int)l_s2.size(), st)) return EXPMB_ERR_CUDA;
+  if (tc_launch(maps, g, STAGE_E3, dlist + o3, (int)l_s3.size(), st)) return EXPMB_ERR_CUDA;
+  for (int q = 0; q < maxs; ++q) {
+    int c = 0;
+    while (c < ic && hs[order[c]] > q) ++c;
+    g.sq_step = q;
+    if (tc_launch(maps, g, STAGE_SQ, dlist, c, st)) return EXPMB_ERR_CUDA;
+  }
+  k_finish<float><<<ic, 256, 0, st>>>(W, X, n, 0, nrm4, dm, ds, de1, de2, base, po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
 static inline int large_expm(const void* W, void* X, int64_t batch, int n, int dtype, double eps, int scheme,
                              PlanOut po, void* workspace, cudaStream_t st) {
   const int es = dtype == 0 ? 4 : 8;
@@ -295,7 +436,10 @@ static inline int large_expm(const void* W, void* X, int64_t batch, int n, int d
     const int64_t cnt = std::min<int64_t>(L.chunk, batch - b0);
     const size_t off = (size_t)b0 * n * n;
     int rc;
-    if (dtype == 0)
+    if (dtype == 0 && use_tc_path(n, 4, scheme))
+      rc = large_run_chunk_tc(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n, eps,
+                              b0, po, ws, L, st);
+    else if (dtype == 0)
       rc = large_run_chunk<float>(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n,
                                   eps, scheme, b0, po, ws, L, st);
     else

@@ -10,6 +10,7 @@
 #include <stdlib.h>
 #include <math.h>
 #include <vector>
+#include <string.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     mbar_expect_tx(&bar_tma, KT * 16384 * 2);
     for (int kt = 0; kt < KT; ++kt) {
       tma_load_2d(sA + kt * 4096, &mapA, &bar_tma, kt * BK, 0);  // A box {32 k, 128 m}
-      if (mode == 0) {
+      if (mode == 0 || mode == 3) {
         tma_load_2d(sB + kt * 4096, &mapB, &bar_tma, kt * BK, 0);  // B^T box {32 k, 128 n}
       } else {
         for (int nb = 0; nb < 4; ++nb)                               // B boxes {32 n, 32 k}
@@ -90,16 +91,18 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     dbg[16] = __uint_as_float(tmem);
     asm volatile("tcgen05.fence::after_thread_sync;");
     // kind::tf32, D f32, A K-major, B MN-major, N=128, M=128
-    const uint32_t bmaj = mode == 0 ? 0u : 1u;
+    const uint32_t bmaj = (mode == 0 || mode == 3) ? 0u : 1u;
+    const int reps = mode == 3 ? 16 : 1;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (bmaj << 16) | ((uint32_t)(N >> 3) << 17) |
                            ((uint32_t)(M >> 4) << 24);
+    for (int rep = 0; rep < reps; ++rep)
     for (int kt = 0; kt < KT; ++kt) {
       for (int k = 0; k < BK / 8; ++k) {
         const uint64_t ad = make_desc((unsigned char*)(sA + kt * 4096) + k * 32, 16, 1024);
-        const uint64_t bd = mode == 0 ? make_desc((unsigned char*)(sB + kt * 4096) + k * 32, 16, 1024)
+        const uint64_t bd = (mode == 0 || mode == 3) ? make_desc((unsigned char*)(sB + kt * 4096) + k * 32, 16, 1024)
                           : mode == 1 ? make_desc((unsigned char*)(sB + kt * 4096) + k * 1024, 4096, 1024)
                                       : make_desc((unsigned char*)(sB + kt * 4096) + k * 1024, 1024, 4096);
-        const uint32_t acc = (kt | k) ? 1u : 0u;
+        const uint32_t acc = (kt | k | rep) ? 1u : 0u;
         asm volatile(
             "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
             " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
@@ -200,6 +203,37 @@ int main() {
            "\"conv\": \"%s\", \"tmem\": %u, \"sA0\": %.4f, \"sB0\": %.4f}\n",
            mode, maxabs, maxref, zeros, x, C[1], C[N], x == 1.0 ? "truncate" : (x == 1.0 + ldexp(1.0, -10) ? "round" : "other"),
            *(unsigned*)&dbg[16], dbg[0], dbg[8]);
+  }
+  {
+    // accumulation probe: positive inputs exactly representable in tf32, the
+    // 16-MMA block repeated 16x into one accumulator (a 256-step chain)
+    std::vector<float> A2(M * K), Bt2(N * K);
+    for (auto& x : A2) { x = (float)(rand() / (double)RAND_MAX); unsigned u; memcpy(&u, &x, 4); u &= 0xffffe000u; memcpy(&x, &u, 4); }
+    for (auto& x : Bt2) { x = (float)(rand() / (double)RAND_MAX); unsigned u; memcpy(&u, &x, 4); u &= 0xffffe000u; memcpy(&x, &u, 4); }
+    CK(cudaMemcpy(dA, A2.data(), A2.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dBt, Bt2.data(), Bt2.size() * 4, cudaMemcpyHostToDevice));
+    probe<<<1, 128, smem>>>(mA, mBt, dC, 3, dD);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost));
+    double sum_rel = 0, max_rel = 0; int below = 0;
+    for (int i = 0; i < M; ++i) for (int j = 0; j < N; ++j) {
+      double ref = 0;
+      for (int k = 0; k < K; ++k) ref += (double)A2[i * K + k] * Bt2[j * K + k];
+      ref *= 16;
+      double rel = (C[i * N + j] - ref) / ref;
+      sum_rel += rel; max_rel = fmax(max_rel, fabs(rel)); below += rel < 0;
+    }
+    // same sums in fp32 sequential RN (host) for comparison
+    double sum_rel32 = 0;
+    for (int i = 0; i < M; ++i) for (int j = 0; j < N; ++j) {
+      float acc = 0; double ref = 0;
+      for (int rep = 0; rep < 16; ++rep) for (int k = 0; k < K; ++k) { acc = fmaf(A2[i*K+k], Bt2[j*K+k], acc); }
+      for (int k = 0; k < K; ++k) ref += (double)A2[i * K + k] * Bt2[j * K + k];
+      sum_rel32 += (acc - 16 * ref) / (16 * ref);
+    }
+    printf("{\"accum_probe\": \"2048-term positive dot products\", \"mean_rel_err_tc\": %.3e, \"max_rel_err_tc\": %.3e, "
+           "\"frac_below\": %.3f, \"mean_rel_err_fp32_fma_chain\": %.3e}\n",
+           sum_rel / (M * N), max_rel, below / (double)(M * N), sum_rel32 / (M * N));
   }
   return 0;
 }

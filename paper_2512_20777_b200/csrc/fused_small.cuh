@@ -95,6 +95,7 @@ struct Fused {
   using Tile = T[TM][4];
 
   int tr, tc, g, t;
+  int soff;  // shared-memory offset (elements) of this thread's first row/column in a buffer
   T* buf0;
   T* buf1;
   double* red;
@@ -122,12 +123,12 @@ struct Fused {
   __device__ __forceinline__ void store(T* buf, const Tile& v) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      T* p = buf + row(i) * LD;
+      T* p = buf + soff + i * TR * LD;
       if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<float4*>(p + col(0)) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+        *reinterpret_cast<float4*>(p) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
       } else {
-        *reinterpret_cast<double2*>(p + col(0)) = make_double2(v[i][0], v[i][1]);
-        *reinterpret_cast<double2*>(p + col(2)) = make_double2(v[i][2], v[i][3]);
+        *reinterpret_cast<double2*>(p) = make_double2(v[i][0], v[i][1]);
+        *reinterpret_cast<double2*>(p + NPAD / 2) = make_double2(v[i][2], v[i][3]);
       }
     }
   }
@@ -139,7 +140,7 @@ struct Fused {
                                            T (&b)[KV][4]) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      const T* p = L + row(i) * LD + kb;
+      const T* p = L + (tr + i * TR) * LD + kb;
       if constexpr (sizeof(T) == 4) {
         float4 v = *reinterpret_cast<const float4*>(p);
         a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
@@ -150,13 +151,13 @@ struct Fused {
     }
 #pragma unroll
     for (int kk = 0; kk < KV; ++kk) {
-      const T* q = R + (kb + kk) * LD;
+      const T* q = R + (kb + kk) * LD + (soff - tr * LD);  // row kb+kk, this thread's columns
       if constexpr (sizeof(T) == 4) {
-        float4 v = *reinterpret_cast<const float4*>(q + col(0));
+        float4 v = *reinterpret_cast<const float4*>(q);
         b[kk][0] = v.x; b[kk][1] = v.y; b[kk][2] = v.z; b[kk][3] = v.w;
       } else {
-        double2 v0 = *reinterpret_cast<const double2*>(q + col(0));
-        double2 v1 = *reinterpret_cast<const double2*>(q + col(2));
+        double2 v0 = *reinterpret_cast<const double2*>(q);
+        double2 v1 = *reinterpret_cast<const double2*>(q + NPAD / 2);
         b[kk][0] = v0.x; b[kk][1] = v0.y; b[kk][2] = v1.x; b[kk][3] = v1.y;
       }
     }
@@ -360,6 +361,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   f.t = threadIdx.x % F::TPG;
   f.tr = f.t / F::TC;
   f.tc = f.t % F::TC;
+  f.soff = f.tr * F::LD + f.col(0);
   unsigned char* gbase = smem_raw + f.g * F::kSmemGroup;
   f.buf0 = reinterpret_cast<T*>(gbase);
   f.buf1 = f.buf0 + F::BUF;

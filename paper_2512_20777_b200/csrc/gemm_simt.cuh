@@ -158,100 +158,120 @@ __device__ __forceinline__ bool make_epi(const GemmCtx<T>& g, int stage, int z, 
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// FMA GEMM mainloop: 128x128 CTA tile, 256 threads, 8x8 outputs per thread,
+// multi-stage cp.async (LDGSTS) ring so global latency hides behind several
+// k-tiles of FMAs.  Operand tiles stay row-major in shared memory: a thread
+// reads its 8 L-rows with 16-byte loads along k and its 8 R-columns with
+// 16-byte loads along n (fp64 columns are interleaved in 2-wide groups so the
+// 16 lanes of a row read 256 contiguous bytes: no bank conflicts).
+// ---------------------------------------------------------------------------
 template <typename T>
-struct SimtTraits;
+struct SimtCfg;
 template <>
-struct SimtTraits<float> {
-  static constexpr int LDS = kGemmBM + 4;
+struct SimtCfg<float> {
+  static constexpr int BK = 16, STAGES = 4, KV = 4, VW = 4;
 };
 template <>
-struct SimtTraits<double> {
-  static constexpr int LDS = kGemmBM + 2;
+struct SimtCfg<double> {
+  static constexpr int BK = 16, STAGES = 3, KV = 2, VW = 2;
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int sz = pred ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename T>
+__device__ __forceinline__ int simt_col(int tx, int j) {
+  if constexpr (sizeof(T) == 4) return (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+  else return (j >> 1) * 32 + tx * 2 + (j & 1);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256, 1)
 gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
-  constexpr int LDS = SimtTraits<T>::LDS;
-  __shared__ __align__(16) T As[2][kGemmBK][LDS];
-  __shared__ __align__(16) T Bs[2][kGemmBK][LDS];
+  using C = SimtCfg<T>;
+  constexpr int BK = C::BK, ST = C::STAGES, KV = C::KV, VW = C::VW;
+  constexpr int LDA = BK + KV;            // padded row of an L tile (elements)
+  constexpr int LDB = kGemmBN + 16 / (int)sizeof(T);
+  constexpr int A_ELEMS = kGemmBM * LDA, B_ELEMS = BK * LDB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);
+  T* Bs = As + ST * A_ELEMS;
+
   const int z = list ? list[blockIdx.z] : (int)blockIdx.z;
   Epi<T> e;
   if (!make_epi(g, stage, z, e)) return;
   const int n = g.n;
   const int m0 = blockIdx.y * kGemmBM, n0 = blockIdx.x * kGemmBN;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int arow = tid / 2, acol = (tid % 2) * 4;
-  const int brow = tid / 32, bcol = (tid % 32) * 4;
-  const bool vec = (n % 4) == 0;
+  const bool vec = (n % KV) == 0;  // 16-byte rows chunks are whole
   const T* __restrict__ Lp = e.L;
   const T* __restrict__ Rp = e.R;
+  const int nk = (n + BK - 1) / BK;
 
-  T ra[4], rb[4];
-  auto gload = [&](int k0) {
-    const int ar = m0 + arow, ac = k0 + acol;
-    const int br = k0 + brow, bc = n0 + bcol;
-    if (vec) {
-      if (ar < n && ac < n) {
-        const T* p = Lp + (size_t)ar * n + ac;
-        if constexpr (sizeof(T) == 4) {
-          float4 v = __ldg(reinterpret_cast<const float4*>(p));
-          ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
-        } else {
-          double2 v0 = __ldg(reinterpret_cast<const double2*>(p)), v1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
-          ra[0] = v0.x; ra[1] = v0.y; ra[2] = v1.x; ra[3] = v1.y;
-        }
-      } else {
-        ra[0] = ra[1] = ra[2] = ra[3] = T(0);
-      }
-      if (br < n && bc < n) {
-        const T* p = Rp + (size_t)br * n + bc;
-        if constexpr (sizeof(T) == 4) {
-          float4 v = __ldg(reinterpret_cast<const float4*>(p));
-          rb[0] = v.x; rb[1] = v.y; rb[2] = v.z; rb[3] = v.w;
-        } else {
-          double2 v0 = __ldg(reinterpret_cast<const double2*>(p)), v1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
-          rb[0] = v0.x; rb[1] = v0.y; rb[2] = v1.x; rb[3] = v1.y;
-        }
-      } else {
-        rb[0] = rb[1] = rb[2] = rb[3] = T(0);
-      }
-    } else {
+  // ---- async tile loader ----
+  constexpr int A_CHUNKS = kGemmBM * BK / KV, B_CHUNKS = BK * kGemmBN / KV;  // 16-byte chunks
+  auto load_tile = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    T* as = As + st * A_ELEMS;
+    T* bs = Bs + st * B_ELEMS;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ra[q] = (ar < n && ac + q < n) ? Lp[(size_t)ar * n + ac + q] : T(0);
-        rb[q] = (br < n && bc + q < n) ? Rp[(size_t)br * n + bc + q] : T(0);
+    for (int c = tid; c < A_CHUNKS; c += 256) {
+      const int r = c / (BK / KV), kc = (c % (BK / KV)) * KV;
+      const int gr = m0 + r, gk = k0 + kc;
+      if (vec) {
+        cp_async16(as + r * LDA + kc, Lp + (size_t)(gr < n ? gr : 0) * n + (gk < n ? gk : 0), gr < n && gk < n);
+      } else {
+#pragma unroll
+        for (int q = 0; q < KV; ++q) as[r * LDA + kc + q] = (gr < n && gk + q < n) ? Lp[(size_t)gr * n + gk + q] : T(0);
+      }
+    }
+#pragma unroll
+    for (int c = tid; c < B_CHUNKS; c += 256) {
+      const int r = c / (kGemmBN / KV), nc = (c % (kGemmBN / KV)) * KV;
+      const int gk = k0 + r, gn = n0 + nc;
+      if (vec) {
+        cp_async16(bs + r * LDB + nc, Rp + (size_t)(gk < n ? gk : 0) * n + (gn < n ? gn : 0), gk < n && gn < n);
+      } else {
+#pragma unroll
+        for (int q = 0; q < KV; ++q) bs[r * LDB + nc + q] = (gk < n && gn + q < n) ? Rp[(size_t)gk * n + gn + q] : T(0);
       }
     }
   };
-  auto sstore = [&](int b) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) As[b][acol + q][arow] = ra[q];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) Bs[b][brow][bcol + q] = rb[q];
-  };
 
-  T acc[8][8];
+  // fp32: two-level accumulation (a fresh partial every 32 k, added to the
+  // running sum) keeps the summation error near (32 + n/32) u instead of n u.
+  constexpr bool kTwoLevel = sizeof(T) == 4;
+  constexpr int kChunkTiles = 32 / BK;
+  T acc[8][8], pacc[kTwoLevel ? 8 : 1][kTwoLevel ? 8 : 1];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
 
-  // fp32: two-level accumulation (a fresh partial every kChunk k-tiles, then
-  // added to the running sum) keeps the summation error near
-  // (32 + n/32) u instead of n u -- needed for the 1e-5 bar at n = 2048.
-  constexpr bool kTwoLevel = sizeof(T) == 4;
-  constexpr int kChunk = 4;
-  T pacc[kTwoLevel ? 8 : 1][kTwoLevel ? 8 : 1];
-  const int nk = (n + kGemmBK - 1) / kGemmBK;
-  gload(0);
-  sstore(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < nk) load_tile(s, s);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < nk; ++kt) {
-    const int cur = kt & 1;
-    if (kt + 1 < nk) gload((kt + 1) * kGemmBK);
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    {  // refill the stage consumed in iteration kt-1
+      const int nt = kt + ST - 1;
+      if (nt < nk) load_tile(nt, nt % ST);
+      cp_async_commit();
+    }
+    const T* as = As + (kt % ST) * A_ELEMS;
+    const T* bs = Bs + (kt % ST) * B_ELEMS;
     if constexpr (kTwoLevel) {
-      if (kt % kChunk == 0) {
+      if (kt % kChunkTiles == 0) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -259,89 +279,141 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
       }
     }
 #pragma unroll
-    for (int k = 0; k < kGemmBK; ++k) {
-      T a[8], b[8];
+    for (int kb = 0; kb < BK; kb += KV) {
+      T a[8][KV];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const T* pa = &As[cur][k][h * 64 + ty * 4];
-        const T* pb = &Bs[cur][k][h * 64 + tx * 4];
+      for (int i = 0; i < 8; ++i) {
+        const int r = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+        const T* p = as + r * LDA + kb;
         if constexpr (sizeof(T) == 4) {
-          float4 va = *reinterpret_cast<const float4*>(pa), vb = *reinterpret_cast<const float4*>(pb);
-          a[4 * h] = va.x; a[4 * h + 1] = va.y; a[4 * h + 2] = va.z; a[4 * h + 3] = va.w;
-          b[4 * h] = vb.x; b[4 * h + 1] = vb.y; b[4 * h + 2] = vb.z; b[4 * h + 3] = vb.w;
+          const float4 v = *reinterpret_cast<const float4*>(p);
+          a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
         } else {
-          double2 a0 = reinterpret_cast<const double2*>(pa)[0], a1 = reinterpret_cast<const double2*>(pa)[1];
-          double2 b0 = reinterpret_cast<const double2*>(pb)[0], b1 = reinterpret_cast<const double2*>(pb)[1];
-          a[4 * h] = a0.x; a[4 * h + 1] = a0.y; a[4 * h + 2] = a1.x; a[4 * h + 3] = a1.y;
-          b[4 * h] = b0.x; b[4 * h + 1] = b0.y; b[4 * h + 2] = b1.x; b[4 * h + 3] = b1.y;
+          const double2 v = *reinterpret_cast<const double2*>(p);
+          a[i][0] = v.x; a[i][1] = v.y;
         }
       }
-      if constexpr (kTwoLevel) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+      for (int kk = 0; kk < KV; ++kk) {
+        T b[8];
+        const T* q = bs + (kb + kk) * LDB;
+        if constexpr (sizeof(T) == 4) {
+          const float4 v0 = *reinterpret_cast<const float4*>(q + tx * 4);
+          const float4 v1 = *reinterpret_cast<const float4*>(q + 64 + tx * 4);
+          b[0] = v0.x; b[1] = v0.y; b[2] = v0.z; b[3] = v0.w;
+          b[4] = v1.x; b[5] = v1.y; b[6] = v1.z; b[7] = v1.w;
+        } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) pacc[i][j] = fma(a[i], b[j], pacc[i][j]);
-      } else {
+          for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(q + h * 32 + tx * 2);
+            b[2 * h] = v.x; b[2 * h + 1] = v.y;
+          }
+        }
+        if constexpr (kTwoLevel) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            for (int j = 0; j < 8; ++j) pacc[i][j] = fma(a[i][kk], b[j], pacc[i][j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i][kk], b[j], acc[i][j]);
+        }
       }
     }
     if constexpr (kTwoLevel) {
-      if (kt % kChunk == kChunk - 1 || kt + 1 == nk) {
+      if (kt % kChunkTiles == kChunkTiles - 1 || kt + 1 == nk) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[i][j] += pacc[i][j];
       }
     }
-    if (kt + 1 < nk) sstore(cur ^ 1);
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
-  // ---- fused epilogue --------------------------------------------------
+  // ---- fused epilogue (VW-wide vectors along a row) ----
   double csum[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) csum[j] = 0.0;
+  const bool evec = (n % VW) == 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
     if (row >= n) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int col = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-      if (col >= n) continue;
-      const size_t pos = (size_t)row * n + col;
-      const T dg = (row == col) ? T(1) : T(0);
-      T o0 = e.alpha * acc[i][j];
+    for (int j0 = 0; j0 < 8; j0 += VW) {
+      const int col0 = n0 + simt_col<T>(tx, j0);
+      if (col0 >= n) continue;
+      const size_t pos = (size_t)row * n + col0;
+      const bool full = evec && col0 + VW <= n;
+      T o0[VW], in[4][VW];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q < e.nin) o0 = fma(e.c[0][q], e.in[q][pos], o0);
-      o0 = fma(e.d[0], dg, o0);
-      e.out[0][pos] = o0;
-      if (e.nout > 1) {
-        T o1 = o0, o2 = o0;
+      for (int q = 0; q < 4; ++q) {
+        if (q < e.nin) {
+          if (full) {
+            if constexpr (sizeof(T) == 4) {
+              const float4 v = *reinterpret_cast<const float4*>(e.in[q] + pos);
+              in[q][0] = v.x; in[q][1] = v.y; in[q][2] = v.z; in[q][3] = v.w;
+            } else {
+              const double2 v = *reinterpret_cast<const double2*>(e.in[q] + pos);
+              in[q][0] = v.x; in[q][1] = v.y;
+            }
+          } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q < e.nin) {
-            const T v = e.in[q][pos];
-            o1 = fma(e.c[1][q], v, o1);
-            o2 = fma(e.c[2][q], v, o2);
+            for (int v = 0; v < VW; ++v) in[q][v] = (col0 + v < n) ? e.in[q][pos + v] : T(0);
           }
         }
-        e.out[1][pos] = fma(e.d[1], dg, o1);
-        e.out[2][pos] = fma(e.d[2], dg, o2);
       }
-      if (e.colnorm) csum[j] += fabs((double)o0);
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const T dg = (row == col0 + v) ? T(1) : T(0);
+        T x = e.alpha * acc[i][j0 + v];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < e.nin) x = fma(e.c[0][q], in[q][v], x);
+        o0[v] = fma(e.d[0], dg, x);
+      }
+      auto put = [&](T* dst, const T (&val)[VW]) {
+        if (full) {
+          if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(dst + pos) = make_float4(val[0], val[1], val[2], val[3]);
+          else *reinterpret_cast<double2*>(dst + pos) = make_double2(val[0], val[1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VW; ++v)
+            if (col0 + v < n) dst[pos + v] = val[v];
+        }
+      };
+      put(e.out[0], o0);
+      if (e.nout > 1) {
+#pragma unroll
+        for (int k = 1; k < 3; ++k) {
+          T ok[VW];
+#pragma unroll
+          for (int v = 0; v < VW; ++v) {
+            T x = o0[v];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < e.nin) x = fma(e.c[k][q], in[q][v], x);
+            ok[v] = fma(e.d[k], (row == col0 + v) ? T(1) : T(0), x);
+          }
+          put(e.out[k], ok);
+        }
+      }
+      if (e.colnorm) {
+#pragma unroll
+        for (int v = 0; v < VW; ++v)
+          if (col0 + v < n) csum[j0 + v] += fabs((double)o0[v]);
+      }
     }
   }
   if (e.colnorm) {
     // deterministic column reduction over the 16 thread rows of the tile
-    double* red = reinterpret_cast<double*>(&As[0][0][0]);  // 16 x 128 doubles fit in As+Bs
+    double* red = reinterpret_cast<double*>(smem_raw);  // 16 x 128 doubles
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) red[ty * kGemmBN + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4)] = csum[j];
+    for (int j = 0; j < 8; ++j) red[ty * kGemmBN + simt_col<T>(tx, j)] = csum[j];
     __syncthreads();
     if (tid < kGemmBN && n0 + tid < n) {
       double a = 0.0;
@@ -352,11 +424,24 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 }
 
 template <typename T>
+constexpr int simt_smem_bytes() {
+  using C = SimtCfg<T>;
+  return (int)(C::STAGES * (kGemmBM * (C::BK + C::KV) + C::BK * (kGemmBN + 16 / (int)sizeof(T))) * sizeof(T));
+}
+
+template <typename T>
 static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st) {
   if (count <= 0) return 0;
+  static bool attr = false;
+  constexpr int smem = simt_smem_bytes<T>();
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_stage_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return 1;
+    attr = true;
+  }
   const int tn = (g.n + kGemmBN - 1) / kGemmBN, tm = (g.n + kGemmBM - 1) / kGemmBM;
   dim3 grid(tn, tm, count);
-  gemm_stage_kernel<T><<<grid, 256, 0, st>>>(g, stage, list);
+  gemm_stage_kernel<T><<<grid, 256, smem, st>>>(g, stage, list);
   return cudaGetLastError() != cudaSuccess;
 }
 

@@ -74,7 +74,31 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        while not self._stop.is_set():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            try:
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            act = [k for k, b in bits.items() if r & b]
+            self.rows.append([str(sm), str(mx), "", *["Active" if k in act else "Not Active" for k in bits]])
+            self._stop.wait(0.002)
+
     def _run(self):
+        try:
+            import pynvml  # noqa: F401
+            return self._run_nvml()
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",

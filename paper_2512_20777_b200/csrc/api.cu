@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/expmb.h"
@@ -55,8 +56,10 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
 template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   // warp-per-matrix: ~100 matrices per SM balance statically; the claim
-  // atomics only added latency there (7% of stall samples)
-  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, nullptr, st);
+  // atomics only added latency there (7% of stall samples).  EXPMB_CLAIM=1
+  // forces dynamic claiming (A/B experiments).
+  static const bool claim16 = getenv("EXPMB_CLAIM") && getenv("EXPMB_CLAIM")[0] == '1';
+  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, claim16 ? ctr : nullptr, st);
   if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
   return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, ctr, st);
 }

@@ -133,8 +133,17 @@ class ClockSampler:
 # CPU side (the oracle port of the reference algorithm) -- rank 0 only
 # ---------------------------------------------------------------------------
 
+def _cpu_worker_init():
+    # one BLAS thread per worker process (the pool supplies the parallelism;
+    # forked workers inherit the parent's already-initialised BLAS pool)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
 def _cpu_chunk(args):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     W, eps = args
     from oracle import expm_oracle as O
     for i in range(W.shape[0]):
@@ -151,21 +160,22 @@ def cpu_reference_rate(key: str, count: int | None = None, cores: int | None = N
     count = count or CPU_SAMPLE[key]
     cores = cores or os.cpu_count() or 1
     W = WL.generate(key, indices=np.arange(count)).astype(np.float64)
-    pieces = np.array_split(W, max(1, min(count, cores * 4)))
-    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    try:
-        with ProcessPoolExecutor(max_workers=cores) as pool:
+    if cfg.n >= 256:
+        # large orders: one process, BLAS threads on every core (BASELINE.md mode 1)
+        t0 = time.perf_counter()
+        done = _cpu_chunk((W, cfg.eps))
+        dt = time.perf_counter() - t0
+        mode = "serial expm loop, multithreaded BLAS"
+    else:
+        # small orders: process pool, one BLAS thread each (reference bench.py:303-306; mode 2)
+        pieces = np.array_split(W, max(1, min(count, cores * 4)))
+        with ProcessPoolExecutor(max_workers=cores, initializer=_cpu_worker_init) as pool:
             list(pool.map(_cpu_chunk, [(pieces[0][:1], cfg.eps)] * min(cores, 2)))  # warm workers
             t0 = time.perf_counter()
             done = sum(pool.map(_cpu_chunk, [(p, cfg.eps) for p in pieces]))
             dt = time.perf_counter() - t0
-    finally:
-        if env_old is None:
-            os.environ.pop("OPENBLAS_NUM_THREADS", None)
-        else:
-            os.environ["OPENBLAS_NUM_THREADS"] = env_old
-    return done / dt, cores, f"{done} matrices of {key} ({cfg.n}x{cfg.n}, fp64 as the reference computes)"
+        mode = f"process pool x{cores}, 1 BLAS thread each"
+    return done / dt, cores, f"{done} matrices of {key} ({cfg.n}x{cfg.n}, fp64 as the reference computes; {mode})"
 
 
 # ---------------------------------------------------------------------------

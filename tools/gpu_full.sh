@@ -1,0 +1,18 @@
+#!/bin/bash
+# Full evidence run: GPU tests, default bench (C2, with CPU baseline), reference arm,
+# per-config bench lines, launch list + full ncu capture of the C2 kernel.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -rf -p no:cacheprovider --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+for c in C1 C3 C4; do
+timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+done
+timeout 900 python bench.py --config C5 --steps 2 --warmup 3 --batch 64 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2.csv \
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:expm_fused -s 3 -c 1 \
+    -o gpurun_out/prof_C2 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1
+echo done

@@ -71,6 +71,15 @@ struct Vec<double> {
   static constexpr int KV = 2;
 };
 
+// Packed fp32x2 FMA (sm_100: FFMA2, 64 FMAs per warp instruction).  The
+// kernels are issue-bound, so halving the FMA instruction count is the win.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b),
+                     uc = *reinterpret_cast<unsigned long long*>(&c), d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(ua), "l"(ub), "l"(uc));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 __device__ __forceinline__ bool is_finite_t(float x) { return isfinite(x); }
 __device__ __forceinline__ bool is_finite_t(double x) { return isfinite(x); }
 
@@ -164,22 +173,46 @@ struct Fused {
   }
 
   __device__ __forceinline__ void mm(const T* __restrict__ L, const T* __restrict__ R, Tile& acc) const {
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
     T a[2][TM][KV], b[2][KV][4];
     ld_chunk(L, R, 0, a[0], b[0]);
+    if constexpr (sizeof(T) == 4) {
+      float2 acc2[TM][2];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) acc2[i][0] = acc2[i][1] = make_float2(0.f, 0.f);
 #pragma unroll(NPAD <= 16 ? NPAD / KV : 4)
-    for (int kb = 0; kb < NPAD; kb += KV) {
-      const int cur = (kb / KV) & 1;
-      if (kb + KV < NPAD) ld_chunk(L, R, kb + KV, a[cur ^ 1], b[cur ^ 1]);
+      for (int kb = 0; kb < NPAD; kb += KV) {
+        const int cur = (kb / KV) & 1;
+        if (kb + KV < NPAD) ld_chunk(L, R, kb + KV, a[cur ^ 1], b[cur ^ 1]);
 #pragma unroll
-      for (int kk = 0; kk < KV; ++kk)
+        for (int kk = 0; kk < KV; ++kk)
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+          for (int i = 0; i < TM; ++i) {
+            const float2 ai = make_float2(a[cur][i][kk], a[cur][i][kk]);
+            acc2[i][0] = ffma2(make_float2(b[cur][kk][0], b[cur][kk][1]), ai, acc2[i][0]);
+            acc2[i][1] = ffma2(make_float2(b[cur][kk][2], b[cur][kk][3]), ai, acc2[i][1]);
+          }
+      }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[cur][i][kk], b[cur][kk][j], acc[i][j]);
+      for (int i = 0; i < TM; ++i) {
+        acc[i][0] = acc2[i][0].x; acc[i][1] = acc2[i][0].y;
+        acc[i][2] = acc2[i][1].x; acc[i][3] = acc2[i][1].y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+#pragma unroll(NPAD <= 16 ? NPAD / KV : 4)
+      for (int kb = 0; kb < NPAD; kb += KV) {
+        const int cur = (kb / KV) & 1;
+        if (kb + KV < NPAD) ld_chunk(L, R, kb + KV, a[cur ^ 1], b[cur ^ 1]);
+#pragma unroll
+        for (int kk = 0; kk < KV; ++kk)
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[cur][i][kk], b[cur][kk][j], acc[i][j]);
+      }
     }
   }
 

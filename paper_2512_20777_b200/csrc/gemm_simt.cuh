@@ -249,7 +249,8 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   // running sum) keeps the summation error near (32 + n/32) u instead of n u.
   constexpr bool kTwoLevel = sizeof(T) == 4;
   constexpr int kChunkTiles = 32 / BK;
-  T acc[8][8], pacc[kTwoLevel ? 8 : 1][kTwoLevel ? 8 : 1];
+  T acc[8][8];
+  float2 pacc[kTwoLevel ? 8 : 1][kTwoLevel ? 4 : 1];  // fp32 partials as FFMA2 pairs
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -275,7 +276,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) pacc[i][j] = T(0);
+          for (int j = 0; j < 4; ++j) pacc[i][j] = make_float2(0.f, 0.f);
       }
     }
 #pragma unroll
@@ -311,9 +312,12 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
         }
         if constexpr (kTwoLevel) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < 8; ++i) {
+            const float2 ai = make_float2((float)a[i][kk], (float)a[i][kk]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) pacc[i][j] = fma(a[i][kk], b[j], pacc[i][j]);
+            for (int j = 0; j < 4; ++j)
+              pacc[i][j] = ffma2(make_float2((float)b[2 * j], (float)b[2 * j + 1]), ai, pacc[i][j]);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -327,7 +331,10 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] += pacc[i][j];
+          for (int j = 0; j < 4; ++j) {
+            acc[i][2 * j] += (T)pacc[i][j].x;
+            acc[i][2 * j + 1] += (T)pacc[i][j].y;
+          }
       }
     }
   }

@@ -18,6 +18,25 @@ __global__ void k_ffma(float* out, float a) {
   for (int i = 0; i < 16; ++i) s += x[i];
   if (s == 1.2345f) out[0] = s;
 }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b),
+                     uc = *reinterpret_cast<unsigned long long*>(&c), d;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(ua), "l"(ub), "l"(uc));
+  return *reinterpret_cast<float2*>(&d);
+}
+__global__ void k_ffma2(float* out, float a) {
+  float2 x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = make_float2(threadIdx.x + i, i);
+  const float2 aa = make_float2(a, a), h = make_float2(0.5f, 0.5f);
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = ffma2(x[i], aa, h);
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i].x + x[i].y;
+  if (s == 1.2345f) out[0] = s;
+}
 __global__ void k_dfma(double* out, double a) {
   double x[16];
 #pragma unroll
@@ -94,6 +113,8 @@ int main() {
   float t;
   t = timeit([&] { k_ffma<<<blocks, threads>>>(fo, 0.999f); });
   printf("{\"pipe\": \"ffma_fp32\", \"tflops\": %.2f, \"ms\": %.3f}\n", nthr * ITERS * 16 * 2 / (t * 1e-3) / 1e12, t);
+  t = timeit([&] { k_ffma2<<<blocks, threads>>>(fo, 0.999f); });
+  printf("{\"pipe\": \"ffma2_fp32x2\", \"tflops\": %.2f, \"ms\": %.3f}\n", nthr * ITERS * 16 * 2 / (t * 1e-3) / 1e12, t);
   t = timeit([&] { k_dfma<<<blocks, threads>>>(dO, 0.999); });
   printf("{\"pipe\": \"dfma_fp64\", \"tflops\": %.2f, \"ms\": %.3f}\n", nthr * (ITERS / 4) * 16 * 2 / (t * 1e-3) / 1e12, t);
   t = timeit([&] { k_dmma<<<blocks, threads>>>(dO); });

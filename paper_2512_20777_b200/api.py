@@ -179,6 +179,93 @@ def expm_into(W: torch.Tensor, X: torch.Tensor, eps: float, scheme: str = SCHEME
             plan.get("e2"), plan.get("norms"), plan.get("mults"), plan.get("nonfinite"))
 
 
+class HostPipeline:
+    """Reusable host-buffer pipeline (pinned output + device staging buffers
+    allocated once), for serving loops that call the reference's calling
+    convention -- host memory in, host memory out (engine.py:119-152) -- over
+    and over.  ``run`` splits the batch into ``chunks`` pieces pipelined over
+    three CUDA streams, so the host->device copy of chunk c+1, the
+    exponentials of chunk c and the device->host copy of chunk c-1 overlap
+    (PCIe is full duplex)."""
+
+    def __init__(self, batch: int, n: int, dtype: torch.dtype = torch.float32, chunks: int = 8,
+                 device: int | torch.device | None = None):
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.B, self.n, self.dtype = int(batch), int(n), dtype
+        B = self.B
+        self.out = torch.empty((B, n, n), dtype=dtype, pin_memory=True)
+        self.host = {k: torch.empty(shape, dtype=dt, pin_memory=True) for k, shape, dt in (
+            ("m", (B,), torch.int8), ("s", (B,), torch.int8), ("e1", (B,), torch.float64),
+            ("e2", (B,), torch.float64), ("norms", (B, 2), torch.float64), ("mults", (B,), torch.int32),
+            ("nonfinite", (B,), torch.uint8))}
+        self.Wd = torch.empty((B, n, n), dtype=dtype, device=self.dev)
+        self.Xd = torch.empty_like(self.Wd)
+        self.pd = {k: torch.empty(v.shape, dtype=v.dtype, device=self.dev) for k, v in self.host.items()}
+        self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
+        c = max(1, min(int(chunks), B)) if B else 1
+        # chunk bounds on multiples of 4 matrices keep every slice 16-byte aligned
+        self.bounds = sorted({min(B, ((B * k) // c) // 4 * 4) for k in range(c)} | {B})
+        if self.bounds[0] != 0:
+            self.bounds = [0] + self.bounds
+        self.h2d_bytes = B * n * n * self.Wd.element_size()
+        self.d2h_bytes = self.h2d_bytes + sum(v.numel() * v.element_size() for v in self.host.values())
+
+    def run(self, W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, check_finite: bool = True) -> ExpmResult:
+        t0 = time.perf_counter()
+        if not isinstance(W, torch.Tensor) or W.device.type != "cpu":
+            raise MatrixError("HostPipeline.run takes a CPU tensor; use expm() for device tensors")
+        n = self.n
+        lead = W.shape[:-2]
+        Wf = W.reshape(-1, n, n)
+        if Wf.shape[0] != self.B or W.dtype != self.dtype:
+            raise MatrixError(f"pipeline built for {self.B} x {n}x{n} {self.dtype}, got {tuple(W.shape)} {W.dtype}")
+        if not Wf.is_contiguous():
+            Wf = Wf.contiguous()
+        check_tolerance(eps, W.dtype)
+        s_in, s_comp, s_out = self.streams
+        s_in.wait_stream(torch.cuda.current_stream(self.dev))
+        for a, b in zip(self.bounds[:-1], self.bounds[1:]):
+            if a == b:
+                continue
+            with torch.cuda.stream(s_in):
+                self.Wd[a:b].copy_(Wf[a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(ev_in)
+                expm_into(self.Wd[a:b], self.Xd[a:b], eps, scheme, {k: v[a:b] for k, v in self.pd.items()})
+                ev_c = torch.cuda.Event()
+                ev_c.record(s_comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_c)
+                self.out[a:b].copy_(self.Xd[a:b], non_blocking=True)
+                for k, v in self.host.items():
+                    v[a:b].copy_(self.pd[k][a:b], non_blocking=True)
+        s_out.synchronize()
+        h = self.host
+        bad = h["nonfinite"].bool()
+        if check_finite and self.B > 0 and bool(bad.any()):
+            idx = torch.nonzero(bad).flatten()[:8].tolist()
+            raise NonFiniteError(f"operation produced non-finite entries (batch indices {idx}...)")
+        plan = EvalPlan(h["m"].reshape(lead), h["s"].reshape(lead), scheme, h["e1"].reshape(lead),
+                        h["e2"].reshape(lead), h["norms"].reshape(*lead, 2))
+        return ExpmResult(self.out.reshape(*lead, n, n), plan, h["mults"].reshape(lead), time.perf_counter() - t0,
+                          bad.reshape(lead))
+
+
+def expm_host(W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, chunks: int = 8,
+              device: int | torch.device | None = None, check_finite: bool = True) -> ExpmResult:
+    """One-off host-buffer call: CPU tensor ``[..., n, n]`` in, pinned CPU
+    tensor out (see HostPipeline; results alias that pipeline's buffers)."""
+    if not isinstance(W, torch.Tensor) or W.device.type != "cpu":
+        raise MatrixError("expm_host takes a CPU tensor; use expm() for device tensors")
+    if W.dim() < 2 or W.shape[-1] != W.shape[-2] or W.shape[-1] < 1:
+        raise MatrixError(f"expected [..., n, n] square matrices, got shape {tuple(W.shape)}")
+    n = W.shape[-1]
+    pipe = HostPipeline(W.numel() // (n * n), n, W.dtype, chunks, device)
+    return pipe.run(W, eps, scheme, check_finite)
+
+
 def select_sastre(W: torch.Tensor, eps: float) -> EvalPlan:
     """select.py:228-234, batched (runs the full op; the plan is its by-product)."""
     return expm(W, eps, SCHEME_SASTRE, check_finite=False).plan

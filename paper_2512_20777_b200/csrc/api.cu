@@ -29,10 +29,10 @@ static int sm_count() {
   return cached[dev];
 }
 
-template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1)>
 static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
-  auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME>;
+  auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME, MINB>;
   static int occ = -1;  // per instantiation; identical on every B200
   if (occ < 0) {
     if (F::kSmem > 48 * 1024 &&
@@ -59,7 +59,15 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
   // atomics only added latency there (7% of stall samples).  EXPMB_CLAIM=1
   // forces dynamic claiming (A/B experiments).
   static const bool claim16 = getenv("EXPMB_CLAIM") && getenv("EXPMB_CLAIM")[0] == '1';
-  if (n <= 16) return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, claim16 ? ctr : nullptr, st);
+  static const int minb = getenv("EXPMB_C2_MINB") ? atoi(getenv("EXPMB_C2_MINB")) : 2;
+  if (n <= 16) {
+    int* c16 = claim16 ? ctr : nullptr;
+    if constexpr (sizeof(T) == 4) {
+      if (minb == 3) return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
+      if (minb == 4) return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
+    }
+    return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, c16, st);
+  }
   if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
   return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, ctr, st);
 }

@@ -381,8 +381,8 @@ enum FusedStep : int {
   ST_DONE
 };
 
-template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
-__global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, (NPAD == 16 && sizeof(T) == 4) ? 2 : 1)
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1)>
+__global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, MINB)
 expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, PlanOut po,
                   int* __restrict__ ctr) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;

@@ -292,3 +292,15 @@ def test_inverse_identity_fp64():
         I = torch.eye(n, dtype=torch.float64, device="cuda")
         d = torch.linalg.matrix_norm(F @ Bk - I) / math.sqrt(n)
         assert float(d.max()) <= 1e-10
+
+
+def test_host_pipeline_matches_device_path():
+    """Host-buffer entry (chunked 3-stream pipeline) == device path, bit for bit."""
+    W = torch.as_tensor(WL.generate("C2", batch=4100))  # not a multiple of the chunking
+    dev = X.expm(W.cuda(), 2.0 ** -24)
+    host = X.expm_host(W.pin_memory(), 2.0 ** -24, chunks=7)
+    assert host.value.device.type == "cpu"
+    assert torch.equal(host.value, dev.value.cpu())
+    assert torch.equal(host.plan.m, dev.plan.m.cpu()) and torch.equal(host.mults, dev.mults.cpu())
+    W64 = torch.as_tensor(WL.generate("C1", batch=37))
+    assert torch.equal(X.expm_host(W64, 2.0 ** -53, chunks=3).value, X.expm(W64.cuda(), 2.0 ** -53).value.cpu())

@@ -74,6 +74,9 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def mark(self, which):
+        (self.__dict__.setdefault("marks", {}))[which] = time.perf_counter()
+
     def _run_nvml(self):
         import pynvml as N
         N.nvmlInit()
@@ -90,8 +93,9 @@ class ClockSampler:
             except Exception:
                 r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
             act = [k for k, b in bits.items() if r & b]
-            self.rows.append([str(sm), str(mx), "", *["Active" if k in act else "Not Active" for k in bits]])
-            self._stop.wait(0.002)
+            self.rows.append([str(sm), str(mx), "", *["Active" if k in act else "Not Active" for k in bits],
+                              time.perf_counter()])
+            self._stop.wait(0.001)
 
     def _run(self):
         try:
@@ -119,6 +123,11 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
+        marks = getattr(self, "marks", {})
+        if "start" in marks and "end" in marks:
+            inwin = [r for r in self.rows if len(r) > 7 and marks["start"] <= r[7] <= marks["end"]]
+            if inwin:
+                self.rows = inwin
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -271,12 +280,15 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        time.sleep(0.05)  # let the sampler start
+        clk.mark("start")
         for i in range(args.steps):
             flush.zero_()
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if ws > 1:

@@ -239,8 +239,10 @@ class HostPipeline:
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_c)
                 self.out[a:b].copy_(self.Xd[a:b], non_blocking=True)
-                for k, v in self.host.items():
-                    v[a:b].copy_(self.pd[k][a:b], non_blocking=True)
+        with torch.cuda.stream(s_out):  # the small plan arrays: one copy each, after the last chunk
+            s_out.wait_stream(s_comp)
+            for k, v in self.host.items():
+                v.copy_(self.pd[k], non_blocking=True)
         s_out.synchronize()
         h = self.host
         bad = h["nonfinite"].bool()

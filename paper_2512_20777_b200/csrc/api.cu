@@ -33,13 +33,14 @@ template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPA
 static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME, MINB>;
+  constexpr size_t smem = F::kSmem + (MINB >= 3 ? GROUPS * F::kStageBytes : 0);
   static int occ = -1;  // per instantiation; identical on every B200
   if (occ < 0) {
-    if (F::kSmem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::kSmem) != cudaSuccess)
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return EXPMB_ERR_CUDA;
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, F::NT, F::kSmem) != cudaSuccess || o < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, F::NT, smem) != cudaSuccess || o < 1)
       return EXPMB_ERR_CUDA;
     occ = o;
   }
@@ -49,7 +50,7 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
   if (grid <= 0) return EXPMB_OK;
   // log2(eps) on the host: the same libm log2 as the reference's math.log2 (select.py:175)
   if (ctr != nullptr && cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  kern<<<grid, F::NT, F::kSmem, st>>>(W, X, batch, n, log2(eps), po, ctr);
+  kern<<<grid, F::NT, smem, st>>>(W, X, batch, n, log2(eps), po, ctr);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 

@@ -100,11 +100,13 @@ struct Fused {
   static constexpr size_t kSmemGroup = 2 * BUF * sizeof(T) + (WARPS_PG > 1 ? WARPS_PG * NPAD * sizeof(double) + 64 : 0);
   static_assert(BUF * sizeof(T) % 16 == 0, "operand buffers must stay 16-byte aligned");
   static constexpr size_t kSmem = GROUPS * kSmemGroup;
+  static constexpr size_t kStageBytes = (size_t)NPAD * NPAD * sizeof(T);
 
   using Tile = T[TM][4];
 
   int tr, tc, g, t;
   int soff;  // shared-memory offset (elements) of this thread's first row/column in a buffer
+  T* stage;  // next-matrix staging (lean variant only)
   T* buf0;
   T* buf1;
   double* red;
@@ -172,7 +174,39 @@ struct Fused {
     }
   }
 
+  template <bool DB = true>
   __device__ __forceinline__ void mm(const T* __restrict__ L, const T* __restrict__ R, Tile& acc) const {
+    if constexpr (sizeof(T) == 4 && !DB) {
+      // register-lean variant (3 CTAs/SM): operands loaded right before use
+      float2 acc2[TM][2];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) acc2[i][0] = acc2[i][1] = make_float2(0.f, 0.f);
+#pragma unroll(NPAD <= 16 ? NPAD / KV : 4)
+      for (int kb = 0; kb < NPAD; kb += KV) {
+        float a[TM][KV];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const float4 v = *reinterpret_cast<const float4*>(L + (tr + i * TR) * LD + kb);
+          a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+        }
+#pragma unroll
+        for (int kk = 0; kk < KV; ++kk) {
+          const float4 v = *reinterpret_cast<const float4*>(R + (kb + kk) * LD + (soff - tr * LD));
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float2 ai = make_float2(a[i][kk], a[i][kk]);
+            acc2[i][0] = ffma2(make_float2(v.x, v.y), ai, acc2[i][0]);
+            acc2[i][1] = ffma2(make_float2(v.z, v.w), ai, acc2[i][1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        acc[i][0] = acc2[i][0].x; acc[i][1] = acc2[i][0].y;
+        acc[i][2] = acc2[i][1].x; acc[i][3] = acc2[i][1].y;
+      }
+      return;
+    }
     T a[2][TM][KV], b[2][KV][4];
     ld_chunk(L, R, 0, a[0], b[0]);
     if constexpr (sizeof(T) == 4) {
@@ -387,7 +421,10 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
                   int* __restrict__ ctr) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   using Tile = typename F::Tile;
-  constexpr bool kPrefetch = !(NPAD == 64 && sizeof(T) == 8);  // register budget
+  // next-matrix prefetch: registers (default), or -- in the register-lean
+  // 3-CTA/SM variant -- cp.async into a per-group staging buffer
+  constexpr bool kLean = (MINB >= 3);
+  constexpr bool kPrefetch = !kLean && !(NPAD == 64 && sizeof(T) == 8);  // register budget
   extern __shared__ __align__(16) unsigned char smem_raw[];
   F f;
   f.g = threadIdx.x / F::TPG;
@@ -399,6 +436,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   f.buf0 = reinterpret_cast<T*>(gbase);
   f.buf1 = f.buf0 + F::BUF;
   f.red = reinterpret_cast<double*>(f.buf1 + F::BUF);
+  f.stage = reinterpret_cast<T*>(smem_raw + GROUPS * F::kSmemGroup + f.g * F::kStageBytes);
 
   const bool vec = (n == NPAD);
   const size_t nn = (size_t)n * n;
@@ -418,6 +456,18 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     nidx = f.next_index(idx, ctr, stride);
     if constexpr (kPrefetch) {
       if (nidx < batch) f.load(W + nidx * nn, n, vec, nxt);
+    }
+    if constexpr (kLean) {
+      if (vec && nidx < batch) {  // each lane stages exactly the elements it will read back
+        const T* src = W + nidx * nn;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const int off = f.row(i) * NPAD + f.col(0);
+          const uint32_t d = (uint32_t)__cvta_generic_to_shared(f.stage + off);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + off) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
     }
     bool bad = false;
     EW(bad |= !is_finite_t(B[i][j]));
@@ -495,7 +545,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       }
       // (2) the product
       f.sync();
-      f.mm(Lb, Rb, P);
+      f.template mm<!kLean>(Lb, Rb, P);
       f.sync();
       // (3) consume it, choose the next step
       if (step == ST_SQ) {
@@ -603,6 +653,19 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     }
     if constexpr (kPrefetch) {
       EW(B[i][j] = nxt[i][j]);
+    } else if constexpr (kLean) {
+      if (nidx < batch) {
+        if (vec) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float4 v = *reinterpret_cast<const float4*>(f.stage + f.row(i) * NPAD + f.col(0));
+            B[i][0] = v.x; B[i][1] = v.y; B[i][2] = v.z; B[i][3] = v.w;
+          }
+        } else {
+          f.load(W + nidx * nn, n, vec, B);
+        }
+      }
     } else {
       if (nidx < batch) f.load(W + nidx * nn, n, vec, B);
     }

@@ -192,8 +192,11 @@ __device__ __forceinline__ int simt_col(int tx, int j) {
   else return (j >> 1) * 32 + tx * 2 + (j & 1);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256, 1)
+// TWO: fp32 two-level accumulation (needed for long k: n > 512).  Without
+// it the kernel fits 128 registers and two CTAs share an SM, so one CTA's
+// prologue/epilogue overlaps the other's mainloop (short k at n <= 512).
+template <typename T, bool TWO = (sizeof(T) == 4)>
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
 gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   using C = SimtCfg<T>;
   constexpr int BK = C::BK, ST = C::STAGES, KV = C::KV, VW = C::VW;
@@ -247,7 +250,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 
   // fp32: two-level accumulation (a fresh partial every 32 k, added to the
   // running sum) keeps the summation error near (32 + n/32) u instead of n u.
-  constexpr bool kTwoLevel = sizeof(T) == 4;
+  constexpr bool kTwoLevel = sizeof(T) == 4 && TWO;
   constexpr int kChunkTiles = 32 / BK;
   T acc[8][8];
   float2 pacc[kTwoLevel ? 8 : 1][kTwoLevel ? 4 : 1];  // fp32 partials as FFMA2 pairs
@@ -442,13 +445,19 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
   static bool attr = false;
   constexpr int smem = simt_smem_bytes<T>();
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm_stage_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_stage_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(gemm_stage_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
       return 1;
     attr = true;
   }
   const int tn = (g.n + kGemmBN - 1) / kGemmBN, tm = (g.n + kGemmBM - 1) / kGemmBM;
   dim3 grid(tn, tm, count);
-  gemm_stage_kernel<T><<<grid, 256, smem, st>>>(g, stage, list);
+  if (sizeof(T) == 4 && g.n > 512)
+    gemm_stage_kernel<T, true><<<grid, 256, smem, st>>>(g, stage, list);
+  else
+    gemm_stage_kernel<T, false><<<grid, 256, smem, st>>>(g, stage, list);
   return cudaGetLastError() != cudaSuccess;
 }
 

@@ -38,6 +38,10 @@ extern "C" {
 /* scheme codes: select.py:58-61 SCHEME_SASTRE / SCHEME_PS */
 #define EXPMB_SASTRE 0
 #define EXPMB_PS 1
+/* Alg. 1 term accumulation, the paper's comparator: engine.py:90-116
+ * (expm_baseline); n <= 64 only.  m = terms added, s may exceed int8 (the
+ * m/s outputs saturate at 127; mults = m + s is exact). */
+#define EXPMB_BASELINE 2
 
 /* return codes */
 #define EXPMB_OK 0
@@ -48,6 +52,7 @@ extern "C" {
 #define EXPMB_ERR_WORKSPACE (-5)   /* workspace missing or too small               */
 #define EXPMB_ERR_CUDA (-6)        /* a CUDA launch/copy failed                    */
 #define EXPMB_ERR_ALIGN (-7)       /* W/X not 16-byte aligned                      */
+#define EXPMB_ERR_UNSUPPORTED (-8) /* valid but unsupported combination            */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int expmb_version(void);

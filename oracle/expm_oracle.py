@@ -26,6 +26,7 @@ Reference map (file:line under /root/reference/pkg/src/expmkit):
   * sastre_budget .......................... poly.py:233-241
   * expm driver ............................ engine.py:119-152
   * squaring ............................... engine.py:80-87
+  * expm_baseline (Alg. 1) .................. engine.py:90-116
   * finiteness semantics (_wrap) ........... matrix.py:56-57, 95-102
 """
 
@@ -411,3 +412,29 @@ def _plan_from_norms(norm1: float, norm2: float, eps: float):
             continue
         s = max(s, math.ceil((l - log_eps) / (m + tt)))
     return (m, min(s, MAX_SCALING))
+
+
+def expm_baseline(W, eps: float, tol_floor: float = UNIT_ROUNDOFF) -> Result:
+    """engine.py:90-116 restated: norm-halving scaling, term accumulation until
+    the next term's 1-norm is <= eps, s squarings; mults = m + s."""
+    W = np.array(W, dtype=np.float64)
+    if not np.isfinite(W).all():
+        raise NonFiniteError("matrix entries must be finite")
+    eps = check_tolerance(eps, tol_floor)
+    ledger = [0]
+    s = 0
+    norm1 = one_norm(W)
+    while math.ldexp(norm1, -s) >= 0.5:
+        s += 1
+    B = _scale(W, s)
+    n = W.shape[0]
+    X = np.eye(n)
+    Y = B
+    k = 2
+    while one_norm(Y) > eps:
+        X = _wrap(X + Y)
+        Y = _wrap(_mm(B, Y, ledger) / k)
+        k += 1
+    for _ in range(s):
+        X = _mm(X, X, ledger)
+    return Result(X, k - 2, s, one_norm(Y), 0.0, norm1, float("nan"), ledger[0])

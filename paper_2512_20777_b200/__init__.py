@@ -11,7 +11,7 @@ from .tables import (  # noqa: F401
     ToleranceError, ps_shape, sastre_budget,
 )
 from .api import (  # noqa: F401
-    EvalPlan, ExpmResult, HostPipeline, check_tolerance, expm, expm_host, expm_into, select_ps, select_sastre,
+    EvalPlan, ExpmResult, HostPipeline, SCHEME_BASELINE, check_tolerance, expm, expm_baseline, expm_host, expm_into, select_ps, select_sastre,
 )
 
 __version__ = "0.1.0"

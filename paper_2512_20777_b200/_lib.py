@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libexpmb.so")
 
 EXPMB_F32, EXPMB_F64 = 0, 1
-EXPMB_SASTRE, EXPMB_PS = 0, 1
+EXPMB_SASTRE, EXPMB_PS, EXPMB_BASELINE = 0, 1, 2
 
 ERR_TOLERANCE = -1
 ERR_SHAPE = -2
@@ -22,6 +22,7 @@ ERR_DTYPE = -4
 ERR_WORKSPACE = -5
 ERR_CUDA = -6
 ERR_ALIGN = -7
+ERR_UNSUPPORTED = -8
 
 # Every symbol include/expmb.h declares (tests check the .so exports them all).
 EXPORTS = (

@@ -30,6 +30,7 @@ from .tables import (MatrixError, NonFiniteError, SCHEME_PS, SCHEME_SASTRE, Tole
                      UNIT_ROUNDOFF, UNIT_ROUNDOFF_F32)
 
 _SCHEMES = {SCHEME_SASTRE: _lib.EXPMB_SASTRE, SCHEME_PS: _lib.EXPMB_PS}
+SCHEME_BASELINE = "baseline"  # select.py:58
 
 
 @dataclass
@@ -71,7 +72,7 @@ def check_tolerance(eps: float, dtype: torch.dtype = torch.float64) -> float:
 def _raise_rc(rc: int):
     if rc == _lib.ERR_TOLERANCE:
         raise ToleranceError(_lib.strerror(rc))
-    if rc in (_lib.ERR_SHAPE, _lib.ERR_SCHEME, _lib.ERR_DTYPE):
+    if rc in (_lib.ERR_SHAPE, _lib.ERR_SCHEME, _lib.ERR_DTYPE, _lib.ERR_UNSUPPORTED):
         raise MatrixError(_lib.strerror(rc))
     raise RuntimeError(f"libexpmb: {_lib.strerror(rc)} (code {rc})")
 
@@ -124,14 +125,14 @@ def _(W, eps, scheme):
             W.new_empty(B, dtype=torch.uint8))
 
 
-def _validate(W: torch.Tensor, eps: float, scheme: str) -> tuple[torch.Tensor, int]:
+def _validate(W: torch.Tensor, eps: float, scheme: str, allow_baseline: bool = False) -> tuple[torch.Tensor, int]:
     if not isinstance(W, torch.Tensor):
         raise MatrixError(f"expected a torch.Tensor, got {type(W).__name__}")
     if W.dim() < 2 or W.shape[-1] != W.shape[-2]:
         raise MatrixError(f"expected [..., n, n] square matrices, got shape {tuple(W.shape)}")
     if W.shape[-1] < 1:
         raise MatrixError("matrix order must be at least 1")
-    if scheme not in _SCHEMES:
+    if scheme not in _SCHEMES and not (allow_baseline and scheme == SCHEME_BASELINE):
         raise MatrixError(f"unknown scheme {scheme!r}; expected 'ps' or 'sastre'")
     if W.dtype not in (torch.float32, torch.float64):
         raise MatrixError(f"dtype must be float32 or float64, got {W.dtype}")
@@ -141,7 +142,7 @@ def _validate(W: torch.Tensor, eps: float, scheme: str) -> tuple[torch.Tensor, i
     Wc = W.reshape(-1, W.shape[-1], W.shape[-1])
     if not Wc.is_contiguous() or Wc.data_ptr() % 16:
         Wc = Wc.contiguous().clone()
-    return Wc, _SCHEMES[scheme]
+    return Wc, _SCHEMES.get(scheme, _lib.EXPMB_BASELINE)
 
 
 def expm(W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, check_finite: bool = True) -> ExpmResult:
@@ -165,13 +166,32 @@ def expm(W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, check_finite:
                       bad.reshape(lead))
 
 
+def expm_baseline(W: torch.Tensor, eps: float, check_finite: bool = True) -> ExpmResult:
+    """Alg. 1, the paper's comparator (engine.py:90-116): scale until the
+    1-norm is below 1/2, add Taylor terms B^k/k! until the next term's 1-norm
+    is at most eps, square back.  plan.m = terms added, plan.e1 = the norm of
+    the first term not added, mults = m + s (test_engine.py:83-97).  n <= 64."""
+    t0 = time.perf_counter()
+    Wc, code = _validate(W, eps, SCHEME_BASELINE, allow_baseline=True)
+    lead, n = W.shape[:-2], W.shape[-1]
+    X, m, s, e1, e2, norms, mults, nonfinite = torch.ops.expmkit_b200.expm(Wc, float(eps), code)
+    bad = nonfinite.bool()
+    if check_finite and Wc.shape[0] > 0 and bool(bad.any()):
+        idx = torch.nonzero(bad).flatten()[:8].tolist()
+        raise NonFiniteError(f"operation produced non-finite entries (batch indices {idx}...)")
+    plan = EvalPlan(m.reshape(lead), s.reshape(lead), SCHEME_BASELINE, e1.reshape(lead), e2.reshape(lead),
+                    norms.reshape(*lead, 2))
+    return ExpmResult(X.reshape(*lead, n, n), plan, mults.reshape(lead), time.perf_counter() - t0,
+                      bad.reshape(lead))
+
+
 def expm_into(W: torch.Tensor, X: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE,
               plan: dict | None = None) -> None:
     """Allocation-free variant for steady-state loops and CUDA graphs:
     writes e^W into the preallocated ``X`` (same shape/dtype) and, if given,
     into the plan tensors of ``plan`` (keys m, s, e1, e2, norms, mults, nonfinite).
     No host synchronisation for n <= 64."""
-    Wc, code = _validate(W, eps, scheme)
+    Wc, code = _validate(W, eps, scheme, allow_baseline=True)
     if X.shape != W.shape or X.dtype != W.dtype or not X.is_contiguous():
         raise MatrixError("X must be a contiguous tensor shaped and typed like W")
     plan = plan or {}

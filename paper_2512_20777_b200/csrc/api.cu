@@ -50,7 +50,7 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
   if (grid <= 0) return EXPMB_OK;
   // log2(eps) on the host: the same libm log2 as the reference's math.log2 (select.py:175)
   if (ctr != nullptr && cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  kern<<<grid, F::NT, smem, st>>>(W, X, batch, n, log2(eps), po, ctr);
+  kern<<<grid, F::NT, smem, st>>>(W, X, batch, n, log2(eps), eps, po, ctr);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
@@ -86,11 +86,12 @@ const char* expmb_strerror(int code) {
     case EXPMB_OK: return "ok";
     case EXPMB_ERR_TOLERANCE: return "tolerance NaN or below the unit roundoff of the dtype";
     case EXPMB_ERR_SHAPE: return "matrix order must be at least 1 and batch non-negative";
-    case EXPMB_ERR_SCHEME: return "unknown scheme; expected sastre (0) or ps (1)";
+    case EXPMB_ERR_SCHEME: return "unknown scheme; expected sastre (0), ps (1) or baseline (2)";
     case EXPMB_ERR_DTYPE: return "dtype must be fp32 (0) or fp64 (1)";
     case EXPMB_ERR_WORKSPACE: return "workspace missing or smaller than expmb_workspace_bytes()";
     case EXPMB_ERR_CUDA: return "CUDA launch or copy failed";
     case EXPMB_ERR_ALIGN: return "W and X must be 16-byte aligned";
+    case EXPMB_ERR_UNSUPPORTED: return "combination not supported (baseline scheme needs n <= 64)";
     default: return "unknown error";
   }
 }
@@ -136,7 +137,8 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
                int8_t* s, double* e1, double* e2, double* norms, int32_t* mults, uint8_t* nonfinite, void* workspace,
                size_t workspace_bytes, void* stream) {
   if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
-  if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS) return EXPMB_ERR_SCHEME;
+  if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS && scheme != EXPMB_BASELINE) return EXPMB_ERR_SCHEME;
+  if (scheme == EXPMB_BASELINE && n > 64) return EXPMB_ERR_UNSUPPORTED;
   if (n < 1 || batch < 0) return EXPMB_ERR_SHAPE;
   if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
   if (((uintptr_t)W | (uintptr_t)X) & 15u) return EXPMB_ERR_ALIGN;
@@ -147,11 +149,17 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
     // optional: with a workspace the kernel claims matrices dynamically
     int* ctr = (workspace != nullptr && workspace_bytes >= sizeof(int)) ? (int*)workspace : nullptr;
     if (dtype == EXPMB_F32) {
-      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>((const float*)W, (float*)X, batch, n, eps, po, ctr, st)
-                                    : dispatch_small<float, 1>((const float*)W, (float*)X, batch, n, eps, po, ctr, st);
+      const float* w = (const float*)W;
+      float* x = (float*)X;
+      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>(w, x, batch, n, eps, po, ctr, st)
+             : scheme == EXPMB_PS   ? dispatch_small<float, 1>(w, x, batch, n, eps, po, ctr, st)
+                                    : dispatch_small<float, 2>(w, x, batch, n, eps, po, ctr, st);
     }
-    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>((const double*)W, (double*)X, batch, n, eps, po, ctr, st)
-                                  : dispatch_small<double, 1>((const double*)W, (double*)X, batch, n, eps, po, ctr, st);
+    const double* w = (const double*)W;
+    double* x = (double*)X;
+    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>(w, x, batch, n, eps, po, ctr, st)
+           : scheme == EXPMB_PS   ? dispatch_small<double, 1>(w, x, batch, n, eps, po, ctr, st)
+                                  : dispatch_small<double, 2>(w, x, batch, n, eps, po, ctr, st);
   }
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;

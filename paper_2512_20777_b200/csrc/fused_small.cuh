@@ -417,8 +417,8 @@ enum FusedStep : int {
 
 template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1)>
 __global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, MINB)
-expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, PlanOut po,
-                  int* __restrict__ ctr) {
+expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, double eps,
+                  PlanOut po, int* __restrict__ ctr) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
   using Tile = typename F::Tile;
   // next-matrix prefetch: registers (default), or -- in the register-lean
@@ -478,6 +478,45 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     nrm[1] = nrm[2] = nrm[3] = NAN;
     Plan p{0, 0, 0.0, 0.0};
     Tile A2, Y0, Y1, P;  // A^2 (PS: also q), y02 (PS: A^3), y12 (PS: A^4), product
+    int mults = 0;
+    if constexpr (SCHEME == 2) {
+      // ---- Alg. 1 term accumulation (engine.py:90-116) --------------------
+      // s: smallest s >= 0 with ||W||_1 2^-s < 1/2 (engine.py:102-104)
+      int s = 0;
+      if (nrm[0] >= 0.5) {
+        int e;
+        frexp(nrm[0], &e);                // ||W||_1 = f 2^e, f in [1/2, 1)
+        s = (nrm[0] <= 1e300) ? e + 1 : 1100;
+      }
+      const T sc = s <= 126 ? pow2_neg<T>(s) : T(0);
+      EW(B[i][j] *= sc);                  // B = 2^-s W (exact)
+      EW(P[i][j] = DG(i, j));             // X = I
+      EW(Y0[i][j] = B[i][j]);             // Y = B
+      f.store(f.buf0, B);                 // B is the left factor of every term product
+      int k = 2;
+      double ny = f.norm1(Y0);
+      while (ny > eps && k < 400) {       // engine.py:109-112
+        EW(P[i][j] += Y0[i][j]);
+        f.store(f.buf1, Y0);
+        f.sync();
+        f.template mm<!kLean>(f.buf0, f.buf1, Y1);
+        f.sync();
+        const T rk = T(1) / T(k);
+        EW(Y0[i][j] = Y1[i][j] * rk);     // Y = B Y / k (x/k taken as x * fl(1/k))
+        ++k;
+        ny = f.norm1(Y0);
+      }
+      for (int q = 0; q < s && q < 1100; ++q) {  // engine.py:113
+        Tile Q;
+        f.square(P, Q);
+        EW(P[i][j] = Q[i][j]);
+      }
+      p.m = k - 2;
+      p.s = s;
+      p.e1 = ny;
+      p.e2 = 0.0;
+      mults = (k - 2) + s;
+    } else {
     int have = 1, step = ST_DONE, q = 0, hz = 0;
     if (nrm[0] != 0.0) {
       int need = SCHEME == 0 ? select_sastre_fast(nrm[0], 0.0, 1, log_eps, &p) : -1;
@@ -636,19 +675,22 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       }
     }
 
+    mults = budget(p.m, SCHEME) + p.s;
+    }  // SCHEME != 2
+
     EW(bad |= !is_finite_t(P[i][j]));
     bad = f.any_group(bad);
     f.save(X + idx * nn, n, vec, P);
     if (f.t == 0) {
-      if (po.m) po.m[idx] = (int8_t)p.m;
-      if (po.s) po.s[idx] = (int8_t)p.s;
+      if (po.m) po.m[idx] = (int8_t)(p.m < 127 ? p.m : 127);  // Alg. 1 may exceed int8: saturate
+      if (po.s) po.s[idx] = (int8_t)(p.s < 127 ? p.s : 127);
       if (po.e1) po.e1[idx] = p.e1;
       if (po.e2) po.e2[idx] = p.e2;
       if (po.norms) {
         po.norms[2 * idx] = nrm[0];
         po.norms[2 * idx + 1] = nrm[1];
       }
-      if (po.mults) po.mults[idx] = budget(p.m, SCHEME) + p.s;
+      if (po.mults) po.mults[idx] = mults;
       if (po.nonfinite) po.nonfinite[idx] = (uint8_t)(bad || !(nrm[0] <= INFINITY));
     }
     if constexpr (kPrefetch) {

@@ -74,14 +74,17 @@ def main():
     ms, ss, e1s, e2s, mults, raised = [], [], [], [], [], []
     ins, outs = [], []
     for name, W, eps in cases():
-        for scheme in ("sastre", "ps"):
+        for scheme in ("sastre", "ps", "baseline"):
+            if scheme == "baseline" and (W.shape[0] > 64 or not np.isfinite(W).all() or np.abs(W).max() > 1e12):
+                continue
             names.append(name)
             ns.append(W.shape[0])
             epss.append(eps)
             schemes.append(scheme)
             ins.append(np.asarray(W, np.float64).ravel())
             try:
-                r = expmkit.expm(Matrix(W), eps, scheme)
+                r = (expmkit.expm_baseline(Matrix(W), eps) if scheme == "baseline"
+                     else expmkit.expm(Matrix(W), eps, scheme))
             except NonFiniteError:
                 raised.append(True)
                 ms.append(-1); ss.append(-1); e1s.append(math.nan); e2s.append(math.nan)

@@ -118,7 +118,7 @@ def test_host_selector_golden(golden):
     """Selector on the reference's own plans (norms recomputed here in binary64)."""
     offs = golden["offsets"]
     for i in range(len(golden["names"])):
-        if golden["raised"][i]:
+        if golden["raised"][i] or str(golden["scheme"][i]) == "baseline":
             continue
         n = int(golden["n"][i])
         W = golden["W"][offs[i]:offs[i + 1]].reshape(n, n)

@@ -25,9 +25,9 @@ def test_oracle_bit_exact_vs_reference(golden):
     for i, name, W, X, eps, scheme in _cases(golden):
         if golden["raised"][i]:
             with pytest.raises(O.NonFiniteError):
-                O.expm(W, eps, scheme)
+                O.expm_baseline(W, eps) if scheme == "baseline" else O.expm(W, eps, scheme)
             continue
-        r = O.expm(W, eps, scheme)
+        r = O.expm_baseline(W, eps) if scheme == "baseline" else O.expm(W, eps, scheme)
         assert (r.m, r.s, r.mults) == (golden["m"][i], golden["s"][i], golden["mults"][i]), name
         assert r.e1 == golden["e1"][i] or (math.isinf(r.e1) and math.isinf(golden["e1"][i])), name
         assert r.e2 == golden["e2"][i] or (math.isinf(r.e2) and math.isinf(golden["e2"][i])), name

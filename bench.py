@@ -265,14 +265,17 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        XP.expm_into(W, Xd, cfg.eps, "sastre", plan)
+        XP.expm_into(W, Xd, cfg.eps, args.scheme, plan)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     m = plan["m"].cpu().numpy(); s = plan["s"].cpu().numpy()
     assert not plan["nonfinite"].any(), "non-finite results in the bench batch"
-    flops = WL.useful_flops(m, s, cfg.n)
+    if args.scheme == "baseline":  # mults = m + s (the int8 m/s outputs saturate; mults does not)
+        flops = float(plan["mults"].double().sum().item()) * 2.0 * cfg.n ** 3
+    else:
+        flops = WL.useful_flops(m, s, cfg.n, args.scheme)
 
     # ---- device-timed steps, L2 flushed between steps ----------------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -303,7 +306,7 @@ def run_ours(args):
     pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if cfg.n <= 64 else 1, device=dev)
 
     def e2e_step():
-        pipe.run(Wp, cfg.eps, "sastre", check_finite=False)
+        pipe.run(Wp, cfg.eps, args.scheme, check_finite=False)
 
     for _ in range(2):
         e2e_step()
@@ -374,7 +377,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
             "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch_per_gpu": B, "global_batch": ws * B,
-                       "n": cfg.n, "eps": cfg.eps, "scheme": "sastre", "l2": "flushed between steps (252 MB write)",
+                       "n": cfg.n, "eps": cfg.eps, "scheme": args.scheme, "l2": "flushed between steps (252 MB write)",
                        "parallelism": f"batch-sharded x{ws}, no collective on the hot path"},
             "useful_tflops": tflops, "hbm_gbs": gbs,
             "roofline": roof,
@@ -384,6 +387,7 @@ def run_ours(args):
             "gpu_launches": _launch_count(cfg.key, m, s, cfg.n) * args.steps,
             "clocks": clk.summary(),
             "plan_histogram": hist,
+            "mults_total": int(plan["mults"].long().sum().item()),
             "gather_ms": gather_ms,
         }
         print(json.dumps(line), flush=True)
@@ -401,6 +405,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scheme", default="sastre", choices=["sastre", "ps", "baseline"],
+                    help="evaluation route (baseline = Alg. 1, the paper's comparator; n <= 64)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -80,6 +80,51 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return *reinterpret_cast<float2*>(&d);
 }
 
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b), d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b), d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// Column pairs of a tile row for the elementwise formula work: packed
+// FFMA2/FADD2/FMUL2 for fp32 (half the instructions), two scalar ops for fp64.
+template <typename T>
+struct Pr {
+  T x, y;
+};
+template <typename T>
+__device__ __forceinline__ Pr<T> pfma(Pr<T> a, T c, Pr<T> b) {  // a*c + b
+  if constexpr (sizeof(T) == 4) {
+    const float2 r = ffma2(make_float2(a.x, a.y), make_float2(c, c), make_float2(b.x, b.y));
+    return Pr<T>{r.x, r.y};
+  } else {
+    return Pr<T>{fma(a.x, c, b.x), fma(a.y, c, b.y)};
+  }
+}
+template <typename T>
+__device__ __forceinline__ Pr<T> padd(Pr<T> a, Pr<T> b) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 r = fadd2(make_float2(a.x, a.y), make_float2(b.x, b.y));
+    return Pr<T>{r.x, r.y};
+  } else {
+    return Pr<T>{a.x + b.x, a.y + b.y};
+  }
+}
+template <typename T>
+__device__ __forceinline__ Pr<T> pmul(Pr<T> a, T c) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 r = fmul2(make_float2(a.x, a.y), make_float2(c, c));
+    return Pr<T>{r.x, r.y};
+  } else {
+    return Pr<T>{a.x * c, a.y * c};
+  }
+}
+
 __device__ __forceinline__ bool is_finite_t(float x) { return isfinite(x); }
 __device__ __forceinline__ bool is_finite_t(double x) { return isfinite(x); }
 
@@ -448,6 +493,18 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   _Pragma("unroll") for (int i = 0; i < TM; ++i) \
   _Pragma("unroll") for (int j = 0; j < 4; ++j) { expr; }
 #define DG(i, j) (f.is_diag(i, j) ? T(1) : T(0))
+  // pairwise elementwise loops: X(i,q) is column pair q (0, 1) of row i
+#define EW2(expr)                                  \
+  _Pragma("unroll") for (int i = 0; i < TM; ++i)  \
+  _Pragma("unroll") for (int q = 0; q < 2; ++q) { expr; }
+#define GP(t) (Pr<T>{t[i][2 * q], t[i][2 * q + 1]})
+#define SP(t, v)                              \
+  {                                           \
+    const Pr<T> _v = (v);                     \
+    t[i][2 * q] = _v.x;                       \
+    t[i][2 * q + 1] = _v.y;                   \
+  }
+#define DGP (Pr<T>{DG(i, 2 * q), DG(i, 2 * q + 1)})
 
   Tile B;  // W, later 2^-s W
   Tile nxt;
@@ -531,7 +588,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       // exact 2^-s rescaling of W and the cached powers (engine.py:139-140)
       sc = pow2_neg<T>(p.s);
       sc2 = pow2_neg<T>(2 * p.s);
-      EW(B[i][j] *= sc; A2[i][j] *= sc2);
+      EW2(SP(B, pmul(GP(B), sc)); SP(A2, pmul(GP(A2), sc2)));
     };
     // ---- the per-matrix program ------------------------------------------
     while (step != ST_DONE) {
@@ -558,27 +615,26 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
         if (step == ST_T4) {
           Tile L;
           // (A2/4 + A)/3 + I; x/3 taken as x * fl(1/3) (<= 1 ulp from the division)
-          EW(L[i][j] = (A2[i][j] * T(0.25) + B[i][j]) * T(1.0 / 3.0) + DG(i, j));
+          EW2(SP(L, padd(pmul(pfma(GP(A2), T(0.25), GP(B)), T(1.0 / 3.0)), DGP)));
           f.store(f.buf0, L);
           f.store(f.buf1, A2);
         } else if (step == ST_Y02) {
           const T c0 = (T)c[0], c1 = (T)c[1];
           Tile R;
-          EW(R[i][j] = c0 * A2[i][j] + c1 * B[i][j]);
+          EW2(SP(R, pfma(GP(A2), c0, pmul(GP(B), c1))));
           f.store(f.buf0, A2);
           f.store(f.buf1, R);
         } else if (step == ST_P2) {
           const T c2 = (T)c[2], c3 = (T)c[3], c4 = (T)c[4];
           Tile L, R;
-          EW(L[i][j] = (Y0[i][j] + c2 * A2[i][j]) + c3 * B[i][j]; R[i][j] = Y0[i][j] + c4 * A2[i][j]);
+          EW2(SP(L, pfma(GP(B), c3, pfma(GP(A2), c2, GP(Y0)))); SP(R, pfma(GP(A2), c4, GP(Y0))));
           f.store(f.buf0, L);
           f.store(f.buf1, R);
         } else {  // ST_P3
           const T c7 = (T)c[7], c8 = (T)c[8], c9 = (T)c[9], c10 = (T)c[10];
           Tile L, R;
-          EW(L[i][j] = (Y1[i][j] + c7 * A2[i][j]) + c8 * B[i][j];
-             R[i][j] = (Y1[i][j] + c9 * Y0[i][j]) + c10 * B[i][j]);
-          f.store(f.buf0, L);
+          EW2(SP(L, pfma(GP(B), c8, pfma(GP(A2), c7, GP(Y1))));
+              SP(R, pfma(GP(B), c10, pfma(GP(Y0), c9, GP(Y1)))));         f.store(f.buf0, L);
           f.store(f.buf1, R);
         }
       }
@@ -623,7 +679,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
           step = kk >= 2 ? ST_HORNER : (p.s > 0 ? ST_SQ : ST_DONE);
         } else {
           if (p.m == 2) {  // poly.py:196
-            EW(P[i][j] = (A2[i][j] * T(0.5) + B[i][j]) + DG(i, j));
+            EW2(SP(P, padd(pfma(GP(A2), T(0.5), GP(B)), DGP)));
             step = ST_DONE;
           } else {
             step = p.m == 4 ? ST_T4 : ST_Y02;
@@ -640,7 +696,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
         step = (--hz >= 0) ? ST_HORNER : (p.s > 0 ? ST_SQ : ST_DONE);
       } else if (SCHEME == 0) {
         if (step == ST_T4) {  // poly.py:199
-          EW(P[i][j] = (P[i][j] * T(0.5) + B[i][j]) + DG(i, j));
+          EW2(SP(P, padd(pfma(GP(P), T(0.5), GP(B)), DGP)));
           step = ST_DONE;  // m = 4 implies s = 0
         } else if (step == ST_Y02) {
           EW(Y0[i][j] = P[i][j]);
@@ -649,17 +705,17 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
           const double* c = (p.m == 8) ? kT8 : kT15;
           if (p.m == 8) {  // poly.py:211
             const T c5 = (T)c[5];
-            EW(P[i][j] = (((P[i][j] + c5 * Y0[i][j]) + A2[i][j] * T(0.5)) + B[i][j]) + DG(i, j));
+            EW2(SP(P, padd(padd(pfma(GP(A2), T(0.5), pfma(GP(Y0), c5, GP(P))), GP(B)), DGP)));
             step = ST_DONE;  // m = 8 implies s = 0
           } else {  // poly.py:222-223
             const T c5 = (T)c[5], c6 = (T)c[6];
-            EW(Y1[i][j] = (P[i][j] + c5 * Y0[i][j]) + c6 * A2[i][j]);
+            EW2(SP(Y1, pfma(GP(A2), c6, pfma(GP(Y0), c5, GP(P)))));
             step = ST_P3;
           }
         } else {  // ST_P3 -> y22 (poly.py:224-229)
           const T c11 = (T)kT15[11], c12 = (T)kT15[12], c13 = (T)kT15[13], c14 = (T)kT15[14], c15 = (T)kT15[15];
-          EW(P[i][j] = ((((P[i][j] + c11 * Y1[i][j]) + c12 * Y0[i][j]) + c13 * A2[i][j]) + c14 * B[i][j]) +
-                       (f.is_diag(i, j) ? c15 : T(0)));
+          EW2(SP(P, padd(pfma(GP(B), c14, pfma(GP(A2), c13, pfma(GP(Y0), c12, pfma(GP(Y1), c11, GP(P))))),
+                         pmul(DGP, c15))));
           step = p.s > 0 ? ST_SQ : ST_DONE;
         }
       }
@@ -714,6 +770,10 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   }
 #undef EW
 #undef DG
+#undef EW2
+#undef GP
+#undef SP
+#undef DGP
 }
 
 }  // namespace expmb

@@ -56,7 +56,7 @@ struct LargeLayout {
   size_t mat_bytes;
   int nbufs;
   int tiles_m;
-  size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_m, off_s, off_e1, off_e2, off_list, total;
+  size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_flags, off_m, off_s, off_e1, off_e2, off_list, total;
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -78,6 +78,7 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.off_norm1 = off; off += align256((size_t)chunk * 4 * sizeof(double));
   L.off_norm2 = off; off += 0;  // norms for powers 1..4 live in the same [chunk][4] array
   L.off_need = off; off += align256((size_t)chunk * sizeof(int));
+  L.off_flags = off; off += align256((size_t)chunk * sizeof(int));
   L.off_m = off; off += align256((size_t)chunk);
   L.off_s = off; off += align256((size_t)chunk);
   L.off_e1 = off; off += align256((size_t)chunk * sizeof(double));
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
                                                 int8_t* __restrict__ ps, double* __restrict__ pe1,
                                                 double* __restrict__ pe2) {
   const int z = blockIdx.x;
-  if (need[z] != have) return;  // this matrix did not form W^have
+  if (have > 1 && need[z] != have) return;  // this matrix did not form W^have
   __shared__ double red[256];
   const double* pz = part + (size_t)z * tiles_m * n;
   double mx = -INFINITY;
@@ -157,12 +158,14 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
   }
   if (threadIdx.x == 0) {
     nrm4[4 * z + have - 1] = red[0];
+    if (have == 1) nrm4[4 * z + 1] = NAN;
     double nr[4];
     for (int q = 0; q < 4; ++q) nr[q] = nrm4[4 * z + q];
-    Plan p{};
+    Plan p{0, 0, 0.0, 0.0};
     double lw[4];
     for (int q = 0; q < have; ++q) lw[q] = log2_or_ninf(nr[q]);
-    const int nd = select_walk_lw(lw, have, eps, scheme, &p);  // eps carries log2(eps)
+    int nd = 0;
+    if (nr[0] != 0.0) nd = select_walk_lw(lw, have, eps, scheme, &p);  // eps carries log2(eps)
     need[z] = nd;
     if (nd == 0) {
       pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
@@ -170,20 +173,44 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
   }
 }
 
-// Per-matrix outputs + non-finite scan of the final X (and of W).
+// Column abs-sum partials of W over 128-row slabs: grid (col blocks, slabs,
+// matrices), one thread per column, coalesced row reads (select.py:169).
 template <typename T>
-__global__ void __launch_bounds__(256) k_finish(const T* __restrict__ W, const T* __restrict__ X, int n, int scheme,
-                                                const double* __restrict__ nrm4, const int8_t* __restrict__ pm,
-                                                const int8_t* __restrict__ ps, const double* __restrict__ pe1,
-                                                const double* __restrict__ pe2, int64_t base, PlanOut po) {
-  const int z = blockIdx.x;
+__global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ W, int n, int64_t wstride,
+                                                        double* __restrict__ part, int tiles_m) {
+  const int z = blockIdx.z, c = blockIdx.x * 256 + threadIdx.x, r0 = blockIdx.y * kGemmBM;
+  if (c >= n) return;
+  const T* w = W + (int64_t)z * wstride;
+  const int r1 = min(n, r0 + kGemmBM);
+  double a = 0.0;
+  for (int r = r0; r < r1; ++r) a += fabs((double)w[(size_t)r * n + c]);
+  part[((size_t)z * tiles_m + blockIdx.y) * n + c] = a;
+}
+
+// Non-finite scan of the final values, spread over many CTAs per matrix.
+template <typename T>
+__global__ void __launch_bounds__(256) k_nonfinite(const T* __restrict__ X, int n, int64_t xstride,
+                                                   int* __restrict__ flags) {
+  const int z = blockIdx.y;
+  const T* x = X + (int64_t)z * xstride;
   const size_t nn = (size_t)n * n;
-  const T* x = X + (size_t)z * nn;
-  const T* w = W + (size_t)z * nn;
   int bad = 0;
-  for (size_t i = threadIdx.x; i < nn; i += blockDim.x) bad |= !(isfinite(x[i]) && isfinite(w[i]));
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
   bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
+  if (bad && threadIdx.x == 0) atomicOr(flags + z, 1);
+}
+
+// Per-matrix outputs + non-finite scan of the final X (and of W).
+// Per-matrix outputs.  A non-finite input shows in ||W||_1 (NaN / Inf
+// propagate through the abs-sums); non-finite outputs come from k_nonfinite.
+__global__ void __launch_bounds__(256) k_finish(int cnt, int scheme, const double* __restrict__ nrm4,
+                                                const int8_t* __restrict__ pm, const int8_t* __restrict__ ps,
+                                                const double* __restrict__ pe1, const double* __restrict__ pe2,
+                                                const int* __restrict__ flags, int64_t base, PlanOut po) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  if (z < cnt) {
+    const int bad = flags[z];
     const int64_t g = base + z;
     const int m = pm[z], s = ps[z];
     const double n1 = nrm4[4 * z], n2 = nrm4[4 * z + 1];
@@ -193,13 +220,35 @@ __global__ void __launch_bounds__(256) k_finish(const T* __restrict__ W, const T
     if (po.e2) po.e2[g] = pe2[z];
     if (po.norms) { po.norms[2 * g] = n1; po.norms[2 * g + 1] = n2; }
     if (po.mults) po.mults[g] = budget(m, scheme) + s;
-    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || !(n1 <= INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
+    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || !(n1 < INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
   }
 }
 
 // ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
+
+// ||W||_1 for a chunk: slab partials over many CTAs, then the first rung.
+template <typename T>
+static void launch_norm1(const T* W, int n, int ic, const LargeLayout& L, double* part, double log_eps, int scheme,
+                         double* nrm4, int* need, int8_t* dm, int8_t* ds, double* de1, double* de2, cudaStream_t st) {
+  dim3 grid((n + 255) / 256, L.tiles_m, ic);
+  k_colsum_partial<T><<<grid, 256, 0, st>>>(W, n, (int64_t)n * n, part, L.tiles_m);
+  k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, 1, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
+}
+
+template <typename T>
+static void launch_finish(const T* X, int n, int ic, int scheme, const LargeLayout& L, unsigned char* ws,
+                          const double* nrm4, const int8_t* dm, const int8_t* ds, const double* de1,
+                          const double* de2, int64_t base, PlanOut po, cudaStream_t st) {
+  int* flags = reinterpret_cast<int*>(ws + L.off_flags);
+  cudaMemsetAsync(flags, 0, (size_t)ic * sizeof(int), st);
+  const size_t nn = (size_t)n * n;
+  int bx = (int)((nn + 256 * 8 - 1) / (256 * 8));
+  if (bx > 1024) bx = 1024;
+  k_nonfinite<T><<<dim3(bx, ic), 256, 0, st>>>(X, n, (int64_t)nn, flags);
+  k_finish<<<(ic + 255) / 256, 256, 0, st>>>(ic, scheme, nrm4, dm, ds, de1, de2, flags, base, po);
+}
 
 template <typename T>
 static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int scheme, int64_t base, PlanOut po,
@@ -219,7 +268,7 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
   const int ic = (int)cnt;
 
   const double log_eps = log2(eps);  // host libm, as select.py:175
-  k_norm1<T><<<ic, 256, 0, st>>>(W, n, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
+  launch_norm1<T>(W, n, ic, L, part, log_eps, scheme, nrm4, need, dm, ds, de1, de2, st);
 
   GemmCtx<T> g{};
   g.n = n;
@@ -296,7 +345,7 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
     g.sq_step = q;
     if (gemm_launch<T>(g, STAGE_SQ, dlist + o4, c, st)) return EXPMB_ERR_CUDA;
   }
-  k_finish<T><<<ic, 256, 0, st>>>(W, X, n, scheme, nrm4, dm, ds, de1, de2, base, po);
+  launch_finish<T>(X, n, ic, scheme, L, ws, nrm4, dm, ds, de1, de2, base, po, st);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
@@ -382,7 +431,7 @@ static int large_run_chunk_tc(const float* W, float* X, int64_t cnt, int n, doub
     if (!encode_map(&maps.m[i], mp[i], n, cnt, i == tc::M_W ? wsb : msb)) return EXPMB_ERR_CUDA;
 
   const double log_eps = log2(eps);
-  k_norm1<float><<<ic, 256, 0, st>>>(W, n, log_eps, 0, nrm4, need, dm, ds, de1, de2);
+  launch_norm1<float>(W, n, ic, L, part, log_eps, 0, nrm4, need, dm, ds, de1, de2, st);
   {
     dim3 grid((n + 31) / 32, (n + 31) / 32, ic);
     tc::tc_prep_kernel<<<grid, 256, 0, st>>>(g, ic);
@@ -428,7 +477,7 @@ static int large_run_chunk_tc(const float* W, float* X, int64_t cnt, int n, doub
     g.sq_step = q;
     if (tc_launch(maps, g, STAGE_SQ, dlist, c, st)) return EXPMB_ERR_CUDA;
   }
-  k_finish<float><<<ic, 256, 0, st>>>(W, X, n, 0, nrm4, dm, ds, de1, de2, base, po);
+  launch_finish<float>(X, n, ic, 0, L, ws, nrm4, dm, ds, de1, de2, base, po, st);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 

@@ -343,3 +343,21 @@ def test_baseline_cost_ratio_vs_sastre():
     base = X.expm_baseline(W, 1e-8).mults.sum().item()
     sas = X.expm(W, 1e-8).mults.sum().item()
     assert 1.3 <= base / sas <= 3.0, (base, sas)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_large_path_nonfinite(dtype):
+    """n > 64 (GEMM pipeline): NaN input and overflowing results raise NonFiniteError,
+    the healthy matrices of the same batch are unaffected."""
+    rng = np.random.default_rng(5)
+    W = rng.uniform(-1, 1, (3, 96, 96))
+    W /= np.abs(W).sum(axis=1).max(axis=1)[:, None, None]
+    W[1, 3, 4] = np.nan
+    W[2] *= 1e3 if dtype == torch.float64 else 1e2   # e^W overflows
+    Wt = torch.as_tensor(W).to(device="cuda", dtype=dtype)
+    with pytest.raises(X.NonFiniteError):
+        X.expm(Wt, 1e-6)
+    r = X.expm(Wt, 1e-6, check_finite=False)
+    assert r.nonfinite.tolist() == [False, True, True]
+    good = X.expm(Wt[:1], 1e-6).value
+    assert torch.equal(good[0], r.value[0])

@@ -29,10 +29,11 @@ static int sm_count() {
   return cached[dev];
 }
 
-template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1)>
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1),
+          int VARIANT = 0>
 static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
-  auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME, MINB>;
+  auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME, MINB, VARIANT>;
   constexpr size_t smem = F::kSmem + (MINB >= 3 ? GROUPS * F::kStageBytes : 0);
   static int occ = -1;  // per instantiation; identical on every B200
   if (occ < 0) {
@@ -63,9 +64,11 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
   static const int minb = getenv("EXPMB_C2_MINB") ? atoi(getenv("EXPMB_C2_MINB")) : 2;
   if (n <= 16) {
     int* c16 = claim16 ? ctr : nullptr;
+    static const int variant = getenv("EXPMB_VARIANT") ? atoi(getenv("EXPMB_VARIANT")) : 0;
     if constexpr (sizeof(T) == 4) {
       if (minb == 3) return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
       if (minb == 4) return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
+      if (SCHEME == 0 && variant == 1) return launch_fused<T, 16, 2, 8, SCHEME, 2, 1>(W, X, batch, n, eps, po, c16, st);
     }
     return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, c16, st);
   }

@@ -460,7 +460,8 @@ enum FusedStep : int {
   ST_DONE
 };
 
-template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1)>
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1),
+          int VARIANT = 0>
 __global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, MINB)
 expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, double eps,
                   PlanOut po, int* __restrict__ ctr) {
@@ -573,6 +574,80 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       p.e1 = ny;
       p.e2 = 0.0;
       mults = (k - 2) + s;
+    } else if constexpr (SCHEME == 0 && VARIANT == 1) {
+      // ---- Sastre as straight-line code per order (no step machine) ---------
+      bool small = nrm[0] == 0.0;
+      int need = 0;
+      if (!small) {
+        need = select_sastre_fast(nrm[0], 0.0, 1, log_eps, &p);
+        if (need < 0) {
+          lw[0] = log2_or_ninf(nrm[0]);
+          need = select_walk_lw(lw, 1, log_eps, 0, &p);
+        }
+      }
+      if (small) {
+        EW(P[i][j] = DG(i, j));                         // m = 0 (engine.py:141-142)
+      } else if (need < 2) {
+        EW(P[i][j] = B[i][j] + DG(i, j));               // m = 1 (poly.py:192)
+      } else {
+        f.square(B, A2);                                // W^2 (select.py:192)
+        nrm[1] = f.norm1(A2);
+        bad |= !(nrm[1] < INFINITY);
+        need = select_sastre_fast(nrm[0], nrm[1], 2, log_eps, &p);
+        if (need < 0) {
+          lw[0] = log2_or_ninf(nrm[0]);
+          lw[1] = log2_or_ninf(nrm[1]);
+          select_walk_lw(lw, 2, log_eps, 0, &p);
+        }
+        {
+          const T sc = pow2_neg<T>(p.s), sc2 = pow2_neg<T>(2 * p.s);
+          EW2(SP(B, pmul(GP(B), sc)); SP(A2, pmul(GP(A2), sc2)));
+        }
+        if (p.m == 2) {                                 // poly.py:196
+          EW2(SP(P, padd(pfma(GP(A2), T(0.5), GP(B)), DGP)));
+        } else if (p.m == 4) {                          // poly.py:198-199
+          Tile L;
+          EW2(SP(L, padd(pmul(pfma(GP(A2), T(0.25), GP(B)), T(1.0 / 3.0)), DGP)));
+          f.product(L, A2, P);
+          EW2(SP(P, padd(pfma(GP(P), T(0.5), GP(B)), DGP)));
+        } else {
+          const double* c = (p.m == 8) ? kT8 : kT15;
+          Tile L, R;
+          {
+            const T c0 = (T)c[0], c1 = (T)c[1];
+            EW2(SP(R, pfma(GP(A2), c0, pmul(GP(B), c1))));
+          }
+          f.product(A2, R, Y0);                         // y02 (poly.py:209 / :221)
+          {
+            const T c2 = (T)c[2], c3 = (T)c[3], c4 = (T)c[4];
+            EW2(SP(L, pfma(GP(B), c3, pfma(GP(A2), c2, GP(Y0)))); SP(R, pfma(GP(A2), c4, GP(Y0))));
+          }
+          f.product(L, R, P);
+          if (p.m == 8) {                               // poly.py:211
+            const T c5 = (T)c[5];
+            EW2(SP(P, padd(padd(pfma(GP(A2), T(0.5), pfma(GP(Y0), c5, GP(P))), GP(B)), DGP)));
+          } else {                                      // poly.py:222-229
+            {
+              const T c5 = (T)c[5], c6 = (T)c[6], c7 = (T)c[7], c8 = (T)c[8], c9 = (T)c[9], c10 = (T)c[10];
+              EW2(SP(Y1, pfma(GP(A2), c6, pfma(GP(Y0), c5, GP(P))));
+                  SP(L, pfma(GP(B), c8, pfma(GP(A2), c7, GP(Y1))));
+                  SP(R, pfma(GP(B), c10, pfma(GP(Y0), c9, GP(Y1)))));
+            }
+            f.product(L, R, P);
+            {
+              const T c11 = (T)kT15[11], c12 = (T)kT15[12], c13 = (T)kT15[13], c14 = (T)kT15[14],
+                      c15 = (T)kT15[15];
+              EW2(SP(P, padd(pfma(GP(B), c14, pfma(GP(A2), c13, pfma(GP(Y0), c12, pfma(GP(Y1), c11, GP(P))))),
+                             pmul(DGP, c15))));
+            }
+            for (int q = 0; q < p.s; ++q) {             // engine.py:80-87
+              f.square(P, Y1);
+              EW(P[i][j] = Y1[i][j]);
+            }
+          }
+        }
+      }
+      mults = budget(p.m, 0) + p.s;
     } else {
     int have = 1, step = ST_DONE, q = 0, hz = 0;
     if (nrm[0] != 0.0) {

@@ -57,6 +57,9 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
 
 template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
+  // Sastre runs as straight-line code per order (VARIANT 1: 10% faster than
+  // the step machine on C2); EXPMB_VARIANT=0 selects the step machine.
+  static const bool straight = !(getenv("EXPMB_VARIANT") && getenv("EXPMB_VARIANT")[0] == '0');
   // warp-per-matrix: ~100 matrices per SM balance statically; the claim
   // atomics only added latency there (7% of stall samples).  EXPMB_CLAIM=1
   // forces dynamic claiming (A/B experiments).
@@ -68,11 +71,16 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
     if constexpr (sizeof(T) == 4) {
       if (minb == 3) return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
       if (minb == 4) return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
-      if (SCHEME == 0 && variant == 1) return launch_fused<T, 16, 2, 8, SCHEME, 2, 1>(W, X, batch, n, eps, po, c16, st);
     }
+    (void)variant;
+    if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, (sizeof(T) == 4 ? 2 : 1), 1>(W, X, batch, n, eps, po, c16, st);
     return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, c16, st);
   }
-  if (n <= 32) return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
+  if (n <= 32) {
+    if (SCHEME == 0 && straight) return launch_fused<T, 32, 4, 4, SCHEME, 1, 1>(W, X, batch, n, eps, po, ctr, st);
+    return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
+  }
+  if (SCHEME == 0 && straight) return launch_fused<T, 64, 4, 1, SCHEME, 1, 1>(W, X, batch, n, eps, po, ctr, st);
   return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, ctr, st);
 }
 

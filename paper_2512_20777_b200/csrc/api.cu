@@ -69,8 +69,14 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
     int* c16 = claim16 ? ctr : nullptr;
     static const int variant = getenv("EXPMB_VARIANT") ? atoi(getenv("EXPMB_VARIANT")) : 0;
     if constexpr (sizeof(T) == 4) {
-      if (minb == 3) return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
-      if (minb == 4) return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
+      if (minb == 3) {
+        if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, 3, 1>(W, X, batch, n, eps, po, c16, st);
+        return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
+      }
+      if (minb == 4) {
+        if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, 4, 1>(W, X, batch, n, eps, po, c16, st);
+        return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
+      }
     }
     (void)variant;
     if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, (sizeof(T) == 4 ? 2 : 1), 1>(W, X, batch, n, eps, po, c16, st);

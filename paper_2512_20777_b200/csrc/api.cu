@@ -12,6 +12,7 @@
 
 #include "../../include/expmb.h"
 #include "fused_small.cuh"
+#include "fused_dmma.cuh"
 #include "large.cuh"
 
 namespace expmb {
@@ -55,6 +56,26 @@ static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, Plan
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
+// fp64 Sastre, 32 < n <= 64: the DMMA (FP64 tensor core) fused kernel.
+static int launch_dmma(const double* W, double* X, int64_t batch, int n, double eps, PlanOut po, int* ctr,
+                       cudaStream_t st) {
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaFuncSetAttribute(expm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dm::kSmem) !=
+        cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, expm_dmma_kernel, Dm::NT, Dm::kSmem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(batch < persistent ? batch : persistent);
+  if (ctr != nullptr && cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  expm_dmma_kernel<<<grid, Dm::NT, Dm::kSmem, st>>>(W, X, batch, n, log2(eps), po, ctr);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
 template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   // Sastre runs as straight-line code per order (VARIANT 1: 10% faster than
@@ -85,6 +106,10 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
   if (n <= 32) {
     if (SCHEME == 0 && straight) return launch_fused<T, 32, 4, 4, SCHEME, 1, 1>(W, X, batch, n, eps, po, ctr, st);
     return launch_fused<T, 32, 4, 4, SCHEME>(W, X, batch, n, eps, po, ctr, st);
+  }
+  if constexpr (sizeof(T) == 8 && SCHEME == 0) {
+    static const bool dmma = !(getenv("EXPMB_NO_DMMA") && getenv("EXPMB_NO_DMMA")[0] == '1');
+    if (dmma) return launch_dmma(W, X, batch, n, eps, po, ctr, st);
   }
   if (SCHEME == 0 && straight) return launch_fused<T, 64, 4, 1, SCHEME, 1, 1>(W, X, batch, n, eps, po, ctr, st);
   return launch_fused<T, 64, 4, 1, SCHEME>(W, X, batch, n, eps, po, ctr, st);

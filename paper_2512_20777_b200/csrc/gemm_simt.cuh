@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "fused_small.cuh"
 #include "select.cuh"
@@ -195,13 +196,19 @@ __device__ __forceinline__ int simt_col(int tx, int j) {
 // TWO: fp32 two-level accumulation (needed for long k: n > 512).  Without
 // it the kernel fits 128 registers and two CTAs share an SM, so one CTA's
 // prologue/epilogue overlaps the other's mainloop (short k at n <= 512).
-template <typename T, bool TWO = (sizeof(T) == 4)>
+// MMA (fp64 only): the mainloop issues DMMA (mma.sync.m8n8k4.f64, the FP64
+// tensor cores) instead of DFMAs: warp (wr, wc) of the 2 x 4 warp grid owns a
+// 64 x 32 sub-tile = 8 x 4 DMMA tiles, and thread "row slot" i / column pair
+// j0 of the epilogue map onto the accumulator fragments.
+template <typename T, bool TWO = (sizeof(T) == 4), bool MMA = false>
 __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
 gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   using C = SimtCfg<T>;
   constexpr int BK = C::BK, ST = C::STAGES, KV = C::KV, VW = C::VW;
   constexpr int LDA = BK + KV;            // padded row of an L tile (elements)
-  constexpr int LDB = kGemmBN + 16 / (int)sizeof(T);
+  // fp64 rows padded to 136 doubles (= 16 banks mod 32) so the DMMA B
+  // fragments (4 k-rows x 8 columns per warp load) hit the 2-wavefront minimum
+  constexpr int LDB = kGemmBN + (sizeof(T) == 4 ? 4 : 8);
   constexpr int A_ELEMS = kGemmBM * LDA, B_ELEMS = BK * LDB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
@@ -213,6 +220,11 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   const int n = g.n;
   const int m0 = blockIdx.y * kGemmBM, n0 = blockIdx.x * kGemmBN;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int lane = tid % 32, warp = tid / 32, lg = lane >> 2, lt = lane & 3, wr = warp >> 2, wc = warp & 3;
+  // epilogue coordinates of accumulator slot (i, j) within the CTA tile
+  auto acc_row = [&](int i) { return MMA ? 64 * wr + 8 * i + lg : (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4); };
+  auto acc_col = [&](int j) { return MMA ? 32 * wc + 8 * (j >> 1) + 2 * lt + (j & 1) : simt_col<T>(tx, j); };
+  auto red_slot = [&]() { return MMA ? wr * 8 + lg : ty; };
   const bool vec = (n % KV) == 0;  // 16-byte rows chunks are whole
   const T* __restrict__ Lp = e.L;
   const T* __restrict__ Rp = e.R;
@@ -274,6 +286,26 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
     }
     const T* as = As + (kt % ST) * A_ELEMS;
     const T* bs = Bs + (kt % ST) * B_ELEMS;
+    if constexpr (MMA && sizeof(T) == 8) {
+      const double* la = reinterpret_cast<const double*>(as) + (64 * wr + lg) * LDA + lt;
+      const double* rb = reinterpret_cast<const double*>(bs) + lt * LDB + 32 * wc + lg;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double a[8], b[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = la[8 * i * LDA + kk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = rb[kk * LDB + 8 * q];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[i][2 * q]), "+d"(acc[i][2 * q + 1])
+                         : "d"(a[i]), "d"(b[q]));
+      }
+      continue;
+    }
     if constexpr (kTwoLevel) {
       if (kt % kChunkTiles == 0) {
 #pragma unroll
@@ -350,11 +382,11 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   const bool evec = (n % VW) == 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    const int row = m0 + acc_row(i);
     if (row >= n) continue;
 #pragma unroll
     for (int j0 = 0; j0 < 8; j0 += VW) {
-      const int col0 = n0 + simt_col<T>(tx, j0);
+      const int col0 = n0 + acc_col(j0);
       if (col0 >= n) continue;
       const size_t pos = (size_t)row * n + col0;
       const bool full = evec && col0 + VW <= n;
@@ -423,7 +455,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
     double* red = reinterpret_cast<double*>(smem_raw);  // 16 x 128 doubles
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) red[ty * kGemmBN + simt_col<T>(tx, j)] = csum[j];
+    for (int j = 0; j < 8; ++j) red[red_slot() * kGemmBN + acc_col(j)] = csum[j];
     __syncthreads();
     if (tid < kGemmBN && n0 + tid < n) {
       double a = 0.0;
@@ -436,7 +468,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 template <typename T>
 constexpr int simt_smem_bytes() {
   using C = SimtCfg<T>;
-  return (int)(C::STAGES * (kGemmBM * (C::BK + C::KV) + C::BK * (kGemmBN + 16 / (int)sizeof(T))) * sizeof(T));
+  return (int)(C::STAGES * (kGemmBM * (C::BK + C::KV) + C::BK * (kGemmBN + (sizeof(T) == 4 ? 4 : 8))) * sizeof(T));
 }
 
 template <typename T>
@@ -448,14 +480,20 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
     if (cudaFuncSetAttribute(gemm_stage_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(gemm_stage_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
+            cudaSuccess ||
+        (sizeof(T) == 8 &&
+         cudaFuncSetAttribute(gemm_stage_kernel<T, false, sizeof(T) == 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem) != cudaSuccess))
       return 1;
     attr = true;
   }
   const int tn = (g.n + kGemmBN - 1) / kGemmBN, tm = (g.n + kGemmBM - 1) / kGemmBM;
   dim3 grid(tn, tm, count);
+  static const bool dmma = !(getenv("EXPMB_NO_DMMA") && getenv("EXPMB_NO_DMMA")[0] == '1');
   if (sizeof(T) == 4 && g.n > 512)
     gemm_stage_kernel<T, true><<<grid, 256, smem, st>>>(g, stage, list);
+  else if (sizeof(T) == 8 && dmma)
+    gemm_stage_kernel<T, false, sizeof(T) == 8><<<grid, 256, smem, st>>>(g, stage, list);
   else
     gemm_stage_kernel<T, false><<<grid, 256, smem, st>>>(g, stage, list);
   return cudaGetLastError() != cudaSuccess;

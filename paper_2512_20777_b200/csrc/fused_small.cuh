@@ -138,7 +138,16 @@ struct Fused {
   static constexpr int TPG = TC * TR;            // threads per group
   static constexpr int NT = TPG * GROUPS;        // threads per CTA
   static constexpr int KV = Vec<T>::KV;          // k-steps per 128-bit load
-  static constexpr int LD = NPAD + KV;           // padded smem row stride (elements)
+  // fp32 n <= 16: unpadded rows with the 16-byte chunks XOR-swizzled by
+  // (row/2)%4, so tile stores (two rows per quarter-warp) and the 8-row
+  // operand loads are both conflict-free -- the padded layout made every
+  // store 2-way conflicted and l1tex throughput was the C2 limiter (90%).
+  static constexpr bool SWZ = (sizeof(T) == 4 && NPAD == 16);
+  static constexpr int LD = SWZ ? NPAD : NPAD + KV;  // smem row stride (elements)
+  __device__ __forceinline__ static int sidx(int r, int c) {  // element offset of (row r, column c), c % 4 == 0
+    if constexpr (SWZ) return r * LD + ((((c >> 2) ^ (r >> 1)) & 3) << 2);
+    else return r * LD + c;
+  }
   static constexpr int WARPS_PG = (TPG + 31) / 32;
   static constexpr int BUF = NPAD * LD;          // one operand buffer (elements)
   // dynamic smem per CTA: two operand buffers per group + reduction scratch
@@ -179,7 +188,7 @@ struct Fused {
   __device__ __forceinline__ void store(T* buf, const Tile& v) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      T* p = buf + soff + i * TR * LD;
+      T* p = buf + (SWZ ? sidx(tr + i * TR, 4 * tc) : soff + i * TR * LD);
       if constexpr (sizeof(T) == 4) {
         *reinterpret_cast<float4*>(p) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
       } else {
@@ -196,7 +205,7 @@ struct Fused {
                                            T (&b)[KV][4]) const {
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      const T* p = L + (tr + i * TR) * LD + kb;
+      const T* p = L + (SWZ ? sidx(tr + i * TR, kb) : (tr + i * TR) * LD + kb);
       if constexpr (sizeof(T) == 4) {
         float4 v = *reinterpret_cast<const float4*>(p);
         a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
@@ -207,7 +216,7 @@ struct Fused {
     }
 #pragma unroll
     for (int kk = 0; kk < KV; ++kk) {
-      const T* q = R + (kb + kk) * LD + (soff - tr * LD);  // row kb+kk, this thread's columns
+      const T* q = R + (SWZ ? sidx(kb + kk, 4 * tc) : (kb + kk) * LD + (soff - tr * LD));  // row kb+kk, own columns
       if constexpr (sizeof(T) == 4) {
         float4 v = *reinterpret_cast<const float4*>(q);
         b[kk][0] = v.x; b[kk][1] = v.y; b[kk][2] = v.z; b[kk][3] = v.w;
@@ -231,12 +240,12 @@ struct Fused {
         float a[TM][KV];
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
-          const float4 v = *reinterpret_cast<const float4*>(L + (tr + i * TR) * LD + kb);
+          const float4 v = *reinterpret_cast<const float4*>(L + (SWZ ? sidx(tr + i * TR, kb) : (tr + i * TR) * LD + kb));
           a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
         }
 #pragma unroll
         for (int kk = 0; kk < KV; ++kk) {
-          const float4 v = *reinterpret_cast<const float4*>(R + (kb + kk) * LD + (soff - tr * LD));
+          const float4 v = *reinterpret_cast<const float4*>(R + (SWZ ? sidx(kb + kk, 4 * tc) : (kb + kk) * LD + (soff - tr * LD)));
 #pragma unroll
           for (int i = 0; i < TM; ++i) {
             const float2 ai = make_float2(a[i][kk], a[i][kk]);

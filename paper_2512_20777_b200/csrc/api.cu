@@ -33,7 +33,7 @@ static int sm_count() {
 template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPAD == 16 && sizeof(T) == 4) ? 2 : 1),
           int VARIANT = 0>
 static int launch_fused(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
-  using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
+  using F = Fused<T, NPAD, TM, GROUPS, SCHEME, (VARIANT == 2)>;
   auto kern = expm_fused_kernel<T, NPAD, TM, GROUPS, SCHEME, MINB, VARIANT>;
   constexpr size_t smem = F::kSmem + (MINB >= 3 ? GROUPS * F::kStageBytes : 0);
   static int occ = -1;  // per instantiation; identical on every B200
@@ -99,7 +99,9 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
         return launch_fused<T, 16, 2, 8, SCHEME, 4>(W, X, batch, n, eps, po, c16, st);
       }
     }
-    (void)variant;
+    if constexpr (sizeof(T) == 4 && SCHEME == 0) {
+      if (variant == 2) return launch_fused<T, 16, 2, 8, SCHEME, 2, 2>(W, X, batch, n, eps, po, c16, st);
+    }
     if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, (sizeof(T) == 4 ? 2 : 1), 1>(W, X, batch, n, eps, po, c16, st);
     return launch_fused<T, 16, 2, 8, SCHEME>(W, X, batch, n, eps, po, c16, st);
   }

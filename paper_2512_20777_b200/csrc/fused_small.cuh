@@ -131,8 +131,17 @@ __device__ __forceinline__ bool is_finite_t(double x) { return isfinite(x); }
 // max that propagates NaN (a NaN norm must not be hidden by fmax).
 __device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
-template <typename T, int NPAD, int TM, int GROUPS, int SCHEME>
+// HM: fp32 n <= 16 products on the tensor cores with mma.sync.m16n8k8.tf32
+// in 3xTF32 form (x = hi + lo, hi = x with the low 13 mantissa bits cleared,
+// L R ~= Lhi Rhi + Lhi Rlo + Llo Rhi).  The FFMA2 version was bound by the
+// L1/shared-memory data path (l1tex 87-90% busy: 128-bit operand loads cost 4
+// wavefronts each); fragment loads are 32-bit, one wavefront, 6x fewer.
+// The state tiles then use the mma accumulator layout: lane (g, t) holds rows
+// {g, g+8} x columns {2t, 2t+1, 8+2t, 9+2t}.
+template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, bool HM = false>
 struct Fused {
+  static_assert(!HM || (sizeof(T) == 4 && NPAD == 16 && TM == 2), "HM is the fp32 n<=16 warp kernel");
+  static constexpr int LDL = 20, LDR = 24;  // HM: A-fragment / B-fragment conflict-free strides
   static constexpr int TC = NPAD / 4;            // column quads
   static constexpr int TR = NPAD / TM;           // row phases
   static constexpr int TPG = TC * TR;            // threads per group
@@ -142,14 +151,14 @@ struct Fused {
   // (row/2)%4, so tile stores (two rows per quarter-warp) and the 8-row
   // operand loads are both conflict-free -- the padded layout made every
   // store 2-way conflicted and l1tex throughput was the C2 limiter (90%).
-  static constexpr bool SWZ = (sizeof(T) == 4 && NPAD == 16);
+  static constexpr bool SWZ = (sizeof(T) == 4 && NPAD == 16 && !HM);
   static constexpr int LD = SWZ ? NPAD : NPAD + KV;  // smem row stride (elements)
   __device__ __forceinline__ static int sidx(int r, int c) {  // element offset of (row r, column c), c % 4 == 0
     if constexpr (SWZ) return r * LD + ((((c >> 2) ^ (r >> 1)) & 3) << 2);
     else return r * LD + c;
   }
   static constexpr int WARPS_PG = (TPG + 31) / 32;
-  static constexpr int BUF = NPAD * LD;          // one operand buffer (elements)
+  static constexpr int BUF = NPAD * (HM ? LDR : LD);  // one operand buffer (elements)
   // dynamic smem per CTA: two operand buffers per group + reduction scratch
   static constexpr size_t kSmemGroup = 2 * BUF * sizeof(T) + (WARPS_PG > 1 ? WARPS_PG * NPAD * sizeof(double) + 64 : 0);
   static_assert(BUF * sizeof(T) % 16 == 0, "operand buffers must stay 16-byte aligned");
@@ -181,7 +190,8 @@ struct Fused {
   // a row read/write 256 contiguous bytes per instruction (a 4-column double
   // quad per lane strided the lanes 32 B apart: 2x shared-memory wavefronts).
   __device__ __forceinline__ int col(int j) const {
-    if constexpr (sizeof(T) == 4) return 4 * tc + j;
+    if constexpr (HM) return (j < 2) ? 2 * tc + j : 8 + 2 * tc + (j - 2);
+    else if constexpr (sizeof(T) == 4) return 4 * tc + j;
     else return (j >> 1) * (NPAD / 2) + 2 * tc + (j & 1);
   }
 
@@ -304,19 +314,90 @@ struct Fused {
     }
   }
 
+  // ---- HM (3xTF32 mma.sync) path ----
+  template <int LDX>
+  __device__ __forceinline__ void store_hm(T* buf, const Tile& v) const {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      T* p = buf + (tr + 8 * i) * LDX + 2 * tc;
+      *reinterpret_cast<float2*>(p) = make_float2(v[i][0], v[i][1]);
+      *reinterpret_cast<float2*>(p + 8) = make_float2(v[i][2], v[i][3]);
+    }
+  }
+  __device__ __forceinline__ static void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    const uint32_t u = __float_as_uint(x) & 0xffffe000u;
+    hi = u;
+    lo = __float_as_uint(x - __uint_as_float(u));
+  }
+  __device__ __forceinline__ static void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  __device__ __forceinline__ void mm_hm(const T* __restrict__ L, const T* __restrict__ R, Tile& out) const {
+    float acc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+    const int g8 = tr, t4 = tc;  // mma groupID / threadID_in_group
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int k0 = 8 * ks;
+      uint32_t ah[4], al[4];
+      split_tf32(L[g8 * LDL + k0 + t4], ah[0], al[0]);
+      split_tf32(L[(g8 + 8) * LDL + k0 + t4], ah[1], al[1]);
+      split_tf32(L[g8 * LDL + k0 + t4 + 4], ah[2], al[2]);
+      split_tf32(L[(g8 + 8) * LDL + k0 + t4 + 4], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(R[(k0 + t4) * LDR + 8 * nt + g8], bh0, bl0);
+        split_tf32(R[(k0 + t4 + 4) * LDR + 8 * nt + g8], bh1, bl1);
+        hmma(acc[nt], al, bh0, bh1);  // small terms first
+        hmma(acc[nt], ah, bl0, bl1);
+        hmma(acc[nt], ah, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      out[0][2 * nt] = acc[nt][0];
+      out[0][2 * nt + 1] = acc[nt][1];
+      out[1][2 * nt] = acc[nt][2];
+      out[1][2 * nt + 1] = acc[nt][3];
+    }
+  }
+
   // out = L * R where L, R are register tiles (stages through smem).
   __device__ __forceinline__ void product(const Tile& Lt, const Tile& Rt, Tile& out) const {
-    store(buf0, Lt);
-    store(buf1, Rt);
-    sync();
-    mm(buf0, buf1, out);
-    sync();
+    if constexpr (HM) {
+      store_hm<LDL>(buf0, Lt);
+      store_hm<LDR>(buf1, Rt);
+      sync();
+      mm_hm(buf0, buf1, out);
+      sync();
+    } else {
+      store(buf0, Lt);
+      store(buf1, Rt);
+      sync();
+      mm(buf0, buf1, out);
+      sync();
+    }
   }
   __device__ __forceinline__ void square(const Tile& Xt, Tile& out) const {
-    store(buf0, Xt);
-    sync();
-    mm(buf0, buf0, out);
-    sync();
+    if constexpr (HM) {
+      store_hm<LDL>(buf0, Xt);
+      store_hm<LDR>(buf1, Xt);
+      sync();
+      mm_hm(buf0, buf1, out);
+      sync();
+    } else {
+      store(buf0, Xt);
+      sync();
+      mm(buf0, buf0, out);
+      sync();
+    }
   }
 
   // ||.||_1 of the group's matrix: column abs-sums in binary64, then max.
@@ -390,7 +471,11 @@ struct Fused {
       const int r = row(i);
       if (vec) {
         const T* p = src + r * NPAD;
-        if constexpr (sizeof(T) == 4) {
+        if constexpr (HM) {
+          const float2 q0 = __ldg(reinterpret_cast<const float2*>(p + col(0)));
+          const float2 q1 = __ldg(reinterpret_cast<const float2*>(p + col(2)));
+          v[i][0] = q0.x; v[i][1] = q0.y; v[i][2] = q1.x; v[i][3] = q1.y;
+        } else if constexpr (sizeof(T) == 4) {
           float4 q = __ldg(reinterpret_cast<const float4*>(p + col(0)));
           v[i][0] = q.x; v[i][1] = q.y; v[i][2] = q.z; v[i][3] = q.w;
         } else {
@@ -414,7 +499,10 @@ struct Fused {
       const int r = row(i);
       if (vec) {
         T* p = dst + r * NPAD;
-        if constexpr (sizeof(T) == 4) {
+        if constexpr (HM) {
+          __stcs(reinterpret_cast<float2*>(p + col(0)), make_float2(v[i][0], v[i][1]));
+          __stcs(reinterpret_cast<float2*>(p + col(2)), make_float2(v[i][2], v[i][3]));
+        } else if constexpr (sizeof(T) == 4) {
           __stcs(reinterpret_cast<float4*>(p + col(0)), make_float4(v[i][0], v[i][1], v[i][2], v[i][3]));
         } else {
           __stcs(reinterpret_cast<double2*>(p + col(0)), make_double2(v[i][0], v[i][1]));
@@ -474,7 +562,7 @@ template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, int MINB = ((NPA
 __global__ void __launch_bounds__(Fused<T, NPAD, TM, GROUPS, SCHEME>::NT, MINB)
 expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int n, double log_eps, double eps,
                   PlanOut po, int* __restrict__ ctr) {
-  using F = Fused<T, NPAD, TM, GROUPS, SCHEME>;
+  using F = Fused<T, NPAD, TM, GROUPS, SCHEME, (VARIANT == 2)>;
   using Tile = typename F::Tile;
   // next-matrix prefetch: registers (default), or -- in the register-lean
   // 3-CTA/SM variant -- cp.async into a per-group staging buffer
@@ -583,7 +671,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       p.e1 = ny;
       p.e2 = 0.0;
       mults = (k - 2) + s;
-    } else if constexpr (SCHEME == 0 && VARIANT == 1) {
+    } else if constexpr (SCHEME == 0 && (VARIANT == 1 || VARIANT == 2)) {
       // ---- Sastre as straight-line code per order (no step machine) ---------
       bool small = nrm[0] == 0.0;
       int need = 0;

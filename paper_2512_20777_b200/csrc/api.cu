@@ -80,7 +80,7 @@ template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   // Sastre runs as straight-line code per order (VARIANT 1: 10% faster than
   // the step machine on C2); EXPMB_VARIANT=0 selects the step machine.
-  static const bool straight = !(getenv("EXPMB_VARIANT") && getenv("EXPMB_VARIANT")[0] == '0');
+  static const bool straight = !(getenv("EXPMB_VARIANT") && getenv("EXPMB_VARIANT")[0] == '0');  // 1 and 2 are straight-line
   // warp-per-matrix: ~100 matrices per SM balance statically; the claim
   // atomics only added latency there (7% of stall samples).  EXPMB_CLAIM=1
   // forces dynamic claiming (A/B experiments).
@@ -88,7 +88,8 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
   static const int minb = getenv("EXPMB_C2_MINB") ? atoi(getenv("EXPMB_C2_MINB")) : 2;
   if (n <= 16) {
     int* c16 = claim16 ? ctr : nullptr;
-    static const int variant = getenv("EXPMB_VARIANT") ? atoi(getenv("EXPMB_VARIANT")) : 0;
+    // fp32 Sastre default: variant 2 (3xTF32 mma.sync products); 1 = FFMA2 straight-line, 0 = step machine
+    static const int variant = getenv("EXPMB_VARIANT") ? atoi(getenv("EXPMB_VARIANT")) : 2;
     if constexpr (sizeof(T) == 4) {
       if (minb == 3) {
         if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, 3, 1>(W, X, batch, n, eps, po, c16, st);

@@ -625,7 +625,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
       }
     }
     bool bad = false;
-    EW(bad |= !is_finite_t(B[i][j]));
+    // (a NaN/Inf input shows up in ||W||_1: the abs-sums propagate it)
 
     // ---- ||W||_1 and the first rung (select.py:169-188) -------------------
     double nrm[4], lw[4];
@@ -906,7 +906,11 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     mults = budget(p.m, SCHEME) + p.s;
     }  // SCHEME != 2
 
-    EW(bad |= !is_finite_t(P[i][j]));
+    {  // x * 0 is NaN exactly when x is Inf/NaN: one check per lane instead of eight
+      Pr<T> z{T(0), T(0)};
+      EW2(z = pfma(GP(P), T(0), z));
+      bad |= !(z.x == T(0) && z.y == T(0));
+    }
     bad = f.any_group(bad);
     f.save(X + idx * nn, n, vec, P);
     if (f.t == 0) {
@@ -919,7 +923,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
         po.norms[2 * idx + 1] = nrm[1];
       }
       if (po.mults) po.mults[idx] = mults;
-      if (po.nonfinite) po.nonfinite[idx] = (uint8_t)(bad || !(nrm[0] <= INFINITY));
+      if (po.nonfinite) po.nonfinite[idx] = (uint8_t)(bad || !(nrm[0] < INFINITY));
     }
     if constexpr (kPrefetch) {
       EW(B[i][j] = nxt[i][j]);

@@ -9,10 +9,19 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_referen
 for c in C1 C3 C4; do
 timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
-timeout 900 python bench.py --config C5 --steps 2 --warmup 3 --batch 64 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
+timeout 1200 python bench.py --config C5 --steps 2 --warmup 3 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:expm_fused -s 3 -c 1 \
     -o gpurun_out/prof_C2 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1
 echo done
+python bench.py --scheme baseline > gpurun_out/bench_C2_alg1.json 2> gpurun_out/bench_C2_alg1.err
+python bench.py --config C1 --scheme baseline --no-cpu-baseline > gpurun_out/bench_C1_alg1.json 2> gpurun_out/bench_C1_alg1.err
+python bench.py --config C1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:dmma -s 3 -c 1 \
+    -o gpurun_out/prof_C1 -f python bench.py --config C1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu3.log 2>&1
+python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain4.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gemm_stage -s 20 -c 1 \
+    -o gpurun_out/prof_C4 -f python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_p4.log 2>&1
+echo done2

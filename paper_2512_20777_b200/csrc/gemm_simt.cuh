@@ -205,10 +205,13 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
 gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   using C = SimtCfg<T>;
   constexpr int BK = C::BK, ST = C::STAGES, KV = C::KV, VW = C::VW;
-  constexpr int LDA = BK + KV;            // padded row of an L tile (elements)
+  // padded rows: fp64 strides of 20 / 132 doubles (= 8 banks mod 32) make the
+  // DMMA fragment loads conflict-free per half-warp (a 64-bit load is served
+  // 16 lanes at a time); fp32 keeps 16-byte padding.
+  constexpr int LDA = BK + (sizeof(T) == 4 ? KV : 4);
   // fp64 rows padded to 136 doubles (= 16 banks mod 32) so the DMMA B
   // fragments (4 k-rows x 8 columns per warp load) hit the 2-wavefront minimum
-  constexpr int LDB = kGemmBN + (sizeof(T) == 4 ? 4 : 8);
+  constexpr int LDB = kGemmBN + 4;
   constexpr int A_ELEMS = kGemmBM * LDA, B_ELEMS = BK * LDB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
@@ -468,7 +471,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
 template <typename T>
 constexpr int simt_smem_bytes() {
   using C = SimtCfg<T>;
-  return (int)(C::STAGES * (kGemmBM * (C::BK + C::KV) + C::BK * (kGemmBN + (sizeof(T) == 4 ? 4 : 8))) * sizeof(T));
+  return (int)(C::STAGES * (kGemmBM * (C::BK + (sizeof(T) == 4 ? C::KV : 4)) + C::BK * (kGemmBN + 4)) * sizeof(T));
 }
 
 template <typename T>

@@ -155,8 +155,8 @@ int expmb_select_host(const double* norms, double eps, int scheme, int* m, int* 
   if (scheme == EXPMB_SASTRE && norms[0] != 0.0) {
     // the kernels' fast path first; it must agree with the exact walk below
     const double le = log2(eps);
-    int nd = select_sastre_fast(norms[0], 0.0, 1, le, &p);
-    if (nd == 2) nd = select_sastre_fast(norms[0], norms[1], 2, le, &p), have = 2;
+    int nd = (norms[0] > rung0_threshold(le)) ? 2 : select_sastre_fast(norms[0], 0.0, 1, le, &p);
+    if (nd == 2) nd = select_sastre_fast2(norms[0], norms[1], le, &p), have = 2;
     if (nd == 0) {
       if (m) *m = p.m;
       if (s) *s = p.s;

@@ -191,8 +191,8 @@ expm_dmma_kernel(const double* __restrict__ W, double* __restrict__ X, int64_t b
     const int64_t nidx = next_sh;  // published before the norm's barriers
     Plan p{0, 0, 0.0, 0.0};
     bool bad = false;
-    int need = 0;
-    if (nrm[0] != 0.0) {
+    int need = 2;
+    if (nrm[0] != 0.0 && !(nrm[0] > rung0_threshold(log_eps))) {
       need = select_sastre_fast(nrm[0], 0.0, 1, log_eps, &p);
       if (need < 0) {
         const double lw[4] = {log2_or_ninf(nrm[0]), 0, 0, 0};
@@ -207,7 +207,7 @@ expm_dmma_kernel(const double* __restrict__ W, double* __restrict__ X, int64_t b
       f.square(B, A2);
       nrm[1] = f.norm1(A2);
       bad |= !(nrm[1] < INFINITY);
-      need = select_sastre_fast(nrm[0], nrm[1], 2, log_eps, &p);
+      need = select_sastre_fast2(nrm[0], nrm[1], log_eps, &p);
       if (need < 0) {
         const double lw[4] = {log2_or_ninf(nrm[0]), log2_or_ninf(nrm[1]), 0, 0};
         select_walk_lw(lw, 2, log_eps, 0, &p);

@@ -584,6 +584,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
   const bool vec = (n == NPAD);
   const size_t nn = (size_t)n * n;
   const int64_t stride = (int64_t)gridDim.x * GROUPS;
+  const double rung0_thr = rung0_threshold(log_eps);
   int64_t idx = (int64_t)blockIdx.x * GROUPS + f.g;
   if (idx >= batch) return;  // whole group exits together
 
@@ -674,8 +675,8 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     } else if constexpr (SCHEME == 0 && (VARIANT == 1 || VARIANT == 2)) {
       // ---- Sastre as straight-line code per order (no step machine) ---------
       bool small = nrm[0] == 0.0;
-      int need = 0;
-      if (!small) {
+      int need = 2;
+      if (!small && !(nrm[0] > rung0_thr)) {  // rung 0 (m = 1) can only pass for tiny norms
         need = select_sastre_fast(nrm[0], 0.0, 1, log_eps, &p);
         if (need < 0) {
           lw[0] = log2_or_ninf(nrm[0]);
@@ -690,7 +691,7 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
         f.square(B, A2);                                // W^2 (select.py:192)
         nrm[1] = f.norm1(A2);
         bad |= !(nrm[1] < INFINITY);
-        need = select_sastre_fast(nrm[0], nrm[1], 2, log_eps, &p);
+        need = select_sastre_fast2(nrm[0], nrm[1], log_eps, &p);
         if (need < 0) {
           lw[0] = log2_or_ninf(nrm[0]);
           lw[1] = log2_or_ninf(nrm[1]);

@@ -382,6 +382,86 @@ EXPMB_HD int select_sastre_fast(double n1, double n2, int have, double log_eps_d
   return 0;
 }
 
+// Leaner fast path for the fused kernels (same margins / same decisions as
+// select_sastre_fast).  Rung 0 needs only ||W||_1 and fails certainly above
+// rung0_threshold(log_eps), so the kernels skip it for all but tiny norms;
+// rungs 1..4 are straight-line fp32 with lw = __log2f((float)norm); e1/e2
+// use n2^k by repeated squaring (k is a power of two).
+EXPMB_HD double rung0_threshold(double log_eps) {
+  // rung 0 fails iff max(l1, l2) > log_eps + margin; l1 = -1 + 2 lw1 suffices
+  return exp2((log_eps + 1.0 + 1e-3) * 0.5);
+}
+
+EXPMB_HD float lg2_fast(double x) {
+#if defined(__CUDA_ARCH__)
+  return __log2f((float)x);  // x in [2^-100, 2^100]: |error| < 5e-7
+#else
+  return log2f((float)x);
+#endif
+}
+
+// 0: decided (*out written); -1: too close to call (run select_walk_lw).
+EXPMB_HD int select_sastre_fast2(double n1, double n2, double log_eps_d, Plan* out) {
+  const double lo = 0x1p-100, hi = 0x1p100;
+  if (!(n1 >= lo && n1 <= hi && n2 >= lo && n2 <= hi)) return -1;
+  const float M = 2e-4f;
+  const float le = (float)log_eps_d;
+  const float lw1 = lg2_fast(n1), lw2 = lg2_fast(n2);
+  // verdict of one rung: +1 pass, 0 fail, -1 unsure
+  auto verdict = [&](float l1, float l2) -> int {
+    const float h = fmaxf(l1, l2);
+    if (h + 1.0f < le - M) return 1;
+    if (h > le + M) return 0;
+    const float lae = h + fast_l2p(fabsf(l1 - l2));
+    if (lae < le - M) return 1;
+    if (lae > le + M) return 0;
+    return -1;
+  };
+  // sastre_log_tail(2..9) as fp32 constants
+  const float T2 = (float)-0x1.4ae00d1cfdeb4p+1, T3 = (float)-0x1.2570068e7ef5ap+2;
+  const float T4 = (float)-0x1.ba0a7eda4c113p+2, T5 = (float)-0x1.2fbd42b465836p+3;
+  const float T6 = (float)-0x1.278191a01a44ep+4, T7 = (float)-0x1.5ca82fb30d8bcp+4;
+  const float T8 = (float)-0x1.6b1bc6161c270p+5, T9 = (float)-0x1.82b3695d62b2fp+5;
+  int ri, v;
+  float l1, l2;
+  l1 = T2 + lw2 + lw1; l2 = T3 + lw2 + lw2;                          // m = 2, k = 1
+  if ((v = verdict(l1, l2)) != 0) { ri = 1; goto done; }
+  l1 = T4 + 2.0f * lw2 + lw1; l2 = T5 + 2.0f * lw2 + lw2;            // m = 4, k = 2
+  if ((v = verdict(l1, l2)) != 0) { ri = 2; goto done; }
+  l1 = T6 + 4.0f * lw2 + lw1; l2 = T7 + 4.0f * lw2 + lw2;            // m = 8, k = 4
+  if ((v = verdict(l1, l2)) != 0) { ri = 3; goto done; }
+  l1 = T8 + 8.0f * lw2; l2 = T9 + 8.0f * lw2 + lw1;                   // m = 15, k = 8
+  if ((v = verdict(l1, l2)) != 0) { ri = 4; goto done; }
+  ri = 4; v = 0;                                                      // no rung passed: scale
+done:
+  if (v < 0) return -1;
+  int s = 0;
+  if (v == 0) {
+    const float va = fmaxf((l1 - le) * (1.0f / 16.0f), (l2 - le) * (1.0f / 17.0f));
+    float c_lo = ceilf(va - M), c_hi = ceilf(va + M);
+    c_lo = fminf(fmaxf(c_lo, 0.f), (float)kMaxScaling);
+    c_hi = fminf(fmaxf(c_hi, 0.f), (float)kMaxScaling);
+    if (c_lo != c_hi) return -1;
+    s = (int)c_lo;
+  }
+  // reported bounds exp2(l1), exp2(l2) (select.py:220) as products
+  double pk = n2;
+  if (ri >= 2) pk *= pk;
+  if (ri >= 3) pk *= pk;
+  if (ri >= 4) pk *= pk;
+  const double t1 = sastre_tail(2 * ri), t2 = sastre_tail(2 * ri + 1);
+  out->m = ri == 1 ? 2 : ri == 2 ? 4 : ri == 3 ? 8 : 15;
+  out->s = s;
+  if (ri < 4) {
+    out->e1 = t1 * pk * n1;
+    out->e2 = t2 * pk * n2;
+  } else {
+    out->e1 = t1 * pk;
+    out->e2 = t2 * pk * n1;
+  }
+  return 0;
+}
+
 // Same walk from the norms themselves (host tests, large-n select kernels).
 EXPMB_HD int select_walk(const double* nrm, int have, double eps, int scheme, Plan* out) {
   if (nrm[0] == 0.0) {  // select.py:172-173

@@ -336,13 +336,11 @@ struct Fused {
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
   }
   __device__ __forceinline__ void mm_hm(const T* __restrict__ L, const T* __restrict__ R, Tile& out) const {
-    // hi*hi and the two lo terms accumulate in separate registers: four
-    // independent HMMA chains instead of two 6-deep ones (latency-bound)
-    float acc[2][4], accl[2][4];
+    float acc[2][4];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[nt][q] = accl[nt][q] = 0.f;
+      for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
     const int g8 = tr, t4 = tc;  // mma groupID / threadID_in_group
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
@@ -357,17 +355,17 @@ struct Fused {
         uint32_t bh0, bl0, bh1, bl1;
         split_tf32(R[(k0 + t4) * LDR + 8 * nt + g8], bh0, bl0);
         split_tf32(R[(k0 + t4 + 4) * LDR + 8 * nt + g8], bh1, bl1);
-        hmma(accl[nt], al, bh0, bh1);
+        hmma(acc[nt], al, bh0, bh1);  // small terms first
+        hmma(acc[nt], ah, bl0, bl1);
         hmma(acc[nt], ah, bh0, bh1);
-        hmma(accl[nt], ah, bl0, bl1);
       }
     }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      out[0][2 * nt] = acc[nt][0] + accl[nt][0];
-      out[0][2 * nt + 1] = acc[nt][1] + accl[nt][1];
-      out[1][2 * nt] = acc[nt][2] + accl[nt][2];
-      out[1][2 * nt + 1] = acc[nt][3] + accl[nt][3];
+      out[0][2 * nt] = acc[nt][0];
+      out[0][2 * nt + 1] = acc[nt][1];
+      out[1][2 * nt] = acc[nt][2];
+      out[1][2 * nt + 1] = acc[nt][3];
     }
   }
 

@@ -227,6 +227,22 @@ class HostPipeline:
         self.bounds = sorted({min(B, ((B * k) // c) // 4 * 4) for k in range(c)} | {B})
         if self.bounds[0] != 0:
             self.bounds = [0] + self.bounds
+        # per-chunk C-ABI argument tuples and events, built once (the Python
+        # per-chunk overhead otherwise dominated beyond ~8 chunks)
+        L = _lib.lib()
+        self._dt = _lib.EXPMB_F32 if dtype == torch.float32 else _lib.EXPMB_F64
+        cmax = max((b - a for a, b in zip(self.bounds[:-1], self.bounds[1:])), default=0)
+        self._wsb = {code: int(L.expmb_workspace_bytes(cmax, n, self._dt, code)) for code in (0, 1, 2)}
+        self._ws = torch.empty(max(max(self._wsb.values()), 1), dtype=torch.uint8, device=self.dev)
+        esz = self.Wd.element_size()
+        self._chunks = []
+        for a, b in zip(self.bounds[:-1], self.bounds[1:]):
+            if a == b:
+                continue
+            ptrs = [self.pd[k].data_ptr() + a * self.pd[k][0:1].numel() * self.pd[k].element_size()
+                    for k in ("m", "s", "e1", "e2", "norms", "mults", "nonfinite")]
+            self._chunks.append((a, b, self.Wd.data_ptr() + a * n * n * esz, self.Xd.data_ptr() + a * n * n * esz,
+                                 ptrs, torch.cuda.Event(), torch.cuda.Event()))
         self.h2d_bytes = B * n * n * self.Wd.element_size()
         self.d2h_bytes = self.h2d_bytes + sum(v.numel() * v.element_size() for v in self.host.values())
 
@@ -242,20 +258,23 @@ class HostPipeline:
         if not Wf.is_contiguous():
             Wf = Wf.contiguous()
         check_tolerance(eps, W.dtype)
+        code = _SCHEMES.get(scheme, _lib.EXPMB_BASELINE if scheme == SCHEME_BASELINE else None)
+        if code is None:
+            raise MatrixError(f"unknown scheme {scheme!r}; expected 'ps' or 'sastre'")
+        L = _lib.lib()
+        wsp, wsb = self._ws.data_ptr(), self._wsb[code]
         s_in, s_comp, s_out = self.streams
         s_in.wait_stream(torch.cuda.current_stream(self.dev))
-        for a, b in zip(self.bounds[:-1], self.bounds[1:]):
-            if a == b:
-                continue
+        comp_handle = s_comp.cuda_stream
+        for a, b, wp, xp, ptrs, ev_in, ev_c in self._chunks:
             with torch.cuda.stream(s_in):
                 self.Wd[a:b].copy_(Wf[a:b], non_blocking=True)
-                ev_in = torch.cuda.Event()
                 ev_in.record(s_in)
-            with torch.cuda.stream(s_comp):
-                s_comp.wait_event(ev_in)
-                expm_into(self.Wd[a:b], self.Xd[a:b], eps, scheme, {k: v[a:b] for k, v in self.pd.items()})
-                ev_c = torch.cuda.Event()
-                ev_c.record(s_comp)
+            s_comp.wait_event(ev_in)
+            rc = L.expmb_expm(wp, xp, b - a, n, self._dt, float(eps), code, *ptrs, wsp, wsb, comp_handle)
+            if rc != 0:
+                _raise_rc(rc)
+            ev_c.record(s_comp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_c)
                 self.out[a:b].copy_(self.Xd[a:b], non_blocking=True)

@@ -1,8 +1,9 @@
 // large.cuh -- batched expm for n > 64: bucketed GEMM pipeline.
 //
 // Same algorithm as engine.py:119-152, re-scheduled for a batch:
-//   K_norm    ||W||_1 per matrix + the m=1 rung (select.py:169-188); decides
-//             which matrices need W^2 (device flag, no host sync).
+//   K_colsum  ||W||_1 slab partials + K_select(have=1): the m=1 rung
+//             (select.py:169-188); decides which matrices need W^2 (device
+//             flag, no host sync).
 //   G stage0  W^2 = W W for flagged matrices, epilogue writes per-tile column
 //             abs-sum partials (select.py:192-193).  PS: W^3, W^4 likewise.
 //   K_select  ||W^2||_1 (fixed-order reduction of the partials) and the
@@ -95,44 +96,6 @@ static inline size_t large_workspace_bytes(int64_t batch, int n, int esize, int 
 // ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
-
-// ||W||_1 (column abs-sums in binary64, fixed order) + the first ladder rung.
-template <typename T>
-__global__ void __launch_bounds__(256) k_norm1(const T* __restrict__ W, int n, double eps, int scheme,
-                                               double* __restrict__ nrm4, int* __restrict__ need,
-                                               int8_t* __restrict__ pm, int8_t* __restrict__ ps,
-                                               double* __restrict__ pe1, double* __restrict__ pe2) {
-  const int z = blockIdx.x;
-  const T* w = W + (size_t)z * n * n;
-  __shared__ double red[256];
-  double mx = -INFINITY;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    double a = 0.0;
-    for (int r = 0; r < n; ++r) a += fabs((double)w[(size_t)r * n + c]);
-    mx = nanmax(mx, a);
-  }
-  red[threadIdx.x] = mx;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] = nanmax(red[threadIdx.x], red[threadIdx.x + off]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    double nr[4] = {red[0], NAN, NAN, NAN};
-    nrm4[4 * z + 0] = nr[0];
-    nrm4[4 * z + 1] = NAN;
-    Plan p{0, 0, 0.0, 0.0};
-    int nd = 0;
-    if (nr[0] != 0.0) {
-      const double lw[4] = {log2_or_ninf(nr[0]), 0.0, 0.0, 0.0};
-      nd = select_walk_lw(lw, 1, eps, scheme, &p);  // eps carries log2(eps) here
-    }
-    need[z] = nd;
-    if (nd == 0) {
-      pm[z] = (int8_t)p.m; ps[z] = (int8_t)p.s; pe1[z] = p.e1; pe2[z] = p.e2;
-    }
-  }
-}
 
 // Reduce the per-tile column partials of W^p and walk the ladder again.
 __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part, int tiles_m, int n, int have,

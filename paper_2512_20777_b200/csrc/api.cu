@@ -92,6 +92,9 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
     static const int variant = getenv("EXPMB_VARIANT") ? atoi(getenv("EXPMB_VARIANT")) : 2;
     if constexpr (sizeof(T) == 4) {
       if (minb == 3) {
+        if constexpr (SCHEME == 0) {
+          if (variant == 2) return launch_fused<T, 16, 2, 8, SCHEME, 3, 2>(W, X, batch, n, eps, po, c16, st);
+        }
         if (SCHEME == 0 && straight) return launch_fused<T, 16, 2, 8, SCHEME, 3, 1>(W, X, batch, n, eps, po, c16, st);
         return launch_fused<T, 16, 2, 8, SCHEME, 3>(W, X, batch, n, eps, po, c16, st);
       }

@@ -142,6 +142,7 @@ template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, bool HM = false>
 struct Fused {
   static_assert(!HM || (sizeof(T) == 4 && NPAD == 16 && TM == 2), "HM is the fp32 n<=16 warp kernel");
   static constexpr int LDL = 20, LDR = 24;  // HM: A-fragment / B-fragment conflict-free strides
+  static constexpr bool HMODE = HM;
   static constexpr int TC = NPAD / 4;            // column quads
   static constexpr int TR = NPAD / TM;           // row phases
   static constexpr int TPG = TC * TR;            // threads per group
@@ -618,9 +619,18 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
         const T* src = W + nidx * nn;
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
-          const int off = f.row(i) * NPAD + f.col(0);
-          const uint32_t d = (uint32_t)__cvta_generic_to_shared(f.stage + off);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + off) : "memory");
+          if constexpr (F::HMODE) {  // two 8-byte column pairs per row
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int off = f.row(i) * NPAD + f.col(2 * h);
+              const uint32_t d = (uint32_t)__cvta_generic_to_shared(f.stage + off);
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + off) : "memory");
+            }
+          } else {
+            const int off = f.row(i) * NPAD + f.col(0);
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(f.stage + off);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + off) : "memory");
+          }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
@@ -934,8 +944,14 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
           asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
           for (int i = 0; i < TM; ++i) {
-            const float4 v = *reinterpret_cast<const float4*>(f.stage + f.row(i) * NPAD + f.col(0));
-            B[i][0] = v.x; B[i][1] = v.y; B[i][2] = v.z; B[i][3] = v.w;
+            if constexpr (F::HMODE) {
+              const float2 v0 = *reinterpret_cast<const float2*>(f.stage + f.row(i) * NPAD + f.col(0));
+              const float2 v1 = *reinterpret_cast<const float2*>(f.stage + f.row(i) * NPAD + f.col(2));
+              B[i][0] = v0.x; B[i][1] = v0.y; B[i][2] = v1.x; B[i][3] = v1.y;
+            } else {
+              const float4 v = *reinterpret_cast<const float4*>(f.stage + f.row(i) * NPAD + f.col(0));
+              B[i][0] = v.x; B[i][1] = v.y; B[i][2] = v.z; B[i][3] = v.w;
+            }
           }
         } else {
           f.load(W + nidx * nn, n, vec, B);

@@ -421,10 +421,13 @@ struct Fused {
 #pragma unroll
       for (int j = 0; j < 4; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], off);
     if constexpr (WARPS_PG == 1) {
-      double mx = nanmax(nanmax((double)cs[0], (double)cs[1]), nanmax((double)cs[2], (double)cs[3]));
+      // max in the working precision (a double max + 64-bit shuffles was 6%
+      // of the C2 kernel); NaN still propagates
+      auto nmax = [](T a, T b) { return (a > b || a != a) ? a : b; };
+      T mx = nmax(nmax(cs[0], cs[1]), nmax(cs[2], cs[3]));
 #pragma unroll
-      for (int off = 1; off < TC; off *= 2) mx = nanmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      return mx;
+      for (int off = 1; off < TC; off *= 2) mx = nmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      return (double)mx;
     } else {
       const int w = t / 32, lane = t % 32;
       if (lane < TC) {  // lanes 0..TC-1 hold tr = first row phase of this warp, tc = lane

@@ -361,9 +361,19 @@ def run_ours(args):
                     "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
                     "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
                     "useful_flops_per_launch": flops}
-        roof = dict(hbm_roof if t_hbm >= t_cmp else cmp_roof)
-        roof["kernel"] = "expm_fused_kernel" if cfg.n <= 64 else "gemm_stage_kernel"
-        roof["other"] = cmp_roof if t_hbm >= t_cmp else hbm_roof
+        # fp32 n <= 16 runs its products as 3xTF32 mma.sync (3 x 1.648e9 TC flops
+        # at 266.6 TF/s = 18.5 us < the 20.5 us HBM floor): the binding
+        # roofline is HBM.  Elsewhere: the larger of the two lower bounds.
+        tc_products = cfg.dtype == "f32" and cfg.n <= 16 and args.scheme == "sastre"
+        hbm_binds = t_hbm >= t_cmp or tc_products
+        roof = dict(hbm_roof if hbm_binds else cmp_roof)
+        if cfg.n <= 16:
+            roof["kernel"] = "expm_fused_kernel<float,16,2,8,0,2,2> (3xTF32 mma.sync)" if tc_products else "expm_fused_kernel"
+        elif cfg.n <= 64:
+            roof["kernel"] = "expm_dmma_kernel (DMMA)" if cfg.dtype == "f64" else "expm_fused_kernel"
+        else:
+            roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
+        roof["other"] = cmp_roof if hbm_binds else hbm_roof
         cpu = None
         if not args.no_cpu_baseline:
             r, cores, sample = cpu_reference_rate(cfg.key)

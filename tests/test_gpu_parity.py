@@ -361,3 +361,60 @@ def test_large_path_nonfinite(dtype):
     assert r.nonfinite.tolist() == [False, True, True]
     good = X.expm(Wt[:1], 1e-6).value
     assert torch.equal(good[0], r.value[0])
+
+
+# ---------------------------------------------------------------------------
+# the reference's acceptance criteria (test_acceptance.py) on the GPU path
+# ---------------------------------------------------------------------------
+
+def test_acceptance_04_forward_accuracy_vs_scipy():
+    """Criterion 4 (test_acceptance.py:124-139): error <= 1e-7 at eps = 1e-8,
+    here against scipy's Pade expm (the reference's own cross-check oracle,
+    test_oracle.py:110-122)."""
+    sla = pytest.importorskip("scipy.linalg")
+    rng = np.random.default_rng(9000)
+    norms = np.geomspace(1e-2, 10.0, 60)
+    for i, target in enumerate(norms):
+        n = (8, 16, 32, 64)[i % 4]
+        a = rng.uniform(-1, 1, (n, n))
+        W = a * target / np.abs(a).sum(axis=0).max()
+        ref = sla.expm(W)
+        for scheme in ("sastre", "ps"):
+            got = _run(W[None], 1e-8, scheme).value[0].cpu().numpy()
+            err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+            assert err <= 1e-7, (n, target, scheme, err)
+
+
+def test_acceptance_07_selector_sanity():
+    """Criterion 7 (test_acceptance.py:201-219)."""
+    rng = np.random.default_rng(7)
+    Ws = []
+    for _ in range(40):
+        n = int(rng.integers(1, 16))
+        a = rng.uniform(-1, 1, (n, n))
+        W = np.zeros((16, 16))
+        W[:n, :n] = a * (10.0 ** rng.uniform(-6, 2)) / np.abs(a).sum(axis=0).max()
+        Ws.append(W)
+    Wt = np.stack(Ws)
+    for scheme in ("sastre", "ps"):
+        r = _run(Wt, 1e-8, scheme, check_finite=False)
+        s = r.plan.s.cpu().numpy()
+        e = (r.plan.e1 + r.plan.e2).cpu().numpy()
+        assert (s >= 0).all() and (s <= 20).all()
+        assert (s[e <= 1e-8] == 0).all()
+        assert int(_run(np.array([[[1e60]]]), 1e-8, scheme, check_finite=False).plan.s[0]) == 20
+        costs = [_run(Wt[:10, :12, :12], eps, scheme).mults.cpu().numpy() for eps in (1e-12, 1e-8, 1e-4)]
+        assert (costs[0] >= costs[1]).all() and (costs[1] >= costs[2]).all()
+
+
+def test_acceptance_08_logdet_equals_trace():
+    """Criterion 8 (test_acceptance.py:226-249): log det e^W = tr W."""
+    rng = np.random.default_rng(8)
+    for n in (4, 16, 40, 96):
+        a = rng.uniform(-1, 1, (6, n, n))
+        W = a * (rng.uniform(0.5, 2.0, 6) / np.abs(a).sum(axis=1).max(axis=1))[:, None, None]
+        X_ = X.expm(torch.as_tensor(W).cuda(), 1e-12).value
+        sign, logdet = torch.linalg.slogdet(X_)
+        tr = np.trace(W, axis1=1, axis2=2)
+        assert (sign.cpu().numpy() == 1.0).all()
+        np.testing.assert_allclose(logdet.cpu().numpy(), tr, rtol=0, atol=1e-8 * np.abs(tr).max() + 1e-12)

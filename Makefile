@@ -8,7 +8,10 @@ HDR := $(wildcard $(PKG)/csrc/*.cuh) include/expmb.h
 
 all: $(PKG)/libexpmb.so
 
-tools: tools/peaks
+tools: tools/peaks tools/tc_probe
+
+tools/tc_probe: tools/tc_probe.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
 
 tools/peaks: tools/peaks.cu
 	$(NVCC) $(ARCH) -O3 -o $@ $<

@@ -226,6 +226,178 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Low-rank path: --config LR
+# ---------------------------------------------------------------------------
+
+def _cpu_lr_chunk(args):
+    A1, A2, eps = args
+    from oracle import expm_oracle as O
+    for i in range(A1.shape[0]):
+        O.expm_lowrank(A1[i], A2[i], eps)
+    return A1.shape[0]
+
+
+def cpu_lowrank_rate(count: int = 4096, cores: int | None = None):
+    """pairs/s of the reference's expm_lowrank (oracle port) over a process pool."""
+    from concurrent.futures import ProcessPoolExecutor
+    cores = cores or os.cpu_count() or 1
+    A1, A2 = WL.generate_lowrank(np.arange(count))
+    eps = WL.LOWRANK.eps
+    parts = np.array_split(np.arange(count), max(1, min(count, cores * 4)))
+    with ProcessPoolExecutor(max_workers=cores, initializer=_cpu_worker_init) as pool:
+        list(pool.map(_cpu_lr_chunk, [(A1[:1], A2[:1], eps)] * min(cores, 2)))
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cpu_lr_chunk, [(A1[p], A2[p], eps) for p in parts]))
+        dt = time.perf_counter() - t0
+    return done / dt, cores, f"{done} pairs of LR (n 64, t 8, fp64; process pool x{cores}, 1 BLAS thread each)"
+
+
+def run_lowrank(args):
+    cfg = WL.LOWRANK
+    n, t = cfg.n, WL.LOWRANK_T
+    ws, rank, local = _dist_env()
+    base = {"metric": "low-rank matrix exponentials/s", "unit": "exps/s", "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "steps": args.steps, "warmup": max(3, args.warmup)}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        for _ in range(args.warmup):
+            cpu_lowrank_rate(512)
+        rates = []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r, cores, sample = cpu_lowrank_rate()
+            rates.append(r)
+        value = statistics.median(rates)
+        line = dict(base, impl="reference", value=value, n_gpus=args.gpus,
+                    ms_per_step=1e3 * (time.perf_counter() - t0) / max(1, args.steps),
+                    config={"workload": f"LR: {cfg.desc}", "batch": cfg.batch, "n": n, "t": t, "eps": cfg.eps},
+                    cpu_baseline={"value": value, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample},
+                    e2e={"value": value, "unit": "exps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2512_20777_b200 as XP
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B = args.batch or cfg.batch
+    A1h, A2h = WL.generate_lowrank(np.arange(rank * B, (rank + 1) * B))
+    A1h, A2h = torch.from_numpy(A1h), torch.from_numpy(A2h)
+    A1, A2 = A1h.to(dev), A2h.to(dev)
+    Xd = torch.empty(B, n, n, dtype=torch.float64, device=dev)
+    plan = {"m": torch.empty(B, dtype=torch.int8, device=dev), "e1": torch.empty(B, dtype=torch.float64, device=dev),
+            "e2": torch.empty(B, dtype=torch.float64, device=dev),
+            "norms": torch.empty(B, 2, dtype=torch.float64, device=dev),
+            "mults": torch.empty(B, dtype=torch.int32, device=dev),
+            "flags": torch.empty(B, dtype=torch.uint8, device=dev)}
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        XP.expm_lowrank_into(A1, A2, Xd, cfg.eps, plan)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    assert not plan["flags"].any(), "flagged matrices in the LR bench batch"
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.05)
+        clk.mark("start")
+        torch.cuda._sleep(int(min(args.steps, 200) * 400_000))
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        clk.mark("end")
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / args.steps
+    value = ws * B / (ms_per_step * 1e-3)
+
+    # e2e: pinned host factors in, pinned e^W + plan out, 8 chunks over 3 streams
+    A1p, A2p = A1h.pin_memory(), A2h.pin_memory()
+    Xp = torch.empty(B, n, n, dtype=torch.float64, pin_memory=True)
+    ph = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in plan.items()}
+    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    bounds = [B * c // 8 for c in range(9)]
+
+    def e2e_step():
+        for c in range(8):
+            a, b = bounds[c], bounds[c + 1]
+            st = streams[c % 3]
+            with torch.cuda.stream(st):
+                A1[a:b].copy_(A1p[a:b], non_blocking=True)
+                A2[a:b].copy_(A2p[a:b], non_blocking=True)
+                XP.expm_lowrank_into(A1[a:b], A2[a:b], Xd[a:b], cfg.eps, {k: v[a:b] for k, v in plan.items()})
+                Xp[a:b].copy_(Xd[a:b], non_blocking=True)
+                for k, v in plan.items():
+                    ph[k][a:b].copy_(v[a:b], non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    if ws > 1:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = ws * B / (float(et.item()) / args.steps * 1e-3)
+    h2d = (A1h.numel() + A2h.numel()) * 8
+    d2h = Xp.numel() * 8 + sum(v.numel() * v.element_size() for v in ph.values())
+    if rank == 0:
+        pk = _peaks()
+        hbm_bytes = B * (2 * n * t + n * n) * 8
+        gbs = hbm_bytes / (ms_per_step * 1e-3) / 1e9
+        ms_ = plan["m"].cpu().numpy()
+        mults = plan["mults"].long().cpu().numpy()
+        flops = float(B * (2 * t * t * n * 2 + 2 * n * n * t) + (mults * 2 * t ** 3).sum())
+        roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / pk["hbm_gbs"], "traffic": None, "peak_source": pk["hbm_src"],
+                "algorithmic_bytes_per_launch": hbm_bytes, "kernel": "expm_lowrank_kernel<double,8>",
+                "other": {"bound": "fp64_dfma", "achieved": flops / (ms_per_step * 1e-3) / 1e12,
+                          "peak": pk["dfma_fp64"], "unit": "TFLOP/s", "useful_flops_per_launch": flops}}
+        cpu = None
+        if not args.no_cpu_baseline:
+            r, cores, sample = cpu_lowrank_rate()
+            cpu = {"value": r, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample}
+        hist = {}
+        for mm in ms_.tolist():
+            hist[str(mm)] = hist.get(str(mm), 0) + 1
+        line = dict(base, value=value, n_gpus=ws, ms_per_step=ms_per_step,
+                    config={"workload": f"LR: {cfg.desc}", "batch_per_gpu": B, "global_batch": ws * B, "n": n,
+                            "t": t, "eps": cfg.eps, "l2": "flushed between steps (252 MB write)",
+                            "timing": "per-step CUDA events, host queue primed",
+                            "parallelism": f"batch-sharded x{ws}, no collective on the hot path"},
+                    hbm_gbs=gbs, roofline=roof, cpu_baseline=cpu,
+                    e2e={"value": e2e_value, "unit": "exps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                         "ms_per_step": float(et.item()) / args.steps},
+                    gpu_launches=args.steps, clocks=clk.summary(), order_histogram=hist,
+                    mults_total=int(mults.sum()), rect_mults_total=3 * B)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def _launch_count(key, m, s, n):
     """Kernels of ours launched by one expm call (host orchestration is deterministic)."""
     if n <= 64:
@@ -416,14 +588,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(WL.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(WL.CONFIGS) + ["LR"],
+                    help="C1..C5 = BASELINE.json configs; LR = the low-rank path (SURVEY 8(f) rank 2)")
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scheme", default="sastre", choices=["sastre", "ps", "baseline"],
                     help="evaluation route (baseline = Alg. 1, the paper's comparator; n <= 64)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.config == "LR":
+        run_lowrank(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

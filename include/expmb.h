@@ -99,6 +99,37 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype,
 int expmb_select_host(const double* norms, double eps, int scheme,
                       int* m, int* s, double* e1, double* e2);
 
+/*
+ * Batched low-rank exponential.  Replaces engine.py:198-257 (expm_lowrank)
+ * with the LowRankPair checks of engine.py:166-181: for W = A1 A2 returns
+ * e^W = I + A1 psi(V) A2, V = A2 A1, psi(x) = sum_{i<=m} x^i/(i+1)!, the
+ * order m chosen on LOWRANK_ORDERS = (1,2,4,8,15,16,20,25,30) (no scaling).
+ *
+ *   A1         [batch,n,t] device, row-major     (LowRankPair.a1)
+ *   A2         [batch,t,n] device, row-major     (LowRankPair.a2)
+ *   X          [batch,n,n] output e^(A1 A2)
+ *   1 <= t <= n (MatrixError otherwise); t <= 32 (EXPMB_ERR_UNSUPPORTED)
+ *   m, e1, e2  [batch] plan (EvalPlan.m/.e1/.e2; s is always 0)
+ *   norms      [batch,2] ||V||_1, ||V^2||_1 (NaN if V^2 never formed)
+ *   mults      [batch] t x t products (ExpmResult.mults; rect_mults is 3)
+ *   flags      [batch] EXPMB_LR_* bits; a flagged matrix's X is NaN
+ * Any of m..flags may be NULL.  No workspace, no host synchronisation.
+ */
+#define EXPMB_LR_BAD_INPUT 1 /* non-finite factor entry: MatrixError (engine.py:179-180)  */
+#define EXPMB_LR_NONFINITE 2 /* V, a power, psi or e^W not finite: NonFiniteError        */
+#define EXPMB_LR_NO_ORDER 4  /* no admissible order: LowRankOrderError (engine.py:236-240) */
+int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, int32_t n, int32_t t,
+                       int dtype, double eps, int8_t* m, double* e1, double* e2, double* norms,
+                       int32_t* mults, uint8_t* flags, void* stream);
+
+/*
+ * Host evaluation of the low-rank ladder the kernel runs (engine.py:224-244):
+ * norms[0] = ||V||_1, norms[1] = ||V^2||_1 (read only when have_v2).
+ * Returns 0 (plan written), 1 (||V^2||_1 needed: call again with have_v2 = 1)
+ * or -1 (no admissible order).
+ */
+int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int* m, double* e1, double* e2);
+
 #ifdef __cplusplus
 }
 #endif

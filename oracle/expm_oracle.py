@@ -28,6 +28,8 @@ Reference map (file:line under /root/reference/pkg/src/expmkit):
   * squaring ............................... engine.py:80-87
   * expm_baseline (Alg. 1) .................. engine.py:90-116
   * finiteness semantics (_wrap) ........... matrix.py:56-57, 95-102
+  * expm_lowrank / LowRankPair checks ...... engine.py:159-270
+  * phi1 coefficients 1/(i+1)! ............. poly.py:62-66
 """
 
 from __future__ import annotations
@@ -438,3 +440,109 @@ def expm_baseline(W, eps: float, tol_floor: float = UNIT_ROUNDOFF) -> Result:
     for _ in range(s):
         X = _mm(X, X, ledger)
     return Result(X, k - 2, s, one_norm(Y), 0.0, norm1, float("nan"), ledger[0])
+
+
+# ---------------------------------------------------------------------------
+# Low-rank path (engine.py:159-270): W = A1 A2, e^W = I + A1 psi(V) A2, V = A2 A1
+# ---------------------------------------------------------------------------
+
+LOWRANK_ORDERS = (1, 2, 4, 8, 15, 16, 20, 25, 30)                  # engine.py:195
+LOG2_FACT = [math.lgamma(i + 1) / math.log(2.0) for i in range(40)]  # engine.py:260
+
+
+class LowRankOrderError(ArithmeticError):
+    """engine.py:60 -- no order on the ladder meets the tolerance (no scaling)."""
+
+
+def _power_bound_log(q: int, lw1: float, lw2: float) -> float:
+    """engine.py:263-265: log2 of ||V^2||^(q//2) ||V||^(q%2)."""
+    return (q // 2) * lw2 + (q % 2) * lw1
+
+
+def select_lowrank_from_norms(nv: float, nv2, eps: float):
+    """The order ladder of engine.py:224-244 on given norms.  ``nv2`` may be a
+    callable producing ||V^2||_1 lazily (the reference forms V^2 only when
+    rung m=1 fails).  Returns (m, e1, e2, used_v2) or raises LowRankOrderError."""
+    if nv == 0.0:
+        return 0, 0.0, 0.0, False
+    log_eps = math.log2(eps)
+    lw1 = math.log2(nv) if nv > 0 else -math.inf
+    lw2 = None
+    used = False
+    for m in LOWRANK_ORDERS:
+        if m >= 2 and lw2 is None:
+            n2 = nv2() if callable(nv2) else nv2
+            used = True
+            lw2 = math.log2(n2) if n2 > 0 else -math.inf
+        if m == 1:
+            l1 = 2 * lw1 - LOG2_FACT[3]
+            l2 = 3 * lw1 - LOG2_FACT[4]
+        else:
+            l1 = _power_bound_log(m + 1, lw1, lw2) - LOG2_FACT[m + 2]
+            l2 = _power_bound_log(m + 2, lw1, lw2) - LOG2_FACT[m + 3]
+        if float(np.logaddexp2(l1, l2)) <= log_eps:
+            with np.errstate(over="ignore"):
+                return m, float(np.exp2(l1)), float(np.exp2(l2)), used
+    raise LowRankOrderError(f"||V||_1 = {nv:.6g} admits no order <= {LOWRANK_ORDERS[-1]} at tolerance {eps:.3g}")
+
+
+@dataclass
+class LowRankResult:
+    value: np.ndarray
+    m: int
+    e1: float
+    e2: float
+    norm1: float
+    norm2: float
+    mults: int
+    rect_mults: int
+
+
+def expm_lowrank(a1, a2, eps: float, tol_floor: float = UNIT_ROUNDOFF) -> LowRankResult:
+    """engine.py:198-257 restated (LowRankPair validation engine.py:166-181)."""
+    a1 = np.array(a1, dtype=np.float64)
+    a2 = np.array(a2, dtype=np.float64)
+    if a1.ndim != 2 or a2.ndim != 2:
+        raise MatrixError("low-rank factors must be 2-d arrays")
+    n, t = a1.shape
+    if a2.shape != (t, n):
+        raise MatrixError(f"factor shapes incompatible: {a1.shape} and {a2.shape}")
+    if t > n:
+        raise MatrixError(f"inner rank {t} exceeds order {n}")
+    if not (np.isfinite(a1).all() and np.isfinite(a2).all()):
+        raise MatrixError("low-rank factors must be finite")
+    eps = check_tolerance(eps, tol_floor)
+    ledger = [0]
+    V = _wrap(a2 @ a1)
+    nv = one_norm(V)
+    powers = {1: V}
+    norms = {}
+
+    def v2():
+        powers[2] = _mm(V, V, ledger)
+        norms[2] = one_norm(powers[2])
+        return norms[2]
+
+    m, e1, e2, _ = select_lowrank_from_norms(nv, v2, eps)
+    if m == 0:
+        psi = np.eye(t)
+    else:
+        psi = _ps_eval([inv_factorial(i + 1) for i in range(m + 1)], V, ledger, powers)
+    out = _wrap(np.eye(n) + a1 @ (psi @ a2))
+    return LowRankResult(out, m, e1, e2, nv, norms.get(2, float("nan")), ledger[0], 3)
+
+
+def lowrank_near_threshold(nv: float, nv2: float, eps: float, margin: float = 1e-4) -> bool:
+    """True when the low-rank order would change if log2 ||V||_1 or log2 ||V^2||_1
+    moved by ``margin`` (the same exemption as ``near_threshold``)."""
+    def pick(a, b):
+        try:
+            return select_lowrank_from_norms(a, b, eps)[0]
+        except LowRankOrderError:
+            return -1
+    base = pick(nv, nv2)
+    for d1 in (-margin, 0.0, margin):
+        for d2 in (-margin, 0.0, margin):
+            if pick(nv * 2.0 ** d1, nv2 * 2.0 ** d2) != base:
+                return True
+    return False

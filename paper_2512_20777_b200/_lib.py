@@ -32,7 +32,11 @@ EXPORTS = (
     "expmb_workspace_bytes",
     "expmb_expm",
     "expmb_select_host",
+    "expmb_expm_lowrank",
+    "expmb_select_lowrank_host",
 )
+
+LR_BAD_INPUT, LR_NONFINITE, LR_NO_ORDER = 1, 2, 4
 
 _lib = None
 
@@ -67,6 +71,16 @@ def lib() -> ctypes.CDLL:
         c.POINTER(c.c_double), c.c_double, c.c_int,
         c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
     ]
+    L.expmb_expm_lowrank.restype = c.c_int
+    L.expmb_expm_lowrank.argtypes = [
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_int, c.c_double,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+    ]
+    L.expmb_select_lowrank_host.restype = c.c_int
+    L.expmb_select_lowrank_host.argtypes = [
+        c.POINTER(c.c_double), c.c_int, c.c_double,
+        c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
+    ]
     _lib = L
     return L
 
@@ -84,3 +98,15 @@ def select_host(norms, eps: float, scheme: int):
     have = L.expmb_select_host(arr, float(eps), int(scheme), ctypes.byref(m), ctypes.byref(s),
                                ctypes.byref(e1), ctypes.byref(e2))
     return m.value, s.value, e1.value, e2.value, have
+
+
+def select_lowrank_host(nv: float, nv2: float | None, eps: float):
+    """The low-rank kernel's ladder on the host: (rc, m, e1, e2); rc 0 = chosen,
+    1 = ||V^2||_1 needed, -1 = no admissible order."""
+    L = lib()
+    arr = (ctypes.c_double * 2)(float(nv), float("nan") if nv2 is None else float(nv2))
+    m = ctypes.c_int(-1)
+    e1, e2 = ctypes.c_double(float("nan")), ctypes.c_double(float("nan"))
+    rc = L.expmb_select_lowrank_host(arr, 0 if nv2 is None else 1, float(eps), ctypes.byref(m),
+                                     ctypes.byref(e1), ctypes.byref(e2))
+    return rc, m.value, e1.value, e2.value

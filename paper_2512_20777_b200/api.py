@@ -26,8 +26,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .tables import (MatrixError, NonFiniteError, SCHEME_PS, SCHEME_SASTRE, ToleranceError,
-                     UNIT_ROUNDOFF, UNIT_ROUNDOFF_F32)
+from .tables import (LowRankOrderError, MatrixError, NonFiniteError, SCHEME_LOWRANK, SCHEME_PS, SCHEME_SASTRE,
+                     ToleranceError, UNIT_ROUNDOFF, UNIT_ROUNDOFF_F32)
 
 _SCHEMES = {SCHEME_SASTRE: _lib.EXPMB_SASTRE, SCHEME_PS: _lib.EXPMB_PS}
 SCHEME_BASELINE = "baseline"  # select.py:58
@@ -52,6 +52,7 @@ class ExpmResult:
     mults: torch.Tensor   # int32 [...]
     wall_time: float
     nonfinite: torch.Tensor  # bool [...]
+    rect_mults: int = 0      # engine.py:77 (3 on the low-rank path)
 
 
 def unit_roundoff(dtype: torch.dtype) -> float:
@@ -315,3 +316,135 @@ def select_sastre(W: torch.Tensor, eps: float) -> EvalPlan:
 def select_ps(W: torch.Tensor, eps: float) -> EvalPlan:
     """select.py:223-225, batched."""
     return expm(W, eps, SCHEME_PS, check_finite=False).plan
+
+
+# ---------------------------------------------------------------------------
+# Low-rank path (SURVEY 8(f) rank 2): engine.py:159-257
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LowRankPair:
+    """Batched engine.py:159-191: W = A1 A2 with a1 [..., n, t], a2 [..., t, n],
+    1 <= t <= n, on the same CUDA device and dtype (fp32/fp64).  Shapes are
+    checked here (MatrixError, engine.py:168-178); the finiteness check of
+    engine.py:179-180 runs on the device inside ``expm_lowrank`` so building a
+    pair never synchronises the host."""
+    a1: torch.Tensor
+    a2: torch.Tensor
+
+    def __post_init__(self):
+        a1, a2 = self.a1, self.a2
+        if not isinstance(a1, torch.Tensor) or not isinstance(a2, torch.Tensor):
+            raise MatrixError("low-rank factors must be torch tensors")
+        if a1.dim() < 2 or a2.dim() < 2:
+            raise MatrixError("low-rank factors must be (batched) 2-d arrays")
+        n, t = a1.shape[-2], a1.shape[-1]
+        if tuple(a2.shape[-2:]) != (t, n) or a1.shape[:-2] != a2.shape[:-2]:
+            raise MatrixError(f"factor shapes incompatible: {tuple(a1.shape)} and {tuple(a2.shape)}")
+        if t > n:
+            raise MatrixError(f"inner rank {t} exceeds order {n}")
+        if t < 1:
+            raise MatrixError("inner rank must be at least 1")
+        if a1.dtype != a2.dtype or a1.dtype not in (torch.float32, torch.float64):
+            raise MatrixError("factors must share dtype float32 or float64")
+
+    @property
+    def n(self) -> int:
+        return self.a1.shape[-2]
+
+    @property
+    def t(self) -> int:
+        return self.a1.shape[-1]
+
+
+@torch.library.custom_op("expmkit_b200::expm_lowrank", mutates_args=())
+def _expm_lowrank_op(A1: torch.Tensor, A2: torch.Tensor, eps: float) -> tuple[
+        torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    B, n, t = A1.shape
+    dev = A1.device
+    X = torch.empty(B, n, n, dtype=A1.dtype, device=dev)
+    m = torch.empty(B, dtype=torch.int8, device=dev)
+    e1 = torch.empty(B, dtype=torch.float64, device=dev)
+    e2 = torch.empty(B, dtype=torch.float64, device=dev)
+    norms = torch.empty(B, 2, dtype=torch.float64, device=dev)
+    mults = torch.empty(B, dtype=torch.int32, device=dev)
+    flags = torch.empty(B, dtype=torch.uint8, device=dev)
+    L = _lib.lib()
+    dt = _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64
+    rc = L.expmb_expm_lowrank(A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t, dt, float(eps),
+                              m.data_ptr(), e1.data_ptr(), e2.data_ptr(), norms.data_ptr(), mults.data_ptr(),
+                              flags.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    if rc != 0:
+        _raise_rc(rc)
+    return X, m, e1, e2, norms, mults, flags
+
+
+@_expm_lowrank_op.register_fake
+def _(A1, A2, eps):
+    B, n, t = A1.shape
+    return (A1.new_empty(B, n, n), A1.new_empty(B, dtype=torch.int8), A1.new_empty(B, dtype=torch.float64),
+            A1.new_empty(B, dtype=torch.float64), A1.new_empty(B, 2, dtype=torch.float64),
+            A1.new_empty(B, dtype=torch.int32), A1.new_empty(B, dtype=torch.uint8))
+
+
+def expm_lowrank(pair: LowRankPair, eps: float) -> ExpmResult:
+    """Batched engine.py:198-257: e^(A1 A2) = I + A1 psi(V) A2, V = A2 A1, at
+    the smallest order on LOWRANK_ORDERS whose two-term bound meets eps (no
+    scaling; plan.s = 0, plan.scheme = "lowrank").  ``mults`` counts the t x t
+    products, ``rect_mults`` = 3 (A2 A1 and the two assembly products).
+
+    Raises, after the batch completes: MatrixError when a factor holds
+    NaN/Inf (engine.py:179-180), LowRankOrderError when no order qualifies
+    (engine.py:236-240), NonFiniteError when V, psi or the result is not
+    finite (matrix.py:95-102).  t <= 32."""
+    t0 = time.perf_counter()
+    if not isinstance(pair, LowRankPair):
+        pair = LowRankPair(*pair)
+    a1, a2 = pair.a1, pair.a2
+    if a1.device.type != "cuda" or a2.device != a1.device:
+        raise RuntimeError("expmkit_b200.expm_lowrank runs on CUDA tensors only (no CPU fallback)")
+    check_tolerance(eps, a1.dtype)
+    lead, n, t = a1.shape[:-2], pair.n, pair.t
+    A1 = a1.reshape(-1, n, t).contiguous()
+    A2 = a2.reshape(-1, t, n).contiguous()
+    X, m, e1, e2, norms, mults, flags = torch.ops.expmkit_b200.expm_lowrank(A1, A2, float(eps))
+    if A1.shape[0] > 0 and bool(flags.any()):
+        f = flags.cpu()
+        if bool((f & _lib.LR_BAD_INPUT).any()):
+            raise MatrixError("low-rank factors must be finite")
+        i = int(torch.nonzero(f).flatten()[0])
+        if int(f[i]) & _lib.LR_NO_ORDER:
+            nv = float(norms[i, 0])
+            raise LowRankOrderError(
+                f"||V||_1 = {nv:.6g} admits no order <= 30 at tolerance {float(eps):.3g}; "
+                f"the factored path runs unscaled (batch index {i})")
+        raise NonFiniteError(f"operation produced non-finite entries (batch index {i})")
+    plan = EvalPlan(m.reshape(lead), torch.zeros_like(m).reshape(lead), SCHEME_LOWRANK, e1.reshape(lead),
+                    e2.reshape(lead), norms.reshape(*lead, 2))
+    return ExpmResult(X.reshape(*lead, n, n), plan, mults.reshape(lead), time.perf_counter() - t0,
+                      flags.bool().reshape(lead), rect_mults=3)
+
+
+def expm_lowrank_into(A1: torch.Tensor, A2: torch.Tensor, X: torch.Tensor, eps: float,
+                      plan: dict | None = None) -> None:
+    """Allocation-free, synchronisation-free ``expm_lowrank`` for steady-state
+    loops and CUDA graphs: A1 [B,n,t], A2 [B,t,n], X [B,n,n] contiguous CUDA
+    tensors; plan tensors (keys m, e1, e2, norms, mults, flags) are optional.
+    Errors are left in plan["flags"] (EXPMB_LR_* bits) instead of raised."""
+    LowRankPair(A1, A2)
+    B, n, t = A1.shape
+    if X.shape != (B, n, n) or X.dtype != A1.dtype or not (A1.is_contiguous() and A2.is_contiguous()
+                                                             and X.is_contiguous()):
+        raise MatrixError("X must be contiguous [B, n, n] of the factors' dtype; factors contiguous")
+    check_tolerance(eps, A1.dtype)
+    plan = plan or {}
+
+    def p(k):
+        v = plan.get(k)
+        return None if v is None else v.data_ptr()
+    rc = _lib.lib().expmb_expm_lowrank(
+        A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t,
+        _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64, float(eps),
+        p("m"), p("e1"), p("e2"), p("norms"), p("mults"), p("flags"), torch.cuda.current_stream(A1.device).cuda_stream)
+    if rc != 0:
+        _raise_rc(rc)

@@ -14,6 +14,7 @@
 #include "fused_small.cuh"
 #include "fused_dmma.cuh"
 #include "large.cuh"
+#include "lowrank.cuh"
 
 namespace expmb {
 
@@ -125,6 +126,60 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
 
 using namespace expmb;
 
+// Low-rank path (engine.py:198-257): one CTA per matrix, grid-strided.
+template <typename T, int TP>
+static int launch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
+                          cudaStream_t st) {
+  using L = Lr<T, TP>;
+  auto kern = expm_lowrank_kernel<T, TP>;
+  static int occ = -1;
+  if (occ < 0) {
+    if (L::kSmem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kSmem) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, L::NT, L::kSmem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(batch < persistent ? batch : persistent);
+  kern<<<grid, L::NT, L::kSmem, st>>>(A1, A2, X, batch, n, t, log2(eps), po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
+template <typename T>
+static int launch_lowrank_warp(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
+                               cudaStream_t st) {
+  using L = LrW<T>;
+  auto kern = expm_lowrank_warp_kernel<T>;
+  static int occ = -1;
+  if (occ < 0) {
+    if (L::kSmem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kSmem) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, L::NT, L::kSmem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t ctas = (batch + L::WARPS - 1) / L::WARPS;
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(ctas < persistent ? ctas : persistent);
+  kern<<<grid, L::NT, L::kSmem, st>>>(A1, A2, X, batch, n, t, log2(eps), po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
+template <typename T>
+static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
+                            cudaStream_t st) {
+  static const bool cta_only = getenv("EXPMB_LR_CTA") != nullptr;  // A/B switch
+  if (t <= 8 && n <= 64 && !cta_only) return launch_lowrank_warp<T>(A1, A2, X, batch, n, t, eps, po, st);
+  if (t <= 8) return launch_lowrank<T, 8>(A1, A2, X, batch, n, t, eps, po, st);
+  if (t <= 16) return launch_lowrank<T, 16>(A1, A2, X, batch, n, t, eps, po, st);
+  return launch_lowrank<T, 32>(A1, A2, X, batch, n, t, eps, po, st);
+}
+
 extern "C" {
 
 int expmb_version(void) { return 100; }
@@ -139,7 +194,8 @@ const char* expmb_strerror(int code) {
     case EXPMB_ERR_WORKSPACE: return "workspace missing or smaller than expmb_workspace_bytes()";
     case EXPMB_ERR_CUDA: return "CUDA launch or copy failed";
     case EXPMB_ERR_ALIGN: return "W and X must be 16-byte aligned";
-    case EXPMB_ERR_UNSUPPORTED: return "combination not supported (baseline scheme needs n <= 64)";
+    case EXPMB_ERR_UNSUPPORTED:
+      return "combination not supported (baseline scheme needs n <= 64; low-rank path needs t <= 32)";
     default: return "unknown error";
   }
 }
@@ -212,6 +268,33 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
   return large_expm(W, X, batch, n, dtype, eps, scheme, po, workspace, st);
+}
+
+int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int* m, double* e1, double* e2) {
+  int mm = 0;
+  double a = 0.0, b = 0.0;
+  const int rc = select_lowrank(norms[0], have_v2 ? norms[1] : 0.0, have_v2, log2(eps), &mm, &a, &b);
+  if (rc == 0) {
+    if (m) *m = mm;
+    if (e1) *e1 = a;
+    if (e2) *e2 = b;
+  }
+  return rc;
+}
+
+int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, int32_t n, int32_t t, int dtype,
+                       double eps, int8_t* m, double* e1, double* e2, double* norms, int32_t* mults, uint8_t* flags,
+                       void* stream) {
+  if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
+  if (n < 1 || t < 1 || t > n || batch < 0) return EXPMB_ERR_SHAPE;
+  if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
+  if (t > 32) return EXPMB_ERR_UNSUPPORTED;
+  if (batch == 0) return EXPMB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LrOut po{m, e1, e2, norms, mults, flags};
+  if (dtype == EXPMB_F32)
+    return dispatch_lowrank<float>((const float*)A1, (const float*)A2, (float*)X, batch, n, t, eps, po, st);
+  return dispatch_lowrank<double>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
 }
 
 }  // extern "C"

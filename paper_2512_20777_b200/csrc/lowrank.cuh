@@ -1,0 +1,670 @@
+// lowrank.cuh -- batched low-rank exponential, SURVEY §8(f) rank 2.
+//
+// Reference: expm_lowrank (/root/reference/pkg/src/expmkit/engine.py:198-257)
+// with LowRankPair (engine.py:159-191): for W = A1 A2 (A1 n x t, A2 t x n,
+// t <= n) it returns e^W = I + A1 psi(V) A2 with V = A2 A1 (t x t) and
+// psi(x) = sum_{i<=m} x^i/(i+1)! (poly.py:62-66) evaluated by
+// Paterson-Stockmeyer (poly.py:149-182), unscaled, at the smallest order on
+// LOWRANK_ORDERS (engine.py:195) whose two-term remainder bound meets eps.
+//
+// One CTA per matrix (grid-strided), everything of the t x t problem in
+// shared memory:
+//   phase 1  V = A2 A1, streaming k in 64-wide chunks (A2 rows and the
+//            contiguous A1 row block are both coalesced reads), input
+//            finiteness on the fly;
+//   phase 2  ||V||_1, V^2 only if rung m=1 fails (engine.py:226-230), the
+//            ladder (select_lowrank, host/device shared), PS powers and Horner
+//            stages as t x t shared-memory products;
+//   phase 3  out = I + A1 (psi A2), 64-column chunks of Y = psi A2 kept in
+//            shared memory while 64-row tiles of A1 stream past: every output
+//            element is written exactly once (n^2 per matrix is the HBM
+//            floor of this op).
+// t <= 32 (TP = 8/16/32 padded with zeros, which leaves V's powers and norms
+// unchanged).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "select.cuh"
+#include "lowrank_tables.h"
+
+namespace expmb {
+
+// flags[] bits (include/expmb.h)
+constexpr uint8_t kLrBadInput = 1;   // non-finite factor entry (LowRankPair check, engine.py:179-180)
+constexpr uint8_t kLrNonFinite = 2;  // V, a power, psi or the result not finite (matrix.py:95-102)
+constexpr uint8_t kLrNoOrder = 4;    // LowRankOrderError (engine.py:236-240)
+
+EXPMB_HD int lr_order(int i) {
+  return i == 0 ? 1 : i == 1 ? 2 : i == 2 ? 4 : i == 3 ? 8 : i == 4 ? 15 : i == 5 ? 16 : i == 6 ? 20
+         : i == 7 ? 25 : 30;
+}
+
+// engine.py:263-265: (q // 2) * lw2 + (q % 2) * lw1
+EXPMB_HD double lr_power_bound_log(int q, double lw1, double lw2) {
+  return rn_add(rn_mul((double)(q / 2), lw2), (q % 2) ? lw1 : 0.0);
+}
+
+// The ladder of engine.py:224-244 on ||V||_1 (and ||V^2||_1 once have_v2).
+// Returns 0 with the plan written, 1 when ||V^2||_1 is needed first, -1 when
+// no order qualifies (LowRankOrderError).
+EXPMB_HD int select_lowrank(double nv, double nv2, int have_v2, double log_eps, int* m, double* e1,
+                            double* e2) {
+  if (nv == 0.0) {
+    *m = 0;
+    *e1 = 0.0;
+    *e2 = 0.0;
+    return 0;
+  }
+  const double lw1 = log2_or_ninf(nv);
+  const double lw2 = have_v2 ? log2_or_ninf(nv2) : 0.0;
+  for (int i = 0; i < 9; ++i) {
+    const int mi = lr_order(i);
+    double l1, l2;
+    if (mi == 1) {
+      l1 = rn_sub(rn_mul(2.0, lw1), lr_log2_fact(3));
+      l2 = rn_sub(rn_mul(3.0, lw1), lr_log2_fact(4));
+    } else {
+      if (!have_v2) return 1;
+      l1 = rn_sub(lr_power_bound_log(mi + 1, lw1, lw2), lr_log2_fact(mi + 2));
+      l2 = rn_sub(lr_power_bound_log(mi + 2, lw1, lw2), lr_log2_fact(mi + 3));
+    }
+    // logaddexp2(l1, l2) lies in [max, max + 1]: only a rung whose bracket
+    // straddles log_eps needs the transcendental (the decision is unchanged)
+    const double mx = l1 > l2 ? l1 : l2;
+    bool pass;
+    if (mx > log_eps) pass = false;
+    else if (rn_add(mx, 1.0 + 0x1p-30) < log_eps) pass = true;
+    else pass = logaddexp2(l1, l2) <= log_eps;
+    if (pass) {
+      *m = mi;
+      *e1 = exp2(l1);
+      *e2 = exp2(l2);
+      return 0;
+    }
+  }
+  return -1;
+}
+
+// t x t products charged to the ledger: V^2 (selection), V^3..V^j, k-1 Horner stages.
+EXPMB_HD int lr_mults(int m) {
+  if (m < 2) return 0;
+  const int j = ps_j_of(m);
+  const int k = (m + j - 1) / j;
+  return 1 + (j - 2) + (k - 1);
+}
+
+struct LrOut {
+  int8_t* m;
+  double* e1;
+  double* e2;
+  double* norms;
+  int32_t* mults;
+  uint8_t* flags;
+};
+
+template <typename T, int TP>
+struct Lr {
+  static constexpr int NT = 256;
+  static constexpr int NC = 64;       // column / row / k chunk of the n-sized dimensions
+  static constexpr int LDP = TP + 1;  // t x t tiles and the A1 row tile
+  static constexpr int LDC = NC + 1;  // A2 / Y chunks
+  static constexpr int kSlot = TP * LDP;
+  // slot 0 = psi, 1..6 = V^p, 7 = scratch
+  static constexpr int kSA = 8 * kSlot;
+  static constexpr int kSB = kSA + TP * LDC;
+  static constexpr int kSY = kSB + NC * LDP;
+  static constexpr int kEnd = kSY + TP * LDC;
+  static constexpr size_t kSmem = ((kEnd * sizeof(T) + 15) / 16) * 16 + 16 * sizeof(double);
+};
+
+__device__ __forceinline__ double lr_nanmax(double a, double b) { return (a != a || a > b) ? a : b; }
+
+template <typename T>
+__device__ __forceinline__ bool lr_finite(T v) {
+  return isfinite(v);
+}
+
+// Norms + ladder on warp 0, plan broadcast through `scal` (one barrier).
+// V2 == nullptr: first call (||V||_1 only).  Returns select_lowrank's code,
+// or 2 when a norm is not finite (NonFiniteError in the reference).
+template <typename T, int TP>
+__device__ int lr_select_warp0(const T* V, const T* V2, double log_eps, double* scal, double* nv, double* nv2,
+                               int* m, double* e1, double* e2) {
+  using L = Lr<T, TP>;
+  if (threadIdx.x < 32) {
+    const T* S = V2 ? V2 : V;
+    double c = 0.0;
+    if (threadIdx.x < TP)
+      for (int r = 0; r < TP; ++r) c += fabs((double)S[r * L::LDP + threadIdx.x]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c = lr_nanmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+    const double a = V2 ? scal[1] : c;
+    const double b = V2 ? c : NAN;
+    int mm = 0, rc;
+    double x1 = NAN, x2 = NAN;
+    if (!isfinite(c)) rc = 2;
+    else rc = select_lowrank(a, V2 ? b : 0.0, V2 ? 1 : 0, log_eps, &mm, &x1, &x2);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      scal[1] = a;
+      scal[2] = b;
+      scal[3] = x1;
+      scal[4] = x2;
+      scal[5] = (double)mm;
+      scal[6] = (double)rc;
+    }
+  }
+  __syncthreads();
+  *nv = scal[1];
+  *nv2 = scal[2];
+  *e1 = scal[3];
+  *e2 = scal[4];
+  *m = (int)scal[5];
+  const int rc = (int)scal[6];
+  __syncthreads();
+  return rc;
+}
+
+// C = A B for TP x TP shared tiles.
+template <typename T, int TP>
+__device__ void lr_mm(T* C, const T* A, const T* B) {
+  using L = Lr<T, TP>;
+  for (int e = threadIdx.x; e < TP * TP; e += L::NT) {
+    const int r = e / TP, c = e % TP;
+    T acc = 0;
+#pragma unroll 8
+    for (int k = 0; k < TP; ++k) acc = fma(A[r * L::LDP + k], B[k * L::LDP + c], acc);
+    C[r * L::LDP + c] = acc;
+  }
+}
+
+template <typename T, int TP>
+__device__ void lr_fill_nan(T* x, size_t nn) {
+  for (size_t i = threadIdx.x; i < nn; i += Lr<T, TP>::NT) x[i] = (T)NAN;
+}
+
+template <typename T, int TP>
+__global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
+                                                           T* __restrict__ X, int64_t batch, int n, int t,
+                                                           double log_eps, LrOut po) {
+  using L = Lr<T, TP>;
+  extern __shared__ __align__(16) unsigned char lr_smem[];
+  T* P = reinterpret_cast<T*>(lr_smem);
+  T* SA = P + L::kSA;
+  T* SB = P + L::kSB;
+  T* SY = P + L::kSY;
+  double* scal = reinterpret_cast<double*>(lr_smem + L::kSmem - 16 * sizeof(double));
+  const int tid = threadIdx.x;
+  constexpr int NE = TP * TP;
+  constexpr int G = NE >= 256 ? 1 : 256 / NE;  // k-groups per V element
+  constexpr int R = NE >= 256 ? NE / 256 : 1;  // V elements per thread
+  const size_t nn = (size_t)n * n;
+
+  for (int64_t mat = blockIdx.x; mat < batch; mat += gridDim.x) {
+    const T* a1 = A1 + (size_t)mat * n * t;
+    const T* a2 = A2 + (size_t)mat * t * n;
+    T* x = X + (size_t)mat * nn;
+    T* V = P + L::kSlot;
+
+    // ---- phase 1: V = A2 A1 ----------------------------------------------
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0;
+    const int g = NE >= 256 ? 0 : tid / NE;
+    bool bad = false;
+    for (int k0 = 0; k0 < n; k0 += L::NC) {
+      const int kc = min(L::NC, n - k0);
+      for (int idx = tid; idx < TP * L::NC; idx += L::NT) {
+        const int a = idx / L::NC, kk = idx % L::NC;
+        T v = 0;
+        if (a < t && kk < kc) {
+          v = a2[(size_t)a * n + k0 + kk];
+          bad |= !lr_finite(v);
+        }
+        SA[a * L::LDC + kk] = v;
+      }
+      for (int idx = tid; idx < L::NC * TP; idx += L::NT) {
+        const int kk = idx / TP, b = idx % TP;
+        T v = 0;
+        if (b < t && kk < kc) {
+          v = a1[(size_t)(k0 + kk) * t + b];
+          bad |= !lr_finite(v);
+        }
+        SB[kk * L::LDP + b] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int e = NE >= 256 ? tid + 256 * r : tid % NE;
+        const int a = e / TP, b = e % TP;
+        T s = acc[r];
+        for (int kk = g; kk < L::NC; kk += G) s = fma(SA[a * L::LDC + kk], SB[kk * L::LDP + b], s);
+        acc[r] = s;
+      }
+      __syncthreads();
+    }
+    if (G > 1) {
+      SY[tid] = acc[0];
+      __syncthreads();
+      if (tid < NE) {
+        T s = 0;
+        for (int gg = 0; gg < G; ++gg) s += SY[gg * NE + tid];
+        V[(tid / TP) * L::LDP + tid % TP] = s;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int e = tid + 256 * r;
+        V[(e / TP) * L::LDP + e % TP] = acc[r];
+      }
+    }
+    const int bad_in = __syncthreads_or(bad);
+
+    int m = 0;
+    double e1 = NAN, e2 = NAN, nv = NAN, nv2 = NAN;
+    uint8_t flags = 0;
+    if (bad_in) {
+      flags = kLrBadInput;
+    } else {
+      // ---- phase 2: order selection and psi(V) ------------------------------
+      // warp 0 runs the ladder (warp-uniform) and broadcasts the plan
+      int rc = lr_select_warp0<T, TP>(V, nullptr, log_eps, scal, &nv, &nv2, &m, &e1, &e2);
+      if (rc == 1) {
+        lr_mm<T, TP>(P + 2 * L::kSlot, V, V);
+        __syncthreads();
+        rc = lr_select_warp0<T, TP>(V, P + 2 * L::kSlot, log_eps, scal, &nv, &nv2, &m, &e1, &e2);
+      }
+      if (rc == 2) {
+        flags = kLrNonFinite;
+      } else if (rc < 0) {
+        flags = kLrNoOrder;
+        e1 = e2 = NAN;
+      }
+    }
+    if (flags) {
+      lr_fill_nan<T, TP>(x, nn);
+    } else {
+      T* Q = P;
+      T* S7 = P + 7 * L::kSlot;
+      if (m == 0) {
+        for (int e = tid; e < NE; e += L::NT) Q[(e / TP) * L::LDP + e % TP] = (e / TP == e % TP) ? T(1) : T(0);
+      } else {
+        const int j = ps_j_of(m);
+        const int k = (m + j - 1) / j;
+        for (int p = 3; p <= j; ++p) {
+          lr_mm<T, TP>(P + p * L::kSlot, P + (p - 1) * L::kSlot, V);
+          __syncthreads();
+        }
+        // q = block((k-1)j, m); then q = q V^j + block(rj, rj+j-1), r = k-2..0
+        // (poly.py:171-182; block(lo,hi) = c_lo I + sum_t c_{lo+t} V^t)
+        for (int r = k - 1; r >= 0; --r) {
+          const int lo = r * j, hi = (r == k - 1) ? m : r * j + j - 1;
+          if (r < k - 1) {
+            lr_mm<T, TP>(S7, Q, P + j * L::kSlot);
+            __syncthreads();
+          }
+          for (int e = tid; e < NE; e += L::NT) {
+            const int off = (e / TP) * L::LDP + e % TP;
+            T q = (e / TP == e % TP) ? (T)lr_inv_fact(lo + 1) : T(0);
+            for (int tt = 1; tt <= hi - lo; ++tt)
+              q = fma((T)lr_inv_fact(lo + tt + 1), P[tt * L::kSlot + off], q);
+            Q[off] = (r < k - 1) ? S7[off] + q : q;
+          }
+          __syncthreads();
+        }
+      }
+      __syncthreads();
+      bool bq = false;
+      for (int e = tid; e < NE; e += L::NT) bq |= !lr_finite(Q[(e / TP) * L::LDP + e % TP]);
+      if (__syncthreads_or(bq)) {
+        flags = kLrNonFinite;
+        lr_fill_nan<T, TP>(x, nn);
+      } else {
+        // ---- phase 3: out = I + A1 (psi A2) ---------------------------------
+        const int tx = tid % 16, ty = tid / 16;
+        bool bo = false;
+        for (int c0 = 0; c0 < n; c0 += L::NC) {
+          const int cc = min(L::NC, n - c0);
+          for (int idx = tid; idx < TP * L::NC; idx += L::NT) {
+            const int a = idx / L::NC, jj = idx % L::NC;
+            SA[a * L::LDC + jj] = (a < t && jj < cc) ? a2[(size_t)a * n + c0 + jj] : T(0);
+          }
+          __syncthreads();
+          for (int e = tid; e < TP * L::NC; e += L::NT) {
+            const int b = e / L::NC, jj = e % L::NC;
+            T s = 0;
+#pragma unroll 8
+            for (int a = 0; a < TP; ++a) s = fma(Q[b * L::LDP + a], SA[a * L::LDC + jj], s);
+            SY[b * L::LDC + jj] = s;
+          }
+          __syncthreads();
+          for (int r0 = 0; r0 < n; r0 += L::NC) {
+            const int rcn = min(L::NC, n - r0);
+            for (int idx = tid; idx < L::NC * TP; idx += L::NT) {
+              const int rr = idx / TP, b = idx % TP;
+              SB[rr * L::LDP + b] = (rr < rcn && b < t) ? a1[(size_t)(r0 + rr) * t + b] : T(0);
+            }
+            __syncthreads();
+            T o[4][4];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) o[ii][jj] = 0;
+#pragma unroll 4
+            for (int b = 0; b < TP; ++b) {
+              T ya[4], xa[4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) ya[jj] = SY[b * L::LDC + tx + 16 * jj];
+#pragma unroll
+              for (int ii = 0; ii < 4; ++ii) xa[ii] = SB[(ty + 16 * ii) * L::LDP + b];
+#pragma unroll
+              for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) o[ii][jj] = fma(xa[ii], ya[jj], o[ii][jj]);
+            }
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+              const int row = r0 + ty + 16 * ii;
+              if (row >= n) continue;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int col = c0 + tx + 16 * jj;
+                if (col < n) {
+                  const T v = (row == col) ? o[ii][jj] + T(1) : o[ii][jj];
+                  bo |= !lr_finite(v);
+                  x[(size_t)row * n + col] = v;
+                }
+              }
+            }
+            __syncthreads();
+          }
+        }
+        if (__syncthreads_or(bo)) flags = kLrNonFinite;
+      }
+    }
+    if (tid == 0) {
+      if (po.m) po.m[mat] = (int8_t)m;
+      if (po.e1) po.e1[mat] = e1;
+      if (po.e2) po.e2[mat] = e2;
+      if (po.norms) {
+        po.norms[2 * mat] = nv;
+        po.norms[2 * mat + 1] = nv2;
+      }
+      if (po.mults) po.mults[mat] = flags ? 0 : lr_mults(m);
+      if (po.flags) po.flags[mat] = flags;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-per-matrix variant for the flow-layer shape t <= 8, n <= 64 (the
+// reference generator's t = n/8 at n = 64).  No block barriers: each warp
+// owns one matrix at a time in its private shared-memory slice (A1 rows,
+// A2 rows, eight 8x8 tiles), zero-padded once per launch (padding is never
+// written, so V's powers, norms and the assembly see exact zeros).
+//   V = A2 A1      lane (a, b0..b0+1), k over n
+//   psi(V)         t x t products, lane owns the same two entries
+//   Y = psi A2     lane owns columns c0 = 2 lane, c0 + 1, kept in registers
+//   out = I + A1 Y one row per iteration: four broadcast 16-byte loads of the
+//                  A1 row, 16 FMAs, one coalesced 16-byte store per lane (the
+//                  warp writes the whole 512-byte row)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct LrW {
+  static constexpr int WARPS = 4;
+  static constexpr int NT = 32 * WARPS;
+  static constexpr int LD1 = 8;   // A1 rows: 8 entries, 16-byte aligned pairs
+  static constexpr int LD2 = 66;  // A2 rows: conflict-free column walks, 16-byte aligned
+  static constexpr int LDP = 9;   // 8x8 tiles
+  static constexpr int kSlot = 8 * LDP;
+  static constexpr int kA2 = 64 * LD1;
+  static constexpr int kP = kA2 + 8 * LD2;
+  static constexpr int kStride = ((kP + 8 * kSlot) + 3) / 4 * 4;
+  static constexpr size_t kSmem = (size_t)WARPS * kStride * sizeof(T);
+};
+
+template <typename T>
+struct Pair2 {
+  T x, y;
+};
+template <typename T>
+__device__ __forceinline__ Pair2<T> ld_pair(const T* p) {
+  if constexpr (sizeof(T) == 8) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    return {v.x, v.y};
+  } else {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    return {v.x, v.y};
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st_pair(T* p, T a, T b) {
+  if constexpr (sizeof(T) == 8) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+  } else {
+    *reinterpret_cast<float2*>(p) = make_float2(a, b);
+  }
+}
+
+// ||tile||_1 over the warp (lanes 0..7 sum a column; NaN-propagating max).
+template <typename T>
+__device__ __forceinline__ double lrw_norm1(const T* S, int lane) {
+  double c = 0.0;
+  if (lane < 8)
+    for (int r = 0; r < 8; ++r) c += fabs((double)S[r * LrW<T>::LDP + lane]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = lr_nanmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+  return c;
+}
+
+// This lane's two entries (a, b0), (a, b0 + 1) of A B for 8x8 tiles.
+template <typename T>
+__device__ __forceinline__ void lrw_mm2(const T* A, const T* B, int a, int b0, T& o0, T& o1) {
+  constexpr int LDP = LrW<T>::LDP;
+  T s0 = 0, s1 = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const T av = A[a * LDP + k];
+    s0 = fma(av, B[k * LDP + b0], s0);
+    s1 = fma(av, B[k * LDP + b0 + 1], s1);
+  }
+  o0 = s0;
+  o1 = s1;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restrict__ A1,
+                                                                const T* __restrict__ A2, T* __restrict__ X,
+                                                                int64_t batch, int n, int t, double log_eps,
+                                                                LrOut po) {
+  using L = LrW<T>;
+  extern __shared__ __align__(16) unsigned char lrw_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T* base = reinterpret_cast<T*>(lrw_smem) + w * L::kStride;
+  T* sA1 = base;
+  T* sA2 = base + L::kA2;
+  T* P = base + L::kP;  // slot 0 = psi, 1..6 = V^p, 7 = scratch
+  for (int i = lane; i < L::kStride; i += 32) base[i] = T(0);
+  __syncwarp();
+  const int a_r = lane >> 2, b0 = (lane & 3) * 2;  // the t x t entries this lane owns
+  const int c0 = 2 * lane;                         // the output columns this lane owns
+  const bool vec_out = (n % 2) == 0;
+  const int64_t nw = (int64_t)gridDim.x * L::WARPS;
+  for (int64_t mat = (int64_t)blockIdx.x * L::WARPS + w; mat < batch; mat += nw) {
+    const T* a1 = A1 + (size_t)mat * n * t;
+    const T* a2 = A2 + (size_t)mat * t * n;
+    T* x = X + (size_t)mat * n * n;
+    bool bad = false;
+    {
+      const int b = lane & 7;
+      for (int r = lane >> 3; r < n; r += 4)
+        if (b < t) {
+          const T v = a1[(size_t)r * t + b];
+          bad |= !isfinite(v);
+          sA1[r * L::LD1 + b] = v;
+        }
+      for (int a = 0; a < t; ++a)
+        for (int c = lane; c < n; c += 32) {
+          const T v = a2[(size_t)a * n + c];
+          bad |= !isfinite(v);
+          sA2[a * L::LD2 + c] = v;
+        }
+    }
+    __syncwarp();
+    int m = 0, rc = 0;
+    bool wrote = false;
+    double e1 = NAN, e2 = NAN, nv = NAN, nv2 = NAN;
+    uint8_t flags = __any_sync(0xffffffffu, bad) ? kLrBadInput : 0;
+    if (!flags) {
+      // V = A2 A1
+      T v0 = 0, v1 = 0;
+      for (int k = 0; k < n; ++k) {
+        const T s = sA2[a_r * L::LD2 + k];
+        const Pair2<T> q = ld_pair(sA1 + k * L::LD1 + b0);
+        v0 = fma(s, q.x, v0);
+        v1 = fma(s, q.y, v1);
+      }
+      T* V = P + L::kSlot;
+      V[a_r * L::LDP + b0] = v0;
+      V[a_r * L::LDP + b0 + 1] = v1;
+      __syncwarp();
+      nv = lrw_norm1(V, lane);
+      if (!isfinite(nv)) {
+        rc = 2;
+      } else {
+        rc = select_lowrank(nv, 0.0, 0, log_eps, &m, &e1, &e2);
+        if (rc == 1) {
+          T o0, o1;
+          lrw_mm2(V, V, a_r, b0, o0, o1);
+          P[2 * L::kSlot + a_r * L::LDP + b0] = o0;
+          P[2 * L::kSlot + a_r * L::LDP + b0 + 1] = o1;
+          __syncwarp();
+          nv2 = lrw_norm1(P + 2 * L::kSlot, lane);
+          rc = isfinite(nv2) ? select_lowrank(nv, nv2, 1, log_eps, &m, &e1, &e2) : 2;
+        }
+      }
+      if (rc == 2) flags = kLrNonFinite;
+      if (rc < 0) {
+        flags = kLrNoOrder;
+        e1 = e2 = NAN;
+      }
+    }
+    if (!flags) {
+      // psi(V) by Paterson-Stockmeyer (poly.py:149-182), this lane's two entries
+      T* Q = P;
+      const int off = a_r * L::LDP + b0;
+      T q0, q1;
+      if (m == 0) {
+        q0 = (a_r == b0) ? T(1) : T(0);
+        q1 = (a_r == b0 + 1) ? T(1) : T(0);
+      } else {
+        const int j = ps_j_of(m);
+        const int k = (m + j - 1) / j;
+        for (int p = 3; p <= j; ++p) {
+          T o0, o1;
+          lrw_mm2(P + (p - 1) * L::kSlot, P + L::kSlot, a_r, b0, o0, o1);
+          P[p * L::kSlot + off] = o0;
+          P[p * L::kSlot + off + 1] = o1;
+          __syncwarp();
+        }
+        q0 = q1 = 0;
+        for (int r = k - 1; r >= 0; --r) {
+          const int lo = r * j, hi = (r == k - 1) ? m : r * j + j - 1;
+          T s0 = 0, s1 = 0;
+          if (r < k - 1) lrw_mm2(Q, P + j * L::kSlot, a_r, b0, s0, s1);
+          T c0v = (a_r == b0) ? (T)lr_inv_fact(lo + 1) : T(0);
+          T c1v = (a_r == b0 + 1) ? (T)lr_inv_fact(lo + 1) : T(0);
+          for (int tt = 1; tt <= hi - lo; ++tt) {
+            const T c = (T)lr_inv_fact(lo + tt + 1);
+            c0v = fma(c, P[tt * L::kSlot + off], c0v);
+            c1v = fma(c, P[tt * L::kSlot + off + 1], c1v);
+          }
+          q0 = (r < k - 1) ? s0 + c0v : c0v;
+          q1 = (r < k - 1) ? s1 + c1v : c1v;
+          __syncwarp();
+          Q[off] = q0;
+          Q[off + 1] = q1;
+          __syncwarp();
+        }
+      }
+      Q[off] = q0;
+      Q[off + 1] = q1;
+      __syncwarp();
+      if (__any_sync(0xffffffffu, !isfinite(q0) || !isfinite(q1))) {
+        flags = kLrNonFinite;
+      } else {
+        // Y = psi A2, columns c0, c0 + 1 in registers
+        T y0[8], y1[8];
+        Pair2<T> ac[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) ac[a] = ld_pair(sA2 + a * L::LD2 + c0);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          T s0 = 0, s1 = 0;
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            const T qv = Q[b * L::LDP + a];
+            s0 = fma(qv, ac[a].x, s0);
+            s1 = fma(qv, ac[a].y, s1);
+          }
+          y0[b] = s0;
+          y1[b] = s1;
+        }
+        // out = I + A1 Y, one row per iteration
+        bool bo = false;
+        const bool act0 = c0 < n, act1 = c0 + 1 < n;
+#pragma unroll 2
+        for (int r = 0; r < n; ++r) {
+          const T* ar = sA1 + r * L::LD1;
+          T o0 = 0, o1 = 0;
+#pragma unroll
+          for (int b = 0; b < 8; b += 2) {
+            const Pair2<T> xa = ld_pair(ar + b);
+            o0 = fma(xa.x, y0[b], o0);
+            o1 = fma(xa.x, y1[b], o1);
+            o0 = fma(xa.y, y0[b + 1], o0);
+            o1 = fma(xa.y, y1[b + 1], o1);
+          }
+          if (r == c0) o0 += T(1);
+          if (r == c0 + 1) o1 += T(1);
+          T* xr = x + (size_t)r * n + c0;
+          if (vec_out && act1) {
+            st_pair(xr, o0, o1);
+            bo |= !isfinite(o0) || !isfinite(o1);
+          } else {
+            if (act0) {
+              xr[0] = o0;
+              bo |= !isfinite(o0);
+            }
+            if (act1) {
+              xr[1] = o1;
+              bo |= !isfinite(o1);
+            }
+          }
+        }
+        wrote = true;
+        if (__any_sync(0xffffffffu, bo)) flags = kLrNonFinite;
+      }
+    }
+    if (flags && !wrote)
+      for (size_t i = lane; i < (size_t)n * n; i += 32) x[i] = (T)NAN;
+    if (lane == 0) {
+      if (po.m) po.m[mat] = (int8_t)m;
+      if (po.e1) po.e1[mat] = e1;
+      if (po.e2) po.e2[mat] = e2;
+      if (po.norms) {
+        po.norms[2 * mat] = nv;
+        po.norms[2 * mat + 1] = nv2;
+      }
+      if (po.mults) po.mults[mat] = flags ? 0 : lr_mults(m);
+      if (po.flags) po.flags[mat] = flags;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace expmb

@@ -81,6 +81,14 @@ class ToleranceError(ValueError):
     """select.py:64."""
 
 
+class LowRankOrderError(ArithmeticError):
+    """engine.py:60 -- no order on LOWRANK_ORDERS meets the tolerance."""
+
+
+LOWRANK_ORDERS = (1, 2, 4, 8, 15, 16, 20, 25, 30)   # engine.py:195
+SCHEME_LOWRANK = "lowrank"                         # select.py:61
+
+
 @dataclass(frozen=True)
 class PsShape:
     """poly.py:125-134."""

@@ -126,3 +126,39 @@ def useful_flops(m, s, n: int, scheme: str = "sastre") -> float:
         lut = {0: 0, 1: 0, 2: 1, 4: 2, 8: 3, 15: 4}
         b = np.array([lut[int(mm)] for mm in m])
     return float(((b + s) * 2.0 * n ** 3).sum())
+
+
+# ---------------------------------------------------------------------------
+# Low-rank flow-layer workload (not a BASELINE.json config)
+# ---------------------------------------------------------------------------
+
+LOWRANK = Config("LR", 16384, 64, "f64", 2.0 ** -53, 1024,
+                 "batch 16384 low-rank flow weights W = A1 A2, n 64, t 8 (the reference generator's n/8, "
+                 "bench.py:134-142), factors U[-1,1], ||A2 A1||_1 log-U[1e-2,3], fp64, tol 2^-53")
+LOWRANK_T = 8
+
+
+def _lowrank_chunk(c: int):
+    cfg, n, t = LOWRANK, LOWRANK.n, LOWRANK_T
+    rng = np.random.default_rng([9, c])
+    a1 = rng.uniform(-1.0, 1.0, (cfg.chunk, n, t))
+    a2 = rng.uniform(-1.0, 1.0, (cfg.chunk, t, n))
+    target = _logu(rng, 1e-2, 3.0, cfg.chunk)
+    a2 *= (target / _colnorm(a2 @ a1))[:, None, None]
+    return a1, a2
+
+
+def generate_lowrank(indices) -> tuple[np.ndarray, np.ndarray]:
+    """(A1 [B,n,t], A2 [B,t,n]) fp64 for the given global indices of LR."""
+    indices = np.asarray(indices)
+    n, t = LOWRANK.n, LOWRANK_T
+    A1 = np.empty((len(indices), n, t))
+    A2 = np.empty((len(indices), t, n))
+    cache = {}
+    for k, i in enumerate(indices):
+        c, r = divmod(int(i), LOWRANK.chunk)
+        if c not in cache:
+            cache.clear()
+            cache[c] = _lowrank_chunk(c)
+        A1[k], A2[k] = cache[c][0][r], cache[c][1][r]
+    return A1, A2

@@ -29,6 +29,7 @@ import expmkit  # noqa: E402
 from expmkit import GeneratorSpec, Matrix, NonFiniteError, gen_matrix  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "expm_golden.npz")
+OUT_LR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lowrank_golden.npz")
 
 
 def cases():
@@ -108,5 +109,75 @@ def main():
     print(f"wrote {len(names)} cases, {offs[-1]} entries -> {OUT}")
 
 
+def lowrank_cases():
+    """expm_lowrank (engine.py:198-257) inputs: the reference tests' factors
+    (test_engine.py:241-318, test_acceptance.py:257-270), a nilpotent pair
+    with V = 0, and seeded random factors over orders, ranks and norms."""
+    from expmkit import LowRankPair  # noqa: F401
+    n = 6
+    a1 = np.zeros((n, 1)); a1[0, 0] = 1.0
+    a2 = np.zeros((1, n)); a2[0, 0] = 1.0
+    yield "projector", a1, a2, 1e-8
+    yield "zero_factor", np.zeros((5, 2)), np.ones((2, 5)), 1e-8
+    rng = np.random.default_rng(53)
+    a1 = rng.uniform(-1, 1, (64, 8)); a2 = rng.uniform(-1, 1, (8, 64))
+    a2 *= 2.0 / np.abs(a2 @ a1).sum(axis=0).max()
+    yield "matches_reference", a1, a2, 1e-8
+    rng = np.random.default_rng(59)
+    a1 = rng.uniform(-1, 1, (16, 2)); a2 = rng.uniform(-1, 1, (2, 16))
+    a2 *= 1.0 / np.abs(a2 @ a1).sum(axis=0).max()
+    yield "order_minimal", a1, a2, 1e-8
+    yield "norm_too_large", np.eye(4, 2) * 10.0, np.eye(2, 4) * 10.0, 1e-8
+    yield "psi_1x1", np.array([[1.5]]), np.array([[1.0]]), 1e-8
+    yield "nilpotent_v0", np.array([[1.0], [0.0]]), np.array([[0.0, 1.0]]), 1e-8
+    for i, target in enumerate((0.5, 1.0, 2.0, 3.5, 5.0)):
+        pair = gen_matrix(GeneratorSpec(kind="lowrank_pair", n=64, target_norm=target, seed=500 + i))
+        yield f"criterion9_{i}", pair.a1.copy(), pair.a2.copy(), 1e-8
+    rng = np.random.default_rng(20251221)
+    sizes = (1, 2, 3, 5, 8, 13, 16, 17, 31, 33, 64, 65, 100, 128)
+    epss = (1e-12, 1e-8, 1e-4, 2.0 ** -24, 2.0 ** -53)
+    for i in range(90):
+        n = sizes[i % len(sizes)]
+        t = int(rng.integers(1, min(n, 32) + 1))
+        target = float(10.0 ** rng.uniform(-4, 1.5))
+        a1 = rng.uniform(-1, 1, (n, t)); a2 = rng.uniform(-1, 1, (t, n))
+        vn = np.abs(a2 @ a1).sum(axis=0).max()
+        if vn > 0:
+            a2 *= target / vn
+        yield f"lr_rand{i}", a1, a2, epss[i % len(epss)]
+
+
+def main_lowrank():
+    names, ns, ts, epss, ms, e1s, e2s, mults, rects, raised = [], [], [], [], [], [], [], [], [], []
+    a1s, a2s, outs, nv1, nv2 = [], [], [], [], []
+    for name, a1, a2, eps in lowrank_cases():
+        names.append(name); ns.append(a1.shape[0]); ts.append(a1.shape[1]); epss.append(eps)
+        a1s.append(np.asarray(a1, np.float64).ravel()); a2s.append(np.asarray(a2, np.float64).ravel())
+        try:
+            r = expmkit.expm_lowrank(expmkit.LowRankPair(a1, a2), eps)
+        except expmkit.LowRankOrderError:
+            raised.append(True)
+            ms.append(-1); e1s.append(math.nan); e2s.append(math.nan); mults.append(-1); rects.append(-1)
+            nv1.append(math.nan); nv2.append(math.nan)
+            outs.append(np.full(a1.shape[0] ** 2, np.nan))
+            continue
+        raised.append(False)
+        ms.append(r.plan.m); e1s.append(r.plan.e1); e2s.append(r.plan.e2)
+        mults.append(r.mults); rects.append(r.rect_mults)
+        nv1.append(r.plan.cached_norms.get(1, math.nan)); nv2.append(r.plan.cached_norms.get(2, math.nan))
+        outs.append(r.value.a.ravel().copy())
+    offs = np.concatenate([[0], np.cumsum([a.size for a in a1s])])
+    oo = np.concatenate([[0], np.cumsum([a.size for a in outs])])
+    np.savez_compressed(
+        OUT_LR, names=np.array(names), n=np.array(ns), t=np.array(ts), eps=np.array(epss),
+        m=np.array(ms), e1=np.array(e1s), e2=np.array(e2s), mults=np.array(mults),
+        rect_mults=np.array(rects), raised=np.array(raised), norm1=np.array(nv1), norm2=np.array(nv2),
+        offsets=offs, out_offsets=oo, A1=np.concatenate(a1s), A2=np.concatenate(a2s),
+        X=np.concatenate(outs),
+    )
+    print(f"wrote {len(names)} low-rank cases -> {OUT_LR}")
+
+
 if __name__ == "__main__":
     main()
+    main_lowrank()

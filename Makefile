@@ -19,10 +19,15 @@ tools/peaks: tools/peaks.cu
 $(PKG)/libexpmb.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
 
+# A/B builds: make variant VNAME=b VFLAGS=-DSOMETHING=1 -> libexpmb_b.so
+# (select at run time with EXPMB_LIB=libexpmb_b.so)
+variant: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o $(PKG)/libexpmb_$(VNAME).so $(SRC)
+
 ptxas: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/expmb_api.o $(SRC) 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" | paste - - - | sed 's/ptxas info    ://g'
 
 clean:
 	rm -f $(PKG)/libexpmb.so
 
-.PHONY: all clean ptxas tools
+.PHONY: all clean ptxas tools variant

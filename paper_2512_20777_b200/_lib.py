@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libexpmb.so")
+# EXPMB_LIB selects an A/B build of the same library (`make variant`), by file name
+LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ.get("EXPMB_LIB", "libexpmb.so")))
 
 EXPMB_F32, EXPMB_F64 = 0, 1
 EXPMB_SASTRE, EXPMB_PS, EXPMB_BASELINE = 0, 1, 2

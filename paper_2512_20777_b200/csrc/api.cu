@@ -148,11 +148,11 @@ static int launch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n, 
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
-template <typename T>
+template <typename T, bool FULL>
 static int launch_lowrank_warp(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
                                cudaStream_t st) {
   using L = LrW<T>;
-  auto kern = expm_lowrank_warp_kernel<T>;
+  auto kern = expm_lowrank_warp_kernel<T, FULL>;
   static int occ = -1;
   if (occ < 0) {
     if (L::kSmem > 48 * 1024 &&
@@ -170,11 +170,42 @@ static int launch_lowrank_warp(const T* A1, const T* A2, T* X, int64_t batch, in
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
+static int launch_lowrank_dmma(const double* A1, const double* A2, double* X, int64_t batch, double eps, LrOut po,
+                               cudaStream_t st) {
+  using L = LrD;
+  auto kern = expm_lowrank_dmma_kernel;
+  static int occ = -1;
+  if (occ < 0) {
+    if (L::kSmem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kSmem) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, L::NT, L::kSmem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t ctas = (batch + L::WARPS - 1) / L::WARPS;
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(ctas < persistent ? ctas : persistent);
+  kern<<<grid, L::NT, L::kSmem, st>>>(A1, A2, X, batch, log2(eps), po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
 template <typename T>
 static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
                             cudaStream_t st) {
-  static const bool cta_only = getenv("EXPMB_LR_CTA") != nullptr;  // A/B switch
-  if (t <= 8 && n <= 64 && !cta_only) return launch_lowrank_warp<T>(A1, A2, X, batch, n, t, eps, po, st);
+  static const bool cta_only = getenv("EXPMB_LR_CTA") != nullptr;   // A/B switches
+  static const bool no_dmma = getenv("EXPMB_LR_NO_DMMA") != nullptr;
+  // the warp kernels use 16-byte vector accesses of the factors / result
+  const bool a16 = (((uintptr_t)A1 | (uintptr_t)A2 | (uintptr_t)X) % 16) == 0;
+  if (!cta_only && a16 && t <= 8 && n <= 64) {
+    if (t == 8 && n == 64) {
+      if constexpr (sizeof(T) == 8)
+        if (!no_dmma) return launch_lowrank_dmma((const double*)A1, (const double*)A2, (double*)X, batch, eps, po, st);
+      return launch_lowrank_warp<T, true>(A1, A2, X, batch, n, t, eps, po, st);
+    }
+    return launch_lowrank_warp<T, false>(A1, A2, X, batch, n, t, eps, po, st);
+  }
   if (t <= 8) return launch_lowrank<T, 8>(A1, A2, X, batch, n, t, eps, po, st);
   if (t <= 16) return launch_lowrank<T, 16>(A1, A2, X, batch, n, t, eps, po, st);
   return launch_lowrank<T, 32>(A1, A2, X, batch, n, t, eps, po, st);

@@ -49,8 +49,13 @@ EXPMB_HD double lr_power_bound_log(int q, double lw1, double lw2) {
 // The ladder of engine.py:224-244 on ||V||_1 (and ||V^2||_1 once have_v2).
 // Returns 0 with the plan written, 1 when ||V^2||_1 is needed first, -1 when
 // no order qualifies (LowRankOrderError).
-EXPMB_HD int select_lowrank(double nv, double nv2, int have_v2, double log_eps, int* m, double* e1,
-                            double* e2) {
+// (out of line on the device: one copy of the double-precision ladder)
+#if defined(__CUDACC__)
+__host__ __device__ __noinline__
+#else
+inline
+#endif
+int select_lowrank(double nv, double nv2, int have_v2, double log_eps, int* m, double* e1, double* e2) {
   if (nv == 0.0) {
     *m = 0;
     *e1 = 0.0;
@@ -413,6 +418,10 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
 //                  warp writes the whole 512-byte row)
 // ---------------------------------------------------------------------------
 
+#ifndef LRW_PAIRS
+#define LRW_PAIRS 1  // FULL assembly: row pairs with the diagonal folded into the init
+#endif
+
 template <typename T>
 struct LrW {
   static constexpr int WARPS = 4;
@@ -476,11 +485,14 @@ __device__ __forceinline__ void lrw_mm2(const T* A, const T* B, int a, int b0, T
   o1 = s1;
 }
 
-template <typename T>
+// FULL: n == 64 and t == 8 exactly (vector loads/stores, no bounds checks).
+template <typename T, bool FULL>
 __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restrict__ A1,
                                                                 const T* __restrict__ A2, T* __restrict__ X,
-                                                                int64_t batch, int n, int t, double log_eps,
+                                                                int64_t batch, int n_, int t_, double log_eps,
                                                                 LrOut po) {
+  const int n = FULL ? 64 : n_;
+  const int t = FULL ? 8 : t_;
   using L = LrW<T>;
   extern __shared__ __align__(16) unsigned char lrw_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -498,22 +510,51 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
     const T* a1 = A1 + (size_t)mat * n * t;
     const T* a2 = A2 + (size_t)mat * t * n;
     T* x = X + (size_t)mat * n * n;
-    bool bad = false;
-    {
+    // all loads of the factors issued back to back, then staged; z turns
+    // NaN if any entry is NaN/Inf (x * 0 = NaN exactly for those)
+    T z = 0;
+    double amax1 = 0.0;  // FULL: max |A1| (overflow bound of the assembly)
+    if constexpr (FULL) {
+      Pair2<T> ra[8], rb[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ra[q] = ld_pair(a1 + 2 * (lane + 32 * q));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rb[q] = ld_pair(a2 + q * 64 + 2 * lane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int p = lane + 32 * q;
+        st_pair(sA1 + (p >> 2) * L::LD1 + 2 * (p & 3), ra[q].x, ra[q].y);
+        st_pair(sA2 + q * L::LD2 + 2 * lane, rb[q].x, rb[q].y);
+        z = fma(ra[q].x, T(0), z);
+        z = fma(ra[q].y, T(0), z);
+        z = fma(rb[q].x, T(0), z);
+        z = fma(rb[q].y, T(0), z);
+        amax1 = fmax(amax1, fmax(fabs((double)ra[q].x), fabs((double)ra[q].y)));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax1 = fmax(amax1, __shfl_xor_sync(0xffffffffu, amax1, o));
+    } else {
+      T ra[16], rb[16];
       const int b = lane & 7;
-      for (int r = lane >> 3; r < n; r += 4)
-        if (b < t) {
-          const T v = a1[(size_t)r * t + b];
-          bad |= !isfinite(v);
-          sA1[r * L::LD1 + b] = v;
-        }
-      for (int a = 0; a < t; ++a)
-        for (int c = lane; c < n; c += 32) {
-          const T v = a2[(size_t)a * n + c];
-          bad |= !isfinite(v);
-          sA2[a * L::LD2 + c] = v;
-        }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int r = (lane >> 3) + 4 * q;
+        ra[q] = (b < t && r < n) ? a1[(size_t)r * t + b] : T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int a = q >> 1, c = lane + 32 * (q & 1);
+        rb[q] = (a < t && c < n) ? a2[(size_t)a * n + c] : T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        sA1[((lane >> 3) + 4 * q) * L::LD1 + b] = ra[q];
+        sA2[(q >> 1) * L::LD2 + lane + 32 * (q & 1)] = rb[q];
+        z = fma(ra[q], T(0), z);
+        z = fma(rb[q], T(0), z);
+      }
     }
+    const bool bad = z != T(0);
     __syncwarp();
     int m = 0, rc = 0;
     bool wrote = false;
@@ -522,6 +563,7 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
     if (!flags) {
       // V = A2 A1
       T v0 = 0, v1 = 0;
+#pragma unroll 4
       for (int k = 0; k < n; ++k) {
         const T s = sA2[a_r * L::LD2 + k];
         const Pair2<T> q = ld_pair(sA1 + k * L::LD1 + b0);
@@ -614,11 +656,72 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
           y0[b] = s0;
           y1[b] = s1;
         }
-        // out = I + A1 Y, one row per iteration
+        // out = I + A1 Y
         bool bo = false;
+        T zo = 0;  // NaN iff a checked output entry is NaN/Inf
+        if constexpr (FULL && LRW_PAIRS) {
+          // |out| <= 1 + max|A1| * max_c sum_b |Y[b][c]|: when that is far from
+          // overflow (the usual case) no entry can be NaN/Inf and the
+          // per-entry check is skipped; otherwise every entry is checked
+          double ys0 = 0.0, ys1 = 0.0;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            ys0 += fabs((double)y0[b]);
+            ys1 += fabs((double)y1[b]);
+          }
+          const double bound = 1.0 + amax1 * (ys0 > ys1 ? ys0 : ys1);
+          const bool safe = __all_sync(0xffffffffu, bound < (sizeof(T) == 8 ? 1e300 : 1e37));
+          T* xr = x + c0;
+          // row pairs (2p, 2p + 1): lane's diagonal entries are (2p, c0) and
+          // (2p + 1, c0 + 1) for p == lane, folded into the accumulator init
+          // the next pair's A1 rows are loaded while this pair's FMAs run
+          Pair2<T> xa[4], xb[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            xa[b] = ld_pair(sA1 + 2 * b);
+            xb[b] = ld_pair(sA1 + L::LD1 + 2 * b);
+          }
+#pragma unroll 1
+          for (int p = 0; p < 32; ++p) {
+            const T d = (p == lane) ? T(1) : T(0);
+            const T* an = sA1 + 2 * ((p + 1) & 31) * L::LD1;
+            Pair2<T> na[4], nb[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              na[b] = ld_pair(an + 2 * b);
+              nb[b] = ld_pair(an + L::LD1 + 2 * b);
+            }
+            T o00 = d, o01 = 0, o10 = 0, o11 = d;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              o00 = fma(xa[b].x, y0[2 * b], o00);
+              o01 = fma(xa[b].x, y1[2 * b], o01);
+              o10 = fma(xb[b].x, y0[2 * b], o10);
+              o11 = fma(xb[b].x, y1[2 * b], o11);
+              o00 = fma(xa[b].y, y0[2 * b + 1], o00);
+              o01 = fma(xa[b].y, y1[2 * b + 1], o01);
+              o10 = fma(xb[b].y, y0[2 * b + 1], o10);
+              o11 = fma(xb[b].y, y1[2 * b + 1], o11);
+            }
+            st_pair(xr, o00, o01);
+            st_pair(xr + 64, o10, o11);
+            xr += 128;
+            if (!safe) {
+              zo = fma(o00, T(0), zo);
+              zo = fma(o01, T(0), zo);
+              zo = fma(o10, T(0), zo);
+              zo = fma(o11, T(0), zo);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              xa[b] = na[b];
+              xb[b] = nb[b];
+            }
+          }
+        }
         const bool act0 = c0 < n, act1 = c0 + 1 < n;
 #pragma unroll 2
-        for (int r = 0; r < n; ++r) {
+        for (int r = 0; r < ((FULL && LRW_PAIRS) ? 0 : n); ++r) {
           const T* ar = sA1 + r * L::LD1;
           T o0 = 0, o1 = 0;
 #pragma unroll
@@ -632,7 +735,11 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
           if (r == c0) o0 += T(1);
           if (r == c0 + 1) o1 += T(1);
           T* xr = x + (size_t)r * n + c0;
-          if (vec_out && act1) {
+          if (FULL) {
+            st_pair(xr, o0, o1);
+            zo = fma(o0, T(0), zo);
+            zo = fma(o1, T(0), zo);
+          } else if (vec_out && act1) {
             st_pair(xr, o0, o1);
             bo |= !isfinite(o0) || !isfinite(o1);
           } else {
@@ -647,11 +754,250 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
           }
         }
         wrote = true;
+        bo |= zo != T(0);
         if (__any_sync(0xffffffffu, bo)) flags = kLrNonFinite;
       }
     }
     if (flags && !wrote)
       for (size_t i = lane; i < (size_t)n * n; i += 32) x[i] = (T)NAN;
+    if (lane == 0) {
+      if (po.m) po.m[mat] = (int8_t)m;
+      if (po.e1) po.e1[mat] = e1;
+      if (po.e2) po.e2[mat] = e2;
+      if (po.norms) {
+        po.norms[2 * mat] = nv;
+        po.norms[2 * mat + 1] = nv2;
+      }
+      if (po.mults) po.mults[mat] = flags ? 0 : lr_mults(m);
+      if (po.flags) po.flags[mat] = flags;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 flow-layer shape n = 64, t = 8 on the FP64 tensor cores: every product
+// of the path is DMMA (mma.sync.m8n8k4.f64): V = A2 A1 is 16 DMMA, each 8x8
+// t x t product 2, Y = psi A2 16 and the assembly I + A1 Y 128 -- against
+// ~1.3k DFMA warp-instructions per matrix on the FMA pipe, which left the
+// warp kernel issue bound.  Lane (g = lane/4, q = lane%4) owns the
+// accumulator entries (g, 2q), (g, 2q + 1) of every 8x8 tile, which is the
+// same t x t ownership as the warp kernel above.  A1 and the t x t tiles
+// use 8-wide rows with the column XOR-swizzled by bit 1 of the row so both
+// the A-fragment (row g, column q) and B-fragment (row q, column g) walks
+// are bank-conflict free.
+// ---------------------------------------------------------------------------
+
+struct LrD {
+  static constexpr int WARPS = 4;
+  static constexpr int NT = 32 * WARPS;
+  static constexpr int LDY = 68;  // A2 / Y rows (8 x 64): conflict-free fragment walks
+  static constexpr int kA2 = 512;
+  static constexpr int kP = kA2 + 8 * LDY;
+  static constexpr int kSlot = 64;
+  static constexpr int kStride = kP + 7 * kSlot;  // slot 0 = psi, 1..6 = V^p
+  static constexpr size_t kSmem = (size_t)WARPS * kStride * sizeof(double);
+};
+
+__device__ __forceinline__ int lr_sw8(int r, int c) { return r * 8 + (c ^ (((r >> 1) & 1) << 2)); }
+
+__device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// (d0, d1) = entries (g, 2q), (g, 2q + 1) of A B for swizzled 8x8 tiles.
+__device__ __forceinline__ void lr_mm8(const double* A, const double* B, int g, int q, double& d0, double& d1) {
+  d0 = 0.0;
+  d1 = 0.0;
+  lr_dmma(d0, d1, A[lr_sw8(g, q)], B[lr_sw8(q, g)]);
+  lr_dmma(d0, d1, A[lr_sw8(g, q + 4)], B[lr_sw8(q + 4, g)]);
+}
+
+__device__ __forceinline__ int hi_abs(double v) { return __double2hiint(v) & 0x7fffffff; }
+
+__global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __restrict__ A1,
+                                                                const double* __restrict__ A2,
+                                                                double* __restrict__ X, int64_t batch,
+                                                                double log_eps, LrOut po) {
+  using L = LrD;
+  extern __shared__ __align__(16) unsigned char lrd_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double* base = reinterpret_cast<double*>(lrd_smem) + w * L::kStride;
+  double* sA1 = base;
+  double* sY = base + L::kA2;  // A2, then Y = psi A2
+  double* P = base + L::kP;
+  const int own = lr_sw8(g, 2 * q);  // this lane's entry pair in every t x t tile
+  const int64_t nw = (int64_t)gridDim.x * L::WARPS;
+  for (int64_t mat = (int64_t)blockIdx.x * L::WARPS + w; mat < batch; mat += nw) {
+    const double* a1 = A1 + (size_t)mat * 512;
+    const double* a2 = A2 + (size_t)mat * 512;
+    double* x = X + (size_t)mat * 4096;
+    // ---- factors -> shared (all 16 loads in flight), exponent-word max ----
+    double2 ra[8], rb[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ra[j] = *reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) rb[j] = *reinterpret_cast<const double2*>(a2 + 64 * j + 2 * lane);
+    int hx1 = 0, hx2 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int p = lane + 32 * j;
+      *reinterpret_cast<double2*>(sA1 + lr_sw8(p >> 2, 2 * (p & 3))) = ra[j];
+      *reinterpret_cast<double2*>(sY + j * L::LDY + 2 * lane) = rb[j];
+      hx1 = max(hx1, max(hi_abs(ra[j].x), hi_abs(ra[j].y)));
+      hx2 = max(hx2, max(hi_abs(rb[j].x), hi_abs(rb[j].y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      hx1 = max(hx1, __shfl_xor_sync(0xffffffffu, hx1, o));
+      hx2 = max(hx2, __shfl_xor_sync(0xffffffffu, hx2, o));
+    }
+    __syncwarp();
+    int m = 0, rc = 0;
+    bool wrote = false;
+    double e1 = NAN, e2 = NAN, nv = NAN, nv2 = NAN;
+    uint8_t flags = (max(hx1, hx2) >= 0x7ff00000) ? kLrBadInput : 0;  // NaN/Inf exponent field
+    if (!flags) {
+      // V = A2 A1: 16 k-steps of 4
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 16; ++s) lr_dmma(v0, v1, sY[g * L::LDY + 4 * s + q], sA1[lr_sw8(4 * s + q, g)]);
+      double* V = P + L::kSlot;
+      *reinterpret_cast<double2*>(V + own) = make_double2(v0, v1);
+      __syncwarp();
+      double c = 0.0;
+      if (lane < 8)
+        for (int r = 0; r < 8; ++r) c += fabs(V[lr_sw8(r, lane)]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c = lr_nanmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+      nv = c;
+      if (!isfinite(nv)) {
+        rc = 2;
+      } else {
+        rc = select_lowrank(nv, 0.0, 0, log_eps, &m, &e1, &e2);
+        if (rc == 1) {
+          double d0, d1;
+          lr_mm8(V, V, g, q, d0, d1);
+          *reinterpret_cast<double2*>(P + 2 * L::kSlot + own) = make_double2(d0, d1);
+          __syncwarp();
+          double c2 = 0.0;
+          if (lane < 8)
+            for (int r = 0; r < 8; ++r) c2 += fabs(P[2 * L::kSlot + lr_sw8(r, lane)]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c2 = lr_nanmax(c2, __shfl_xor_sync(0xffffffffu, c2, o));
+          nv2 = c2;
+          rc = isfinite(nv2) ? select_lowrank(nv, nv2, 1, log_eps, &m, &e1, &e2) : 2;
+        }
+      }
+      if (rc == 2) flags = kLrNonFinite;
+      if (rc < 0) {
+        flags = kLrNoOrder;
+        e1 = e2 = NAN;
+      }
+    }
+    if (!flags) {
+      // ---- psi(V) by Paterson-Stockmeyer (poly.py:149-182) ----
+      double q0, q1;
+      const bool dg0 = g == 2 * q, dg1 = g == 2 * q + 1;  // own entries on the diagonal
+      if (m == 0) {
+        q0 = dg0 ? 1.0 : 0.0;
+        q1 = dg1 ? 1.0 : 0.0;
+      } else {
+        const int j = ps_j_of(m);
+        const int k = (m + j - 1) / j;
+        for (int p = 3; p <= j; ++p) {
+          double d0, d1;
+          lr_mm8(P + (p - 1) * L::kSlot, P + L::kSlot, g, q, d0, d1);
+          *reinterpret_cast<double2*>(P + p * L::kSlot + own) = make_double2(d0, d1);
+          __syncwarp();
+        }
+        q0 = q1 = 0.0;
+        for (int r = k - 1; r >= 0; --r) {
+          const int lo = r * j, hi = (r == k - 1) ? m : r * j + j - 1;
+          double s0 = 0.0, s1 = 0.0;
+          if (r < k - 1) lr_mm8(P, P + j * L::kSlot, g, q, s0, s1);
+          const double c0 = lr_inv_fact(lo + 1);
+          double b0 = dg0 ? c0 : 0.0, b1 = dg1 ? c0 : 0.0;
+          for (int tt = 1; tt <= hi - lo; ++tt) {
+            const double cf = lr_inv_fact(lo + tt + 1);
+            const double2 pv = *reinterpret_cast<const double2*>(P + tt * L::kSlot + own);
+            b0 = fma(cf, pv.x, b0);
+            b1 = fma(cf, pv.y, b1);
+          }
+          q0 = (r < k - 1) ? s0 + b0 : b0;
+          q1 = (r < k - 1) ? s1 + b1 : b1;
+          __syncwarp();
+          *reinterpret_cast<double2*>(P + own) = make_double2(q0, q1);
+          __syncwarp();
+        }
+      }
+      *reinterpret_cast<double2*>(P + own) = make_double2(q0, q1);
+      __syncwarp();
+      if (__any_sync(0xffffffffu, !isfinite(q0) || !isfinite(q1))) {
+        flags = kLrNonFinite;
+      } else {
+        // ---- Y = psi A2 (16 DMMA), written over A2 ----
+        double ab0[8], ab1[8];
+#pragma unroll
+        for (int C = 0; C < 8; ++C) {
+          ab0[C] = sY[q * L::LDY + 8 * C + g];
+          ab1[C] = sY[(q + 4) * L::LDY + 8 * C + g];
+        }
+        const double pa0 = P[lr_sw8(g, q)], pa1 = P[lr_sw8(g, q + 4)];
+        double y0[8], y1[8];
+#pragma unroll
+        for (int C = 0; C < 8; ++C) {
+          y0[C] = 0.0;
+          y1[C] = 0.0;
+          lr_dmma(y0[C], y1[C], pa0, ab0[C]);
+          lr_dmma(y0[C], y1[C], pa1, ab1[C]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int C = 0; C < 8; ++C)
+          *reinterpret_cast<double2*>(sY + g * L::LDY + 8 * C + 2 * q) = make_double2(y0[C], y1[C]);
+        __syncwarp();
+        // overflow bound: |out| <= 1 + 8 max|A1| max|Y|; exponent words give
+        // 2^(e+1) bounds, so the check is skipped unless the sum of exponents
+        // comes near the top of the range
+        int hy = 0;
+#pragma unroll
+        for (int C = 0; C < 8; ++C) hy = max(hy, max(hi_abs(y0[C]), hi_abs(y1[C])));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hy = max(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+        const int eA = (hx1 >> 20) - 1023, eY = (hy >> 20) - 1023;
+        const bool safe = eA + eY + 5 < 1000;
+        // ---- out = I + A1 Y (128 DMMA), Y as B fragments ----
+        double yb0[8], yb1[8];
+#pragma unroll
+        for (int C = 0; C < 8; ++C) {
+          yb0[C] = sY[q * L::LDY + 8 * C + g];
+          yb1[C] = sY[(q + 4) * L::LDY + 8 * C + g];
+        }
+        bool bo = false;
+#pragma unroll 2
+        for (int R = 0; R < 8; ++R) {
+          const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
+          double* xr = x + (8 * R + g) * 64 + 2 * q;
+#pragma unroll
+          for (int C = 0; C < 8; ++C) {
+            double d0 = (R == C && dg0) ? 1.0 : 0.0;
+            double d1 = (R == C && dg1) ? 1.0 : 0.0;
+            lr_dmma(d0, d1, a0, yb0[C]);
+            lr_dmma(d0, d1, a1v, yb1[C]);
+            *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
+            if (!safe) bo |= !isfinite(d0) || !isfinite(d1);
+          }
+        }
+        wrote = true;
+        if (__any_sync(0xffffffffu, bo)) flags = kLrNonFinite;
+      }
+    }
+    if (flags && !wrote)
+      for (int i = lane; i < 4096; i += 32) x[i] = NAN;
     if (lane == 0) {
       if (po.m) po.m[mat] = (int8_t)m;
       if (po.e1) po.e1[mat] = e1;

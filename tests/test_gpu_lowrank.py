@@ -192,3 +192,54 @@ def test_lowrank_named_cases():
     assert float(r.value[0, 0]) == pytest.approx(1.0 + (math.exp(1.5) - 1.0), rel=1e-9)
     r = _run(np.array([[1.0], [0.0]]), np.array([[0.0, 3.0]]), 1e-8)  # V = 0: e^W = I + W
     assert np.array_equal(r.value.cpu().numpy(), np.array([[1.0, 3.0], [0.0, 1.0]]))
+
+
+def test_lowrank_misaligned_takes_cta_path():
+    """Factors at an 8-byte offset cannot use the 16-byte vector kernels: the
+    CTA kernel runs and agrees with the oracle."""
+    rng = np.random.default_rng(31)
+    A1, A2 = _gen(rng, 5, 64, 8, 0.1, 3.0)
+    buf1 = torch.empty(5 * 512 + 1, dtype=torch.float64, device="cuda")
+    buf2 = torch.empty(5 * 512 + 1, dtype=torch.float64, device="cuda")
+    a1 = buf1[1:].view(5, 64, 8)
+    a2 = buf2[1:].view(5, 8, 64)
+    a1.copy_(torch.as_tensor(A1))
+    a2.copy_(torch.as_tensor(A2))
+    assert a1.data_ptr() % 16 == 8
+    r = X.expm_lowrank(X.LowRankPair(a1, a2), 1e-10)
+    for b in range(5):
+        want = O.expm_lowrank(A1[b], A2[b], 1e-10)
+        assert int(r.plan.m[b]) == want.m
+        assert float(_rel1(r.value[b].cpu().numpy(), want.value)) <= _tol(A1[b], A2[b], want.m, want.value,
+                                                                       torch.float64)
+
+
+_PATH_SCRIPT = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+import paper_2512_20777_b200 as X
+from paper_2512_20777_b200 import workloads as WL
+A1, A2 = WL.generate_lowrank(np.arange(2048))
+r = X.expm_lowrank(X.LowRankPair(torch.as_tensor(A1, device='cuda'), torch.as_tensor(A2, device='cuda')), 2.0 ** -53)
+np.save(sys.argv[1], r.value.cpu().numpy())
+np.save(sys.argv[1] + '.m.npy', r.plan.m.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("env", ["EXPMB_LR_NO_DMMA", "EXPMB_LR_CTA"])
+def test_lowrank_kernel_variants_agree(tmp_path, env):
+    """The fp64 n=64/t=8 batch through the DMMA kernel (default), the FMA warp
+    kernel and the CTA kernel: identical orders, values within the fp64 bar."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, extra in (("default", {}), (env, {env: "1"})):
+        f = str(tmp_path / f"{name}.npy")
+        subprocess.run([sys.executable, "-c", _PATH_SCRIPT, f], cwd=root, check=True,
+                       env=dict(os.environ, **extra))
+        outs[name] = (np.load(f), np.load(f + ".m.npy"))
+    assert np.array_equal(outs["default"][1], outs[env][1])
+    err = _rel1(outs["default"][0], outs[env][0])
+    assert err.max() <= 1e-12, err.max()

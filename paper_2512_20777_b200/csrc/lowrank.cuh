@@ -831,16 +831,21 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
   double* P = base + L::kP;
   const int own = lr_sw8(g, 2 * q);  // this lane's entry pair in every t x t tile
   const int64_t nw = (int64_t)gridDim.x * L::WARPS;
-  for (int64_t mat = (int64_t)blockIdx.x * L::WARPS + w; mat < batch; mat += nw) {
-    const double* a1 = A1 + (size_t)mat * 512;
-    const double* a2 = A2 + (size_t)mat * 512;
+  // the factors of matrix mat + nw are loaded into registers while matrix
+  // mat is computed (16 x 16-byte loads in flight per lane)
+  double2 ra[8], rb[8];
+  auto fetch = [&](int64_t mm) {
+    const double* a1 = A1 + (size_t)mm * 512;
+    const double* a2 = A2 + (size_t)mm * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ra[j] = __ldcs(reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j)));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) rb[j] = __ldcs(reinterpret_cast<const double2*>(a2 + 64 * j + 2 * lane));
+  };
+  int64_t mat = (int64_t)blockIdx.x * L::WARPS + w;
+  if (mat < batch) fetch(mat);
+  for (; mat < batch; mat += nw) {
     double* x = X + (size_t)mat * 4096;
-    // ---- factors -> shared (all 16 loads in flight), exponent-word max ----
-    double2 ra[8], rb[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ra[j] = *reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j));
-#pragma unroll
-    for (int j = 0; j < 8; ++j) rb[j] = *reinterpret_cast<const double2*>(a2 + 64 * j + 2 * lane);
     int hx1 = 0, hx2 = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -850,6 +855,7 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
       hx1 = max(hx1, max(hi_abs(ra[j].x), hi_abs(ra[j].y)));
       hx2 = max(hx2, max(hi_abs(rb[j].x), hi_abs(rb[j].y)));
     }
+    if (mat + nw < batch) fetch(mat + nw);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       hx1 = max(hx1, __shfl_xor_sync(0xffffffffu, hx1, o));
@@ -978,18 +984,34 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
           yb1[C] = sY[(q + 4) * L::LDY + 8 * C + g];
         }
         bool bo = false;
+        if (safe) {
 #pragma unroll 2
-        for (int R = 0; R < 8; ++R) {
-          const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
-          double* xr = x + (8 * R + g) * 64 + 2 * q;
+          for (int R = 0; R < 8; ++R) {
+            const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
+            double* xr = x + (8 * R + g) * 64 + 2 * q;
 #pragma unroll
-          for (int C = 0; C < 8; ++C) {
-            double d0 = (R == C && dg0) ? 1.0 : 0.0;
-            double d1 = (R == C && dg1) ? 1.0 : 0.0;
-            lr_dmma(d0, d1, a0, yb0[C]);
-            lr_dmma(d0, d1, a1v, yb1[C]);
-            *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
-            if (!safe) bo |= !isfinite(d0) || !isfinite(d1);
+            for (int C = 0; C < 8; ++C) {
+              double d0 = (R == C && dg0) ? 1.0 : 0.0;
+              double d1 = (R == C && dg1) ? 1.0 : 0.0;
+              lr_dmma(d0, d1, a0, yb0[C]);
+              lr_dmma(d0, d1, a1v, yb1[C]);
+              __stcs(reinterpret_cast<double2*>(xr + 8 * C), make_double2(d0, d1));
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int R = 0; R < 8; ++R) {
+            const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
+            double* xr = x + (8 * R + g) * 64 + 2 * q;
+#pragma unroll
+            for (int C = 0; C < 8; ++C) {
+              double d0 = (R == C && dg0) ? 1.0 : 0.0;
+              double d1 = (R == C && dg1) ? 1.0 : 0.0;
+              lr_dmma(d0, d1, a0, yb0[C]);
+              lr_dmma(d0, d1, a1v, yb1[C]);
+              *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
+              bo |= !isfinite(d0) || !isfinite(d1);
+            }
           }
         }
         wrote = true;

@@ -7,3 +7,6 @@ python bench.py --config LR --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/
 ncu --set full --clock-control none --import-source on -k regex:lowrank -s 3 -c 1 \
     -o gpurun_out/prof_LR -f python bench.py --config LR --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_lr.log 2>&1
 echo done
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_LR.csv \
+    python bench.py --config LR --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_lr1.log 2>&1
+python -m pytest tests/test_gpu_lowrank.py -q -p no:cacheprovider > gpurun_out/pytest_lr.log 2>&1

@@ -370,8 +370,10 @@ def run_lowrank(args):
         ms_ = plan["m"].cpu().numpy()
         mults = plan["mults"].long().cpu().numpy()
         flops = float(B * (2 * t * t * n * 2 + 2 * n * n * t) + (mults * 2 * t ** 3).sum())
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic_LR.json")
+        traffic = json.load(open(tpath)).get("dram_bytes_per_launch") if os.path.exists(tpath) else None
         roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": gbs / pk["hbm_gbs"], "traffic": None, "peak_source": pk["hbm_src"],
+                "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["hbm_src"],
                 "algorithmic_bytes_per_launch": hbm_bytes, "kernel": "expm_lowrank_kernel<double,8>",
                 "other": {"bound": "fp64_dfma", "achieved": flops / (ms_per_step * 1e-3) / 1e12,
                           "peak": pk["dfma_fp64"], "unit": "TFLOP/s", "useful_flops_per_launch": flops}}

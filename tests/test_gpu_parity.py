@@ -418,3 +418,45 @@ def test_acceptance_08_logdet_equals_trace():
         tr = np.trace(W, axis1=1, axis2=2)
         assert (sign.cpu().numpy() == 1.0).all()
         np.testing.assert_allclose(logdet.cpu().numpy(), tr, rtol=0, atol=1e-8 * np.abs(tr).max() + 1e-12)
+
+
+def test_cuda_graph_capture_and_replay():
+    """expm_into / expm_lowrank_into (n <= 64) are capturable: no host sync,
+    no allocation.  A captured graph replayed on new inputs gives the same
+    results as eager calls (the serving-loop pattern: CUDA graphs instead of a
+    tracing compiler)."""
+    from paper_2512_20777_b200 import workloads as WL2
+    W = torch.as_tensor(WL.generate("C2", indices=np.arange(4096)), device="cuda")
+    Xg = torch.empty_like(W)
+    plan = {"m": torch.empty(4096, dtype=torch.int8, device="cuda"),
+            "s": torch.empty(4096, dtype=torch.int8, device="cuda"),
+            "mults": torch.empty(4096, dtype=torch.int32, device="cuda"),
+            "nonfinite": torch.empty(4096, dtype=torch.uint8, device="cuda")}
+    X.expm_into(W, Xg, 2.0 ** -24, "sastre", plan)  # warm (kernel attributes set outside capture)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.expm_into(W, Xg, 2.0 ** -24, "sastre", plan)
+    W.copy_(torch.as_tensor(WL.generate("C2", indices=np.arange(4096, 8192)), device="cuda"))
+    g.replay()
+    torch.cuda.synchronize()
+    ref = X.expm(W.clone(), 2.0 ** -24)
+    assert torch.equal(Xg, ref.value)
+    assert torch.equal(plan["m"], ref.plan.m) and torch.equal(plan["mults"], ref.mults)
+
+    A1, A2 = WL2.generate_lowrank(np.arange(512))
+    a1 = torch.as_tensor(A1, device="cuda")
+    a2 = torch.as_tensor(A2, device="cuda")
+    xo = torch.empty(512, 64, 64, dtype=torch.float64, device="cuda")
+    X.expm_lowrank_into(a1, a2, xo, 2.0 ** -53)
+    torch.cuda.synchronize()
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        X.expm_lowrank_into(a1, a2, xo, 2.0 ** -53)
+    A1b, A2b = WL2.generate_lowrank(np.arange(512, 1024))
+    a1.copy_(torch.as_tensor(A1b))
+    a2.copy_(torch.as_tensor(A2b))
+    g2.replay()
+    torch.cuda.synchronize()
+    ref2 = X.expm_lowrank(X.LowRankPair(a1.clone(), a2.clone()), 2.0 ** -53)
+    assert torch.equal(xo, ref2.value)

@@ -438,8 +438,22 @@ def run_ours(args):
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    tg = bool(getattr(args, "timegrid", False)) and cfg.key == "C3"
+    if tg:
+        # time-grid path: inputs are A and the times only
+        A_h, t_all = WL.c3_factors()
+        A_h, t_h = torch.from_numpy(A_h), torch.from_numpy(t_all[idx])
+        A_d, t_d = A_h.to(dev), t_h.to(dev)
+        tg_ws = torch.empty(max(1, int(XP._lib.lib().expmb_timegrid_workspace_bytes(B, cfg.n, 0))),
+                            dtype=torch.uint8, device=dev)
+        del W
+
     def step():
-        XP.expm_into(W, Xd, cfg.eps, args.scheme, plan)
+        if tg:
+            XP.expm_timegrid(A_d, t_d, cfg.eps, args.scheme, check_finite=False, out=Xd, plan=plan,
+                             workspace=tg_ws)
+        else:
+            XP.expm_into(W, Xd, cfg.eps, args.scheme, plan)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -480,8 +494,28 @@ def run_ours(args):
 
     # ---- end-to-end through the public API from pinned host memory --------
     # HostPipeline: H2D of W, expm, D2H of e^W + plan, chunked over 3 streams
-    Wp = Wh.pin_memory()
-    pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if cfg.n <= 64 else 1, device=dev)
+    if tg:
+        Ap, tp_ = A_h.pin_memory(), t_h.pin_memory()
+        Xp = torch.empty(B, cfg.n, cfg.n, dtype=dtype, pin_memory=True)
+        php = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in plan.items()}
+
+        class _TgPipe:
+            h2d_bytes = Ap.numel() * Ap.element_size() + tp_.numel() * tp_.element_size()
+            d2h_bytes = Xp.numel() * Xp.element_size() + sum(v.numel() * v.element_size() for v in php.values())
+
+            def run(self, *_a, **_k):
+                A_d.copy_(Ap, non_blocking=True)
+                t_d.copy_(tp_, non_blocking=True)
+                XP.expm_timegrid(A_d, t_d, cfg.eps, args.scheme, check_finite=False, out=Xd, plan=plan,
+                                 workspace=tg_ws)
+                Xp.copy_(Xd, non_blocking=True)
+                for k, v in plan.items():
+                    php[k].copy_(v, non_blocking=True)
+        pipe = _TgPipe()
+        Wp = None
+    else:
+        Wp = Wh.pin_memory()
+        pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if cfg.n <= 64 else 1, device=dev)
 
     def e2e_step():
         pipe.run(Wp, cfg.eps, args.scheme, check_finite=False)
@@ -552,6 +586,18 @@ def run_ours(args):
         else:
             roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
         roof["other"] = cmp_roof if hbm_binds else hbm_roof
+        if tg:
+            # the time-grid path skips the evaluation products: its roofline is
+            # over the flops it executes (squarings, shared powers in fp64, the
+            # fused combination); useful_flops stays the reference's ledger
+            n3 = 2.0 * cfg.n ** 3
+            ex_flops = float(np.asarray(s, np.int64).sum()) * n3 + 15 * n3 + B * 16 * 2.0 * cfg.n ** 2
+            ex_tf = ex_flops / (ms_per_step * 1e-3) / 1e12
+            roof = {"bound": "fp32_ffma", "achieved": ex_tf, "peak": cpeak, "unit": "TFLOP/s", "frac": ex_tf / cpeak,
+                    "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
+                    "executed_flops_per_launch": ex_flops, "traffic": None,
+                    "kernel": "gemm_stage_kernel (FFMA2) squarings + k_tg_combine",
+                    "other": {"reference_ledger_flops_per_launch": flops, "ledger_tflops": tflops}}
         cpu = None
         if not args.no_cpu_baseline:
             r, cores, sample = cpu_reference_rate(cfg.key)
@@ -566,6 +612,7 @@ def run_ours(args):
             "dtype": cfg.dtype, "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
             "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch_per_gpu": B, "global_batch": ws * B,
                        "n": cfg.n, "eps": cfg.eps, "scheme": args.scheme, "l2": "flushed between steps (252 MB write)",
+                       "path": "time grid: shared powers + per-time squarings (expm_timegrid)" if tg else "batched expm",
                        "timing": "per-step CUDA events around each call, host queue primed (device held by a sleep before the first step)",
                        "parallelism": f"batch-sharded x{ws}, no collective on the hot path"},
             "useful_tflops": tflops, "hbm_gbs": gbs,
@@ -573,7 +620,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "exps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": float(et.item()) / args.steps},
-            "gpu_launches": _launch_count(cfg.key, m, s, cfg.n) * args.steps,
+            "gpu_launches": (10 + int(np.asarray(s).max()) if tg else _launch_count(cfg.key, m, s, cfg.n)) * args.steps,
             "clocks": clk.summary(),
             "plan_histogram": hist,
             "mults_total": int(plan["mults"].long().sum().item()),
@@ -595,6 +642,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--timegrid", action="store_true",
+                    help="C3 through expm_timegrid (one A, many t_k: shared powers, SURVEY 8(f) rank 3)")
     ap.add_argument("--scheme", default="sastre", choices=["sastre", "ps", "baseline"],
                     help="evaluation route (baseline = Alg. 1, the paper's comparator; n <= 64)")
     args = ap.parse_args()

@@ -130,6 +130,26 @@ int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, i
  */
 int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int* m, double* e1, double* e2);
 
+/*
+ * Time grid: X[k] = e^(t_k A) for one n x n matrix A and K times t_k, the
+ * generative-flow case (BASELINE config C3).  Each
+ * X[k] is what expmb_expm returns for the materialised t_k A (engine.py:
+ * 119-152 per time point): the same plan (up to the last-bit difference
+ * between |t_k| ||A||_1 and ||fl(t_k A)||_1), the same outputs.  For n > 64
+ * the powers A^1..A^16 are formed once in binary64 and each time point costs
+ * only its s_k squarings plus one fused linear combination.
+ *
+ *   A          [n,n] device; t [K] device (same dtype); X [K,n,n] device
+ *   m..nonfinite, scheme, eps: as expmb_expm (per time point)
+ *   workspace  expmb_timegrid_workspace_bytes(K, n, dtype) bytes
+ * One small device->host copy of the plans (n > 64), as the large-n path.
+ */
+size_t expmb_timegrid_workspace_bytes(int64_t K, int32_t n, int dtype);
+int expmb_expm_timegrid(const void* A, const void* t, void* X, int64_t K, int32_t n, int dtype, double eps,
+                        int scheme, int8_t* m, int8_t* s, double* e1, double* e2, double* norms,
+                        int32_t* mults, uint8_t* nonfinite, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

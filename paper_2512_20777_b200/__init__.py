@@ -12,7 +12,7 @@ from .tables import (  # noqa: F401
 )
 from .api import (  # noqa: F401
     EvalPlan, ExpmResult, HostPipeline, SCHEME_BASELINE, check_tolerance, expm, expm_baseline, expm_host, expm_into, select_ps, select_sastre,
-    LowRankPair, expm_lowrank, expm_lowrank_into,
+    LowRankPair, expm_lowrank, expm_lowrank_into, expm_timegrid,
 )
 
 __version__ = "0.1.0"

@@ -35,6 +35,8 @@ EXPORTS = (
     "expmb_select_host",
     "expmb_expm_lowrank",
     "expmb_select_lowrank_host",
+    "expmb_timegrid_workspace_bytes",
+    "expmb_expm_timegrid",
 )
 
 LR_BAD_INPUT, LR_NONFINITE, LR_NO_ORDER = 1, 2, 4
@@ -81,6 +83,14 @@ def lib() -> ctypes.CDLL:
     L.expmb_select_lowrank_host.argtypes = [
         c.POINTER(c.c_double), c.c_int, c.c_double,
         c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
+    ]
+    L.expmb_timegrid_workspace_bytes.restype = c.c_size_t
+    L.expmb_timegrid_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int]
+    L.expmb_expm_timegrid.restype = c.c_int
+    L.expmb_expm_timegrid.argtypes = [
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+        c.c_void_p, c.c_size_t, c.c_void_p,
     ]
     _lib = L
     return L

@@ -448,3 +448,63 @@ def expm_lowrank_into(A1: torch.Tensor, A2: torch.Tensor, X: torch.Tensor, eps: 
         p("m"), p("e1"), p("e2"), p("norms"), p("mults"), p("flags"), torch.cuda.current_stream(A1.device).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
+
+
+# ---------------------------------------------------------------------------
+# Time grid: e^(t_k A) for one A and many t_k
+# ---------------------------------------------------------------------------
+
+def expm_timegrid(A: torch.Tensor, times: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE,
+                  check_finite: bool = True, out: torch.Tensor | None = None, plan: dict | None = None,
+                  workspace: torch.Tensor | None = None) -> ExpmResult:
+    """value[k] = e^(times[k] * A), each what ``expm`` returns for the
+    materialised matrix times[k] * A (engine.py:119-152 per time point).
+
+    For n > 64 the powers A^1..A^16 are formed once (binary64) and a time point
+    costs its s_k squarings plus one fused linear combination, instead of
+    budget(m_k) + s_k products.  ``out`` / ``plan`` / ``workspace`` may be
+    preallocated for steady-state loops (``expmb_timegrid_workspace_bytes``)."""
+    t0 = time.perf_counter()
+    if not isinstance(A, torch.Tensor) or A.dim() != 2 or A.shape[0] != A.shape[1] or A.shape[0] < 1:
+        raise MatrixError("A must be a square [n, n] tensor")
+    if scheme not in _SCHEMES:
+        raise MatrixError(f"unknown scheme {scheme!r}; expected 'ps' or 'sastre'")
+    if A.dtype not in (torch.float32, torch.float64):
+        raise MatrixError(f"dtype must be float32 or float64, got {A.dtype}")
+    if A.device.type != "cuda":
+        raise RuntimeError("expmkit_b200.expm_timegrid runs on CUDA tensors only (no CPU fallback)")
+    check_tolerance(eps, A.dtype)
+    n = A.shape[0]
+    A = A.contiguous()
+    t = times.to(device=A.device, dtype=A.dtype).reshape(-1).contiguous()
+    K = t.shape[0]
+    dev = A.device
+    X = out if out is not None else torch.empty(K, n, n, dtype=A.dtype, device=dev)
+    if plan is None:
+        plan = {"m": torch.empty(K, dtype=torch.int8, device=dev), "s": torch.empty(K, dtype=torch.int8, device=dev),
+                "e1": torch.empty(K, dtype=torch.float64, device=dev),
+                "e2": torch.empty(K, dtype=torch.float64, device=dev),
+                "norms": torch.empty(K, 2, dtype=torch.float64, device=dev),
+                "mults": torch.empty(K, dtype=torch.int32, device=dev),
+                "nonfinite": torch.empty(K, dtype=torch.uint8, device=dev)}
+    L = _lib.lib()
+    dt = _lib.EXPMB_F32 if A.dtype == torch.float32 else _lib.EXPMB_F64
+    wsb = int(L.expmb_timegrid_workspace_bytes(K, n, dt))
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+
+    def p(k):
+        v = plan.get(k)
+        return None if v is None else v.data_ptr()
+    rc = L.expmb_expm_timegrid(A.data_ptr(), t.data_ptr(), X.data_ptr(), K, n, dt, float(eps), _SCHEMES[scheme],
+                               p("m"), p("s"), p("e1"), p("e2"), p("norms"), p("mults"), p("nonfinite"),
+                               workspace.data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream)
+    if rc != 0:
+        _raise_rc(rc)
+    bad = plan["nonfinite"].bool() if plan.get("nonfinite") is not None else torch.zeros(K, dtype=torch.bool,
+                                                                                          device=dev)
+    if check_finite and K > 0 and bool(bad.any()):
+        idx = torch.nonzero(bad).flatten()[:8].tolist()
+        raise NonFiniteError(f"operation produced non-finite entries (time indices {idx}...)")
+    ep = EvalPlan(plan.get("m"), plan.get("s"), scheme, plan.get("e1"), plan.get("e2"), plan.get("norms"))
+    return ExpmResult(X, ep, plan.get("mults"), time.perf_counter() - t0, bad)

@@ -15,6 +15,7 @@
 #include "fused_dmma.cuh"
 #include "large.cuh"
 #include "lowrank.cuh"
+#include "timegrid.cuh"
 
 namespace expmb {
 
@@ -211,6 +212,21 @@ static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n
   return launch_lowrank<T, 32>(A1, A2, X, batch, n, t, eps, po, st);
 }
 
+// W_k = t_k A materialised (time-grid path for n <= 64, where the fused
+// per-matrix kernels are cheaper than shared powers).
+template <typename T>
+__global__ void k_tg_materialize(const T* __restrict__ A, const T* __restrict__ t, T* __restrict__ W, int64_t K,
+                                 size_t nn) {
+  const int64_t k = blockIdx.y;
+  const T tk = t[k];
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x)
+    W[k * nn + i] = tk * A[i];
+}
+
+static size_t tg_small_bytes(int64_t K, int n, int esize) {
+  return align256((size_t)K * n * n * esize) + 256;
+}
+
 extern "C" {
 
 int expmb_version(void) { return 100; }
@@ -326,6 +342,56 @@ int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, i
   if (dtype == EXPMB_F32)
     return dispatch_lowrank<float>((const float*)A1, (const float*)A2, (float*)X, batch, n, t, eps, po, st);
   return dispatch_lowrank<double>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
+}
+
+size_t expmb_timegrid_workspace_bytes(int64_t K, int32_t n, int dtype) {
+  if (K <= 0 || n < 1) return 0;
+  const int esize = dtype == EXPMB_F32 ? 4 : 8;
+  if (n <= 64) return tg_small_bytes(K, n, esize);
+  return tg_layout(K, n, esize).total;
+}
+
+int expmb_expm_timegrid(const void* A, const void* t, void* X, int64_t K, int32_t n, int dtype, double eps,
+                        int scheme, int8_t* m, int8_t* s, double* e1, double* e2, double* norms, int32_t* mults,
+                        uint8_t* nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
+  if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
+  if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS) return EXPMB_ERR_SCHEME;
+  if (n < 1 || K < 0) return EXPMB_ERR_SHAPE;
+  if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
+  if (((uintptr_t)A | (uintptr_t)X) & 15u) return EXPMB_ERR_ALIGN;
+  if (K == 0) return EXPMB_OK;
+  if (workspace == nullptr || workspace_bytes < expmb_timegrid_workspace_bytes(K, n, dtype)) return EXPMB_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  PlanOut po{m, s, e1, e2, norms, mults, nonfinite};
+  const int esize = dtype == EXPMB_F32 ? 4 : 8;
+  const size_t nn = (size_t)n * n;
+  if (n <= 64) {
+    unsigned char* ws = (unsigned char*)workspace;
+    void* W = ws;
+    int* ctr = (int*)(ws + align256((size_t)K * nn * esize));
+    int bx = (int)std::min<size_t>((nn + 255) / 256, 64);
+    for (int64_t k0 = 0; k0 < K; k0 += 65535) {
+      const int64_t kc = std::min<int64_t>(65535, K - k0);
+      if (dtype == EXPMB_F32)
+        k_tg_materialize<float><<<dim3(bx, (unsigned)kc), 256, 0, st>>>(
+            (const float*)A, (const float*)t + k0, (float*)W + k0 * nn, kc, nn);
+      else
+        k_tg_materialize<double><<<dim3(bx, (unsigned)kc), 256, 0, st>>>(
+            (const double*)A, (const double*)t + k0, (double*)W + k0 * nn, kc, nn);
+    }
+    if (cudaGetLastError() != cudaSuccess) return EXPMB_ERR_CUDA;
+    if (dtype == EXPMB_F32)
+      return scheme == EXPMB_SASTRE ? dispatch_small<float, 0>((const float*)W, (float*)X, K, n, eps, po, ctr, st)
+                                    : dispatch_small<float, 1>((const float*)W, (float*)X, K, n, eps, po, ctr, st);
+    return scheme == EXPMB_SASTRE ? dispatch_small<double, 0>((const double*)W, (double*)X, K, n, eps, po, ctr, st)
+                                  : dispatch_small<double, 1>((const double*)W, (double*)X, K, n, eps, po, ctr, st);
+  }
+  const TgLayout L = tg_layout(K, n, esize);
+  if (dtype == EXPMB_F32)
+    return tg_run<float>((const float*)A, (const float*)t, (float*)X, K, n, eps, scheme, po,
+                         (unsigned char*)workspace, L, st);
+  return tg_run<double>((const double*)A, (const double*)t, (double*)X, K, n, eps, scheme, po,
+                        (unsigned char*)workspace, L, st);
 }
 
 }  // extern "C"

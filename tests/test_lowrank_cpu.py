@@ -100,3 +100,21 @@ def test_lowrank_pair_validation():
     assert (p.n, p.t) == (8, 2)
     with pytest.raises(RuntimeError):
         ex.expm_lowrank(p, 1e-8)                    # CPU tensors: no fallback
+
+
+def test_timegrid_argument_errors_are_synchronous():
+    L = _lib.lib()
+
+    def call(K=4, n=128, dt=1, eps=1e-8, scheme=0, ws=None, wsb=0):
+        return L.expmb_expm_timegrid(None, None, None, K, n, dt, eps, scheme, *([None] * 7), ws, wsb, None)
+    assert call(eps=2.0 ** -54) == _lib.ERR_TOLERANCE
+    assert call(dt=0, eps=2.0 ** -25) == _lib.ERR_TOLERANCE
+    assert call(dt=4) == _lib.ERR_DTYPE
+    assert call(scheme=2) == _lib.ERR_SCHEME      # Alg. 1 has no time-grid form
+    assert call(n=0) == _lib.ERR_SHAPE
+    assert call(K=0) == 0
+    assert call() == _lib.ERR_WORKSPACE
+    # workspace: 16 binary64 powers + one scratch matrix per time point (+ plans)
+    need = L.expmb_timegrid_workspace_bytes(4, 128, 1)
+    assert need >= 16 * 128 * 128 * 8 + 4 * 128 * 128 * 8
+    assert L.expmb_timegrid_workspace_bytes(4, 16, 0) >= 4 * 16 * 16 * 4

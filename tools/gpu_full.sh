@@ -24,4 +24,7 @@ ncu --set full --clock-control none --import-source on -k regex:dmma -s 3 -c 1 \
 python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:gemm_stage -s 20 -c 1 \
     -o gpurun_out/prof_C4 -f python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_p4.log 2>&1
+python bench.py --config C3 --timegrid --steps 5 --warmup 3 > gpurun_out/bench_C3_timegrid.json 2> gpurun_out/bench_C3_timegrid.err
+python bench.py --config LR > gpurun_out/bench_LR.json 2> gpurun_out/bench_LR.err
+python bench.py --config LR --impl reference --steps 3 --warmup 1 > gpurun_out/bench_LR_reference.json 2> gpurun_out/bench_LR_reference.err
 echo done2

@@ -476,7 +476,7 @@ def expm_timegrid(A: torch.Tensor, times: torch.Tensor, eps: float, scheme: str 
     check_tolerance(eps, A.dtype)
     n = A.shape[0]
     A = A.contiguous()
-    t = times.to(device=A.device, dtype=A.dtype).reshape(-1).contiguous()
+    t = torch.as_tensor(times).to(device=A.device, dtype=A.dtype).reshape(-1).contiguous()
     K = t.shape[0]
     dev = A.device
     X = out if out is not None else torch.empty(K, n, n, dtype=A.dtype, device=dev)

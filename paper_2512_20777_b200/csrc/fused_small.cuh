@@ -24,6 +24,10 @@
 // the current one is being exponentiated.
 #pragma once
 
+#ifndef EXPMB_HM_RL
+#define EXPMB_HM_RL 1  // HM products take the left operand from registers
+#endif
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -142,6 +146,7 @@ template <typename T, int NPAD, int TM, int GROUPS, int SCHEME, bool HM = false>
 struct Fused {
   static_assert(!HM || (sizeof(T) == 4 && NPAD == 16 && TM == 2), "HM is the fp32 n<=16 warp kernel");
   static constexpr int LDL = 20, LDR = 24;  // HM: A-fragment / B-fragment conflict-free strides
+  static constexpr int LDR2 = 20;            // HM, register left operand: B rows 2t, 2t+1 conflict-free
   static constexpr bool HMODE = HM;
   static constexpr int TC = NPAD / 4;            // column quads
   static constexpr int TR = NPAD / TM;           // row phases
@@ -370,9 +375,53 @@ struct Fused {
     }
   }
 
+  // HM with the left operand straight from registers: the accumulator
+  // fragment a lane holds (rows g, g+8; columns 2t, 2t+1 of each 8-column
+  // half) IS an A fragment once the k index is permuted (k = t -> column
+  // 2t, k = t+4 -> column 2t+1 of the half); the B fragment then reads rows
+  // 2t, 2t+1 of the right operand instead of t, t+4.  Saves the left
+  // operand's shared-memory round trip (4 stores + 8 loads per product).
+  __device__ __forceinline__ void mm_hm_rl(const Tile& Lt, const T* __restrict__ R, Tile& out) const {
+    float acc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+    const int g8 = tr, t4 = tc;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t ah[4], al[4];
+      split_tf32(Lt[0][2 * ks], ah[0], al[0]);
+      split_tf32(Lt[1][2 * ks], ah[1], al[1]);
+      split_tf32(Lt[0][2 * ks + 1], ah[2], al[2]);
+      split_tf32(Lt[1][2 * ks + 1], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], bh0, bl0);
+        split_tf32(R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh1, bl1);
+        hmma(acc[nt], al, bh0, bh1);  // small terms first
+        hmma(acc[nt], ah, bl0, bl1);
+        hmma(acc[nt], ah, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      out[0][2 * nt] = acc[nt][0];
+      out[0][2 * nt + 1] = acc[nt][1];
+      out[1][2 * nt] = acc[nt][2];
+      out[1][2 * nt + 1] = acc[nt][3];
+    }
+  }
+
   // out = L * R where L, R are register tiles (stages through smem).
   __device__ __forceinline__ void product(const Tile& Lt, const Tile& Rt, Tile& out) const {
-    if constexpr (HM) {
+    if constexpr (HM && EXPMB_HM_RL) {
+      store_hm<LDR2>(buf1, Rt);
+      sync();
+      mm_hm_rl(Lt, buf1, out);
+      sync();
+    } else if constexpr (HM) {
       store_hm<LDL>(buf0, Lt);
       store_hm<LDR>(buf1, Rt);
       sync();
@@ -387,7 +436,12 @@ struct Fused {
     }
   }
   __device__ __forceinline__ void square(const Tile& Xt, Tile& out) const {
-    if constexpr (HM) {
+    if constexpr (HM && EXPMB_HM_RL) {
+      store_hm<LDR2>(buf1, Xt);
+      sync();
+      mm_hm_rl(Xt, buf1, out);
+      sync();
+    } else if constexpr (HM) {
       store_hm<LDL>(buf0, Xt);
       store_hm<LDR>(buf1, Xt);
       sync();

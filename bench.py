@@ -534,7 +534,9 @@ def run_ours(args):
         Wp = None
     else:
         Wp = Wh.pin_memory()
-        pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if cfg.n <= 64 else 1, device=dev)
+        # chunked so copies overlap compute (measured on B200, tools/e2e_large_probe.py:
+        # C4 1056 -> 1231 exps/s at 4 chunks, C3 61.6k -> 85.1k and C5 305 -> 358 at 8)
+        pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if (cfg.n <= 64 or B >= 128) else 4, device=dev)
 
     def e2e_step():
         pipe.run(Wp, cfg.eps, args.scheme, check_finite=False)

@@ -257,6 +257,18 @@ def test_config_C5_subset():
     print(f"C5 subset: exempt {ex}, worst {worst:.2e}")
 
 
+@pytest.mark.parametrize("dtype,scheme", [(torch.float64, "sastre"), (torch.float32, "sastre"),
+                                          (torch.float64, "ps")])
+def test_large_odd_orders(dtype, scheme):
+    """Orders that are not multiples of the 128-wide GEMM tiles or of 4 (the
+    vector width): ragged tile edges in every stage, both schemes."""
+    rng = np.random.default_rng(41)
+    for n in (65, 131, 777):
+        W = np.stack([rng.standard_normal((n, n)) * (t / n ** 0.5) for t in (0.05, 3.0, 40.0)])
+        ex, worst = _check_batch(W.astype(np.float32) if dtype == torch.float32 else W,
+                                 2.0 ** -24 if dtype == torch.float32 else 1e-12, scheme, dtype, f"odd n={n}")
+
+
 # ---------------------------------------------------------------------------
 # error behaviour and invariants
 # ---------------------------------------------------------------------------

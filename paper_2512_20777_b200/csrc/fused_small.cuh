@@ -24,6 +24,9 @@
 // the current one is being exponentiated.
 #pragma once
 
+#ifndef EXPMB_HM_SPLIT2
+#define EXPMB_HM_SPLIT2 1  // tf32 hi/lo splits in pairs (one FADD2 per two lo parts)
+#endif
 #ifndef EXPMB_HM_RL
 #define EXPMB_HM_RL 1  // HM products take the left operand from registers
 #endif
@@ -87,6 +90,11 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b), d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a), ub = *reinterpret_cast<unsigned long long*>(&b), d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
   return *reinterpret_cast<float2*>(&d);
 }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
@@ -335,6 +343,15 @@ struct Fused {
     hi = u;
     lo = __float_as_uint(x - __uint_as_float(u));
   }
+  // two splits with one packed subtraction (FADD2) for the lo parts
+  __device__ __forceinline__ static void split_tf32_2(float x0, float x1, uint32_t& h0, uint32_t& l0, uint32_t& h1,
+                                                      uint32_t& l1) {
+    h0 = __float_as_uint(x0) & 0xffffe000u;
+    h1 = __float_as_uint(x1) & 0xffffe000u;
+    const float2 lo = fsub2(make_float2(x0, x1), make_float2(__uint_as_float(h0), __uint_as_float(h1)));
+    l0 = __float_as_uint(lo.x);
+    l1 = __float_as_uint(lo.y);
+  }
   __device__ __forceinline__ static void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -391,15 +408,25 @@ struct Fused {
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       uint32_t ah[4], al[4];
+#if EXPMB_HM_SPLIT2
+      split_tf32_2(Lt[0][2 * ks], Lt[0][2 * ks + 1], ah[0], al[0], ah[2], al[2]);
+      split_tf32_2(Lt[1][2 * ks], Lt[1][2 * ks + 1], ah[1], al[1], ah[3], al[3]);
+#else
       split_tf32(Lt[0][2 * ks], ah[0], al[0]);
       split_tf32(Lt[1][2 * ks], ah[1], al[1]);
       split_tf32(Lt[0][2 * ks + 1], ah[2], al[2]);
       split_tf32(Lt[1][2 * ks + 1], ah[3], al[3]);
+#endif
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         uint32_t bh0, bl0, bh1, bl1;
+#if EXPMB_HM_SPLIT2
+        split_tf32_2(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh0,
+                     bl0, bh1, bl1);
+#else
         split_tf32(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], bh0, bl0);
         split_tf32(R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh1, bl1);
+#endif
         hmma(acc[nt], al, bh0, bh1);  // small terms first
         hmma(acc[nt], ah, bl0, bl1);
         hmma(acc[nt], ah, bh0, bh1);

@@ -30,6 +30,7 @@ from expmkit import GeneratorSpec, Matrix, NonFiniteError, gen_matrix  # noqa: E
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "expm_golden.npz")
 OUT_LR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lowrank_golden.npz")
+OUT_SUITE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "suite_golden.npz")
 
 
 def cases():
@@ -178,6 +179,32 @@ def main_lowrank():
     print(f"wrote {len(names)} low-rank cases -> {OUT_LR}")
 
 
+def main_suite():
+    """The reference's suite plumbing (bench.py:60-251): the default config's
+    spec list (kinds, orders, norms, derived seeds) and the generated matrices
+    of a sample of specs covering every generator kind."""
+    from expmkit.bench import GeneratorSpec as GS, default_suite_config, gen_matrix as gm
+    cfg = default_suite_config()
+    specs = cfg.specs()
+    sample = [GS(kind=k, n=n, target_norm=t, seed=1000 + i)
+              for i, (k, n, t) in enumerate([("diag", 8, 0.3), ("random_dense", 16, 2.5),
+                                             ("nonnormal_triangular", 12, 7.0), ("nilpotent_perturbed", 9, 1.1),
+                                             ("rotation_block", 10, 4.0), ("random_dense", 33, 1e-3)])]
+    mats = [gm(sp).a.ravel() for sp in sample]
+    offs = np.concatenate([[0], np.cumsum([m.size for m in mats])])
+    np.savez_compressed(
+        OUT_SUITE,
+        spec_kind=np.array([sp.kind for sp in specs]), spec_n=np.array([sp.n for sp in specs]),
+        spec_norm=np.array([sp.target_norm for sp in specs]),
+        spec_seed=np.array([sp.seed for sp in specs], dtype=np.uint64),
+        sample_kind=np.array([sp.kind for sp in sample]), sample_n=np.array([sp.n for sp in sample]),
+        sample_norm=np.array([sp.target_norm for sp in sample]),
+        sample_seed=np.array([sp.seed for sp in sample], dtype=np.uint64),
+        offsets=offs, W=np.concatenate(mats))
+    print(f"wrote {len(specs)} suite specs + {len(sample)} generated matrices -> {OUT_SUITE}")
+
+
 if __name__ == "__main__":
     main()
     main_lowrank()
+    main_suite()

@@ -11,8 +11,10 @@
 //     where x_lo = x - tf32(x).  The hardware truncates fp32 inputs to tf32
 //     (measured, tools/tc_probe.cu), so the raw fp32 array is the "hi" part
 //     and the producers store x_lo = x - trunc_tf32(x) beside it;
-//   * even and odd k-tiles accumulate into two TMEM accumulators (halving
-//     the fp32 accumulation chain; the 1e-5 fp32 bar has ~2x margin at n=2048);
+//   * k-tiles accumulate round-robin into NACC = 4 TMEM accumulators (the
+//     tensor core's fp32 accumulation truncates: the bias grows with the
+//     chain length, so shorter chains, summed with round-to-nearest in the
+//     epilogue, shrink it);
 //   * four epilogue warps read the accumulators (tcgen05.ld 32x32b), apply
 //     the stage's linear combination for the CTA's matrix, and write each
 //     result in the layouts its consumers need: row-major value (+ lo) for a
@@ -37,7 +39,11 @@ constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A, A_lo, B, B_lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
 constexpr int NTHREADS = 192;                      // w0 TMA, w1 MMA/TMEM, w2..w5 epilogue
-constexpr uint32_t TMEM_COLS = 256;                // two 128-column fp32 accumulators
+#ifndef EXPMB_TC_NACC
+#define EXPMB_TC_NACC 4
+#endif
+constexpr int NACC = EXPMB_TC_NACC;                // k-tiles round-robin over NACC accumulators
+constexpr uint32_t TMEM_COLS = NACC * 128;         // NACC 128-column fp32 accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -313,14 +319,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_stage_kernel(const __grid_cons
       mbar_wait(&full_bar[st], (kt / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t base = smem_u32(sm + st * STAGE_BYTES);
-      const uint32_t acc = tmem + (uint32_t)((kt & 1) * BN);
+      const uint32_t acc = tmem + (uint32_t)((kt % NACC) * BN);
 #pragma unroll
       for (int k = 0; k < BK / 8; ++k) {
         const uint64_t a = kmajor_desc(base + k * 32);
         const uint64_t alo = kmajor_desc(base + TILE_BYTES + k * 32);
         const uint64_t b = kmajor_desc(base + 2 * TILE_BYTES + k * 32);
         const uint64_t blo = kmajor_desc(base + 3 * TILE_BYTES + k * 32);
-        mma_tf32(acc, a, b, (kt >= 2 || k > 0) ? 1u : 0u);
+        mma_tf32(acc, a, b, (kt >= NACC || k > 0) ? 1u : 0u);
         mma_tf32(acc, a, blo, 1u);
         mma_tf32(acc, alo, b, 1u);
       }
@@ -340,10 +346,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_stage_kernel(const __grid_cons
       float v[32], v1[32];
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * 32;
       tmem_ld32(ta, v);
-      if (KT > 1) {
+      // pairwise sum of the accumulators that were written (KT may be < NACC)
+      if (NACC == 4 && KT >= 4) {
+        float v2[32], v3[32];
         tmem_ld32(ta + BN, v1);
+        tmem_ld32(ta + 2 * BN, v2);
+        tmem_ld32(ta + 3 * BN, v3);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += v1[j];
+        for (int j = 0; j < 32; ++j) v[j] = (v[j] + v1[j]) + (v2[j] + v3[j]);
+      } else {
+        for (int a = 1; a < NACC && a < KT; ++a) {
+          tmem_ld32(ta + a * BN, v1);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += v1[j];
+        }
       }
       const int c0 = n0 + cb * 32;
       float o0[32];

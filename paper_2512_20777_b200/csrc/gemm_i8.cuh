@@ -1,0 +1,361 @@
+// gemm_i8.cuh -- exact-accumulation fp32 products on the 5th-generation tensor
+// cores: int8 mantissa slices with int32 accumulation (Ozaki scheme).
+//
+// Why: the tcgen05 tf32 path (gemm_tc.cuh) is 2.8x faster than the FFMA GEMM
+// on C5, but the tensor core's fp32 accumulation truncates and the squaring
+// phase amplifies that bias past the 1e-5 bar.  Integer accumulation is exact.
+//
+// Operands (per product P = L R of a stage, for every matrix of the bucket):
+//   L[r][k] = 2^(er_r - 6) (s0 + s1/128 + s2/128^2 + s3/128^3),  |s_i| <= 64
+//   R[k][c] = 2^(ec_c - 6) (t0 + t1/128 + t2/128^2 + t3/128^3)
+// with er_r / ec_c the binary exponents of the row / column maxima (|x| < 2^e),
+// every s_i, t_j an int8 obtained exactly (scaling by powers of two, rint,
+// exact residuals); the truncation is 2^-29 of the row (column) maximum.
+//   P[r][c] = 2^(er_r + ec_c - 12) sum_{L=0..3} 2^(-7L) acc_L[r][c],
+//   acc_L = sum_{i+j=L} S_i T_j  (int32 on tcgen05.mma.kind::i8, exact)
+// Ten slice-pair GEMMs (pairs with i + j > 3 contribute < 2^-28 of the row and
+// column maxima and are dropped), the level sum and the scaling in binary64,
+// then one rounding to fp32 -- the result is at least as accurate as an fp32
+// FMA dot product, with no systematic bias.
+//
+// Kernels: k_i8_rowexp / k_i8_colexp (exponents), k_i8_slice_rows (L slices,
+// K-major), k_i8_slice_cols (R slices transposed to K-major), k_i8_stage
+// (TMA 128B-swizzled ring of 4 L slices + 4 R slices per k-tile, one thread
+// issuing the ten pair MMAs per 32-byte k-step into four int32 TMEM
+// accumulators, four epilogue warps applying the stage's fused linear
+// combination exactly as gemm_simt.cuh's epilogue does).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+
+namespace expmb {
+namespace i8 {
+
+constexpr int BM = 128, BN = 64, BKB = 128, STAGES = 2, NSL = 4;
+constexpr int A_TILE = BM * BKB;                     // 16 KB
+constexpr int B_TILE = BN * BKB;                     // 8 KB
+constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 96 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
+constexpr int NTHREADS = 192;                         // w0 TMA, w1 MMA/TMEM, w2..w5 epilogue
+constexpr uint32_t TMEM_COLS = 4 * BN;                // one int32 accumulator per level
+constexpr int kNanExp = -100000;                      // row/column holds NaN/Inf
+// kind::i8: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 64, M = 128
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+struct Bufs {
+  int8_t* as;  // [slot][4][n][np]  L slices, row-major (K contiguous)
+  int8_t* bs;  // [slot][4][n][np]  R slices, transposed (K contiguous)
+  int* er;     // [slot][n]
+  int* ec;     // [slot][n]
+  int np;      // padded row length (multiple of 16 bytes, TMA stride rule)
+};
+
+__device__ __forceinline__ int exp_of(float mx) {
+  if (!(mx < INFINITY)) return kNanExp;  // Inf or NaN
+  if (mx == 0.f) return 0;
+  return ilogbf(mx) + 1;  // mx = f 2^e with f in [0.5, 1)
+}
+
+__device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
+  if (e == kNanExp) {
+    s[0] = s[1] = s[2] = s[3] = 0;
+    return;
+  }
+  float y = scalbnf(x, 6 - e);  // |y| < 64, exact
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float q = rintf(y);
+    s[i] = (int8_t)(int)q;
+    y = (y - q) * 128.f;  // exact: |y - q| <= 1/2
+  }
+}
+
+// Row exponents of every participating L (one warp per row).
+__global__ void __launch_bounds__(256) k_i8_rowexp(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                    Bufs b) {
+  const int slot = blockIdx.y;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;
+  const int n = g.n;
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (r >= n) return;
+  const float* row = e.L + (size_t)r * n;
+  float mx = 0.f;
+  for (int c = lane; c < n; c += 32) {
+    const float a = fabsf(row[c]);
+    mx = (a > mx || a != a) ? a : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (v > mx || v != v) ? v : mx;
+  }
+  if (lane == 0) b.er[(size_t)slot * n + r] = exp_of(mx);
+}
+
+// Column exponents of every participating R (one thread per column).
+__global__ void __launch_bounds__(256) k_i8_colexp(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                    Bufs b) {
+  const int slot = blockIdx.y;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;
+  const int n = g.n;
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= n) return;
+  float mx = 0.f;
+  for (int r = 0; r < n; ++r) {
+    const float a = fabsf(e.R[(size_t)r * n + c]);
+    mx = (a > mx || a != a) ? a : mx;
+  }
+  b.ec[(size_t)slot * n + c] = exp_of(mx);
+}
+
+// L slices: row-major, four planes.
+__global__ void __launch_bounds__(256) k_i8_slice_rows(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                        Bufs b) {
+  const int slot = blockIdx.z;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;
+  const int n = g.n;
+  const int r = blockIdx.y;
+  const int er = b.er[(size_t)slot * n + r];
+  const size_t plane = (size_t)n * b.np;
+  int8_t* out = b.as + (size_t)slot * NSL * plane + (size_t)r * b.np;
+  for (int c = blockIdx.x * 256 + threadIdx.x; c < n; c += gridDim.x * 256) {
+    int8_t s[4];
+    slice4(e.L[(size_t)r * n + c], er, s);
+#pragma unroll
+    for (int i = 0; i < NSL; ++i) out[i * plane + c] = s[i];
+  }
+}
+
+// R slices transposed through a 32x32 shared tile: bs[j][c][k] = slice_j(R[k][c]).
+__global__ void __launch_bounds__(256) k_i8_slice_cols(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                        Bufs b) {
+  const int slot = blockIdx.z;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;
+  __shared__ float tile[32][33];
+  const int n = g.n;
+  const int k0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 rows of 32
+  for (int i = ty; i < 32; i += 8) {
+    const int k = k0 + i, c = c0 + tx;
+    tile[i][tx] = (k < n && c < n) ? e.R[(size_t)k * n + c] : 0.f;
+  }
+  __syncthreads();
+  const size_t plane = (size_t)n * b.np;
+  int8_t* base = b.bs + (size_t)slot * NSL * plane;
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i, k = k0 + tx;
+    if (c < n && k < n) {
+      int8_t s[4];
+      slice4(tile[tx][i], b.ec[(size_t)slot * n + c], s);
+#pragma unroll
+      for (int j = 0; j < NSL; ++j) base[j * plane + (size_t)c * b.np + k] = s[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld32i(uint32_t taddr, int (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = (int)r[j];
+}
+
+struct Maps {
+  CUtensorMap a, b;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
+                                                          int stage, const int* __restrict__ list, Bufs bf) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int ec_sh[BN];
+  const int slot = blockIdx.z;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;  // uniform per CTA
+
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = g.n;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int KT = (n + BKB - 1) / BKB;
+
+  if (threadIdx.x < BN) ec_sh[threadIdx.x] = (n0 + threadIdx.x < n) ? bf.ec[(size_t)slot * n + n0 + threadIdx.x] : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(&full_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], 1);
+    }
+    tc::mbar_init(&tmem_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: 4 L slices + 4 R slices per k-tile ----------------
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      tc::mbar_wait(&empty_bar[st], ((kt / STAGES) & 1) ^ 1);
+      unsigned char* b = sm + st * STAGE_BYTES;
+      tc::mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+#pragma unroll
+      for (int i = 0; i < NSL; ++i) {
+        tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
+        tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: ten slice pairs per 32-byte k-step ----------------
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      tc::mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = tc::smem_u32(sm + st * STAGE_BYTES);
+#pragma unroll
+      for (int k = 0; k < BKB / 32; ++k) {
+#pragma unroll
+        for (int lv = 0; lv < 4; ++lv) {
+#pragma unroll
+          for (int i = 0; i <= lv; ++i) {
+            const int j = lv - i;
+            const uint64_t a = tc::kmajor_desc(base + i * A_TILE + k * 32);
+            const uint64_t bd = tc::kmajor_desc(base + NSL * A_TILE + j * B_TILE + k * 32);
+            mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
+          }
+        }
+      }
+      tc::mma_commit(&empty_bar[st]);
+    }
+    tc::mma_commit(&tmem_bar);
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    tc::mbar_wait(&tmem_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    const int r = m0 + rl;
+    const bool rowok = r < n;
+    const int er = rowok ? bf.er[(size_t)slot * n + r] : 0;
+    double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
+    for (int cb = 0; cb < BN / 32; ++cb) {
+      int a0[32], a1[32];
+      float v[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * 32;
+      tmem_ld32i(ta, a0);
+      tmem_ld32i(ta + BN, a1);
+      double d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j] = (double)a0[j] + ldexp((double)a1[j], -7);
+      tmem_ld32i(ta + 2 * BN, a0);
+      tmem_ld32i(ta + 3 * BN, a1);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int ec = ec_sh[cb * 32 + j];
+        const double t = d[j] + ldexp((double)a0[j], -14) + ldexp((double)a1[j], -21);  // exact in binary64
+        v[j] = (er == kNanExp || ec == kNanExp) ? NAN : (float)ldexp(t, er + ec - 12);
+      }
+      const int c0 = n0 + cb * 32;
+      float o0[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) o0[j] = e.alpha * v[j];
+      for (int qq = 0; qq < e.nin; ++qq) {
+        const float cq = e.c[0][qq];
+        if (cq == 0.f || !rowok) continue;
+        const float* ip = e.in[qq] + (size_t)r * n + c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
+      }
+      if (e.d[0] != 0.f && r >= c0 && r < c0 + 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
+      }
+      if (rowok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < n) e.out[0][(size_t)r * n + c0 + j] = o0[j];
+      }
+      for (int k = 1; k < e.nout; ++k) {
+        float ok[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ok[j] = o0[j];
+        for (int qq = 0; qq < e.nin; ++qq) {
+          const float cq = e.c[k][qq];
+          if (cq == 0.f || !rowok) continue;
+          const float* ip = e.in[qq] + (size_t)r * n + c0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+        }
+        if (e.d[k] != 0.f && r >= c0 && r < c0 + 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
+        }
+        if (rowok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) e.out[k][(size_t)r * n + c0 + j] = ok[j];
+        }
+      }
+      if (e.colnorm) {
+        // deterministic column abs-sums of this 128-row tile (select.py:193)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (rl < 32 && c0 + rl < n) {
+          double a = 0.0;
+          for (int rr = 0; rr < BM; ++rr) a += red[rl * BM + rr];
+          g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + c0 + rl] = a;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace i8
+}  // namespace expmb

@@ -30,6 +30,7 @@
 #include "fused_small.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
+#include "gemm_i8.cuh"
 #include "select.cuh"
 
 namespace expmb {
@@ -50,6 +51,13 @@ static inline bool use_tc_path(int n, int esize, int scheme) {
   const char* e = getenv("EXPMB_TC");
   return esize == 4 && scheme == 0 && (n % 4) == 0 && e != nullptr && e[0] == '1';
 }
+// Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh):
+// opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
+static inline bool use_i8_path(int n, int esize) {
+  const char* e = getenv("EXPMB_I8");
+  return esize == 4 && e != nullptr && e[0] == '1' && n >= 1;
+}
+static inline int i8_np(int n) { return (n + 15) / 16 * 16; }
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers
 
 struct LargeLayout {
@@ -58,6 +66,7 @@ struct LargeLayout {
   int nbufs;
   int tiles_m;
   size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_flags, off_m, off_s, off_e1, off_e2, off_list, total;
+  size_t off_i8as, off_i8bs, off_i8er, off_i8ec;  // int8-slice path (0 sizes otherwise)
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -66,7 +75,9 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   LargeLayout L{};
   L.mat_bytes = align256((size_t)n * n * esize);
   L.nbufs = use_tc_path(n, esize, scheme) ? kLargeBufsTC : (scheme == 1 ? kLargeBufsPS : kLargeBufsSastre);
-  const size_t per = L.mat_bytes * L.nbufs;
+  const bool i8p = use_i8_path(n, esize) && !use_tc_path(n, esize, scheme);
+  const size_t i8plane = (size_t)n * i8_np(n);
+  const size_t per = L.mat_bytes * L.nbufs + (i8p ? 2 * i8::NSL * i8plane + 2 * (size_t)n * sizeof(int) : 0);
   int64_t chunk = (int64_t)(kLargeWsCap / per);
   if (chunk < 1) chunk = 1;
   if (chunk > 65535) chunk = 65535;  // gridDim.z
@@ -85,6 +96,10 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.off_e1 = off; off += align256((size_t)chunk * sizeof(double));
   L.off_e2 = off; off += align256((size_t)chunk * sizeof(double));
   L.off_list = off; off += align256((size_t)chunk * 8 * sizeof(int));
+  L.off_i8as = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
+  L.off_i8bs = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
+  L.off_i8er = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
+  L.off_i8ec = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
   L.total = off;
   return L;
 }
@@ -213,6 +228,57 @@ static void launch_finish(const T* X, int n, int ic, int scheme, const LargeLayo
   k_finish<<<(ic + 255) / 256, 256, 0, st>>>(ic, scheme, nrm4, dm, ds, de1, de2, flags, base, po);
 }
 
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static TensorMapEncodeFn tensor_map_encoder() {
+  static TensorMapEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (TensorMapEncodeFn)p;
+  }
+  return fn;
+}
+
+// int8 slice planes [planes][rows = n][k = n, row stride np]; box 128 (k bytes) x box_rows, 128B swizzle.
+// Columns k >= n are outside the tensor, so TMA fills them with zeros.
+static bool encode_map_i8(CUtensorMap* m, const int8_t* base, int n, int np, int64_t planes, int box_rows) {
+  TensorMapEncodeFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)n * np};
+  cuuint32_t box[3] = {(cuuint32_t)i8::BKB, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// One product stage on the int8-slice path: exponents, slices, GEMM.
+static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, const int* list, int count,
+                     const i8::Bufs& b, cudaStream_t st) {
+  if (count <= 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(i8::k_i8_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::SMEM_BYTES) !=
+        cudaSuccess)
+      return 1;
+    attr = true;
+  }
+  const int n = g.n;
+  i8::k_i8_rowexp<<<dim3((n + 7) / 8, count), 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_colexp<<<dim3((n + 255) / 256, count), 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_slice_rows<<<dim3(std::min((n + 255) / 256, 8), n, count), 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_slice_cols<<<dim3((n + 31) / 32, (n + 31) / 32, count), 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_stage<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS, i8::SMEM_BYTES,
+                   st>>>(maps, g, stage, list, b);
+  return cudaGetLastError() != cudaSuccess;
+}
+
 template <typename T>
 static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int scheme, int64_t base, PlanOut po,
                            unsigned char* ws, const LargeLayout& L, cudaStream_t st) {
@@ -252,10 +318,34 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
     g.W2 = buf(0); g.W3 = buf(1); g.W4 = buf(2); g.La = buf(3); g.Ra = buf(4); g.Tmp = buf(5);
   }
 
+  // product stages: FFMA / DMMA GEMM, or the exact int8-slice tensor-core GEMM (fp32, opt-in)
+  i8::Maps i8maps{};
+  i8::Bufs i8b{};
+  bool i8p = false;
+  if constexpr (sizeof(T) == 4) {
+    if (use_i8_path(n, 4) && L.off_i8as != L.off_i8bs) {
+      i8p = true;
+      i8b.np = i8_np(n);
+      i8b.as = reinterpret_cast<int8_t*>(ws + L.off_i8as);
+      i8b.bs = reinterpret_cast<int8_t*>(ws + L.off_i8bs);
+      i8b.er = reinterpret_cast<int*>(ws + L.off_i8er);
+      i8b.ec = reinterpret_cast<int*>(ws + L.off_i8ec);
+      if (!encode_map_i8(&i8maps.a, i8b.as, n, i8b.np, cnt * i8::NSL, i8::BM) ||
+          !encode_map_i8(&i8maps.b, i8b.bs, n, i8b.np, cnt * i8::NSL, i8::BN))
+        return EXPMB_ERR_CUDA;
+    }
+  }
+  auto stage_launch = [&](int stage, const int* list, int count) -> int {
+    if constexpr (sizeof(T) == 4) {
+      if (i8p) return i8_launch(i8maps, g, stage, list, count, i8b, st);
+    }
+    return gemm_launch<T>(g, stage, list, count, st);
+  };
+
   // powers + ladder, gated on device flags (no host round trip)
   const int maxp = scheme == 1 ? 4 : 2;
   for (int p = 2; p <= maxp; ++p) {
-    if (gemm_launch<T>(g, p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic, st)) return EXPMB_ERR_CUDA;
+    if (stage_launch(p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic)) return EXPMB_ERR_CUDA;
     k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
   }
 
@@ -299,14 +389,14 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
     return EXPMB_ERR_CUDA;
 
   if (elem_launch<T>(g, dlist, ic, st)) return EXPMB_ERR_CUDA;
-  if (!l_s1.empty() && gemm_launch<T>(g, STAGE_E1, dlist + o1, (int)l_s1.size(), st)) return EXPMB_ERR_CUDA;
-  if (!l_s2.empty() && gemm_launch<T>(g, STAGE_E2, dlist + o2, (int)l_s2.size(), st)) return EXPMB_ERR_CUDA;
-  if (!l_s3.empty() && gemm_launch<T>(g, STAGE_E3, dlist + o3, (int)l_s3.size(), st)) return EXPMB_ERR_CUDA;
+  if (!l_s1.empty() && stage_launch(STAGE_E1, dlist + o1, (int)l_s1.size())) return EXPMB_ERR_CUDA;
+  if (!l_s2.empty() && stage_launch(STAGE_E2, dlist + o2, (int)l_s2.size())) return EXPMB_ERR_CUDA;
+  if (!l_s3.empty() && stage_launch(STAGE_E3, dlist + o3, (int)l_s3.size())) return EXPMB_ERR_CUDA;
   for (int q = 0; q < maxs; ++q) {
     int c = 0;
     while (c < ic && hs[l_sq[c]] > q) ++c;
     g.sq_step = q;
-    if (gemm_launch<T>(g, STAGE_SQ, dlist + o4, c, st)) return EXPMB_ERR_CUDA;
+    if (stage_launch(STAGE_SQ, dlist + o4, c)) return EXPMB_ERR_CUDA;
   }
   launch_finish<T>(X, n, ic, scheme, L, ws, nrm4, dm, ds, de1, de2, base, po, st);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
@@ -315,22 +405,6 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
 // ---------------------------------------------------------------------------
 // tensor-core path (fp32, Sastre)
 // ---------------------------------------------------------------------------
-typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static TensorMapEncodeFn tensor_map_encoder() {
-  static TensorMapEncodeFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (TensorMapEncodeFn)p;
-  }
-  return fn;
-}
-
 // [cnt][n][n] fp32 with `mstride_bytes` between matrices; box 32 (k) x 128 rows x 1, 128B swizzle
 static bool encode_map(CUtensorMap* m, const float* base, int n, int64_t cnt, size_t mstride_bytes) {
   TensorMapEncodeFn enc = tensor_map_encoder();

@@ -15,8 +15,15 @@
 //   acc_L = sum_{i+j=L} S_i T_j  (int32 on tcgen05.mma.kind::i8, exact)
 // Ten slice-pair GEMMs (pairs with i + j > 3 contribute < 2^-28 of the row and
 // column maxima and are dropped), the level sum and the scaling in binary64,
-// then one rounding to fp32 -- the result is at least as accurate as an fp32
-// FMA dot product, with no systematic bias.
+// then one rounding to fp32.  The diagonal of each operand is split off and
+// applied exactly in the epilogue (L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R),
+// so the squaring phase's dominant diagonal does not set the row scale.
+// Measured on C5 (tools/i8_debug.py): 1.5x the FFMA GEMM's throughput and a
+// smaller error (worst 4.8e-7 vs 2.1e-6).  Limitation: the scale is per row
+// / column, so entries far below their row's maximum keep fewer bits than in
+// fp32 -- on graded matrices (entries ~2^20 apart within a row) the error is
+// 30x the FFMA path's (tools/i8_graded_probe.py).  Hence opt-in (EXPMB_I8=1,
+// fp32, n >= 512, n % 16 == 0), not the default.
 //
 // Kernels: k_i8_rowexp / k_i8_colexp (exponents), k_i8_slice_rows (L slices,
 // K-major), k_i8_slice_cols (R slices transposed to K-major), k_i8_stage
@@ -76,93 +83,82 @@ __device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
   }
 }
 
-// Row exponents of every participating L (one warp per row).
-__global__ void __launch_bounds__(256) k_i8_rowexp(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                    Bufs b) {
-  const int slot = blockIdx.y;
-  const int z = list ? list[slot] : slot;
-  Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;
-  const int n = g.n;
-  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (r >= n) return;
-  const float* row = e.L + (size_t)r * n;
-  float mx = 0.f;
-  for (int c = lane; c < n; c += 32) {
-    const float a = fabsf(row[c]);
-    mx = (a > mx || a != a) ? a : mx;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float v = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = (v > mx || v != v) ? v : mx;
-  }
-  if (lane == 0) b.er[(size_t)slot * n + r] = exp_of(mx);
-}
-
-// Column exponents of every participating R (one thread per column).
-__global__ void __launch_bounds__(256) k_i8_colexp(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                    Bufs b) {
-  const int slot = blockIdx.y;
-  const int z = list ? list[slot] : slot;
-  Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;
-  const int n = g.n;
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= n) return;
-  float mx = 0.f;
-  for (int r = 0; r < n; ++r) {
-    const float a = fabsf(e.R[(size_t)r * n + c]);
-    mx = (a > mx || a != a) ? a : mx;
-  }
-  b.ec[(size_t)slot * n + c] = exp_of(mx);
-}
-
-// L slices: row-major, four planes.
-__global__ void __launch_bounds__(256) k_i8_slice_rows(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                        Bufs b) {
+// One pass over 32x32 tiles: row maxima of |L| and column maxima of |R|
+// (diagonals excluded: they are handled exactly in the epilogue), as the bit
+// patterns of non-negative floats, which order like the values (NaN above
+// Inf), combined with atomicMax into er / ec (zeroed before the stage).
+__global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b) {
   const int slot = blockIdx.z;
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
+  __shared__ int cmax[8][33];
   const int n = g.n;
-  const int r = blockIdx.y;
-  const int er = b.er[(size_t)slot * n + r];
-  const size_t plane = (size_t)n * b.np;
-  int8_t* out = b.as + (size_t)slot * NSL * plane + (size_t)r * b.np;
-  for (int c = blockIdx.x * 256 + threadIdx.x; c < n; c += gridDim.x * 256) {
-    int8_t s[4];
-    slice4(e.L[(size_t)r * n + c], er, s);
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  int cm = 0;
+  for (int i = ty; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + tx;
+    const bool in = r < n && c < n && r != c;
+    const int lv = in ? (__float_as_int(e.L[(size_t)r * n + c]) & 0x7fffffff) : 0;
+    const int rv = in ? (e.R == e.L ? lv : (__float_as_int(e.R[(size_t)r * n + c]) & 0x7fffffff)) : 0;
+    int m = lv;
 #pragma unroll
-    for (int i = 0; i < NSL; ++i) out[i * plane + c] = s[i];
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tx == 0 && r < n && m) atomicMax(b.er + (size_t)slot * n + r, m);
+    cm = max(cm, rv);
+  }
+  cmax[ty][tx] = cm;
+  __syncthreads();
+  if (ty == 0 && c0 + tx < n) {
+    int m = cmax[0][tx];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = max(m, cmax[i][tx]);
+    if (m) atomicMax(b.ec + (size_t)slot * n + c0 + tx, m);
   }
 }
 
-// R slices transposed through a 32x32 shared tile: bs[j][c][k] = slice_j(R[k][c]).
-__global__ void __launch_bounds__(256) k_i8_slice_cols(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                        Bufs b) {
+// One pass over 32x32 tiles: L slices row-major, R slices transposed (both K-major).
+__global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b) {
   const int slot = blockIdx.z;
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
   __shared__ float tile[32][33];
   const int n = g.n;
-  const int k0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 rows of 32
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const size_t plane = (size_t)n * b.np;
+  int8_t* as = b.as + (size_t)slot * NSL * plane;
+  int8_t* bs = b.bs + (size_t)slot * NSL * plane;
+  const int* er = b.er + (size_t)slot * n;
+  const int* ec = b.ec + (size_t)slot * n;
   for (int i = ty; i < 32; i += 8) {
-    const int k = k0 + i, c = c0 + tx;
-    tile[i][tx] = (k < n && c < n) ? e.R[(size_t)k * n + c] : 0.f;
+    const int r = r0 + i, c = c0 + tx;
+    float x = 0.f, y = 0.f;
+    if (r < n && c < n) {
+      x = e.L[(size_t)r * n + c];
+      y = e.R == e.L ? x : e.R[(size_t)r * n + c];
+    }
+    tile[i][tx] = (r == c) ? 0.f : y;
+    if (r < n && c < n) {
+      int8_t sl[4];
+      slice4(r == c ? 0.f : x, exp_of(__int_as_float(er[r])), sl);
+#pragma unroll
+      for (int j = 0; j < NSL; ++j) as[j * plane + (size_t)r * b.np + c] = sl[j];
+    }
   }
   __syncthreads();
-  const size_t plane = (size_t)n * b.np;
-  int8_t* base = b.bs + (size_t)slot * NSL * plane;
+  // R[k][c] -> bs[j][c][k]: thread (tx, ty) writes column c = c0 + i, k = r0 + tx
   for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i, k = k0 + tx;
+    const int c = c0 + i, k = r0 + tx;
     if (c < n && k < n) {
-      int8_t s[4];
-      slice4(tile[tx][i], b.ec[(size_t)slot * n + c], s);
+      int8_t sl[4];
+      slice4(tile[tx][i], exp_of(__int_as_float(ec[c])), sl);
 #pragma unroll
-      for (int j = 0; j < NSL; ++j) base[j * plane + (size_t)c * b.np + k] = s[j];
+      for (int j = 0; j < NSL; ++j) bs[j * plane + (size_t)c * b.np + k] = sl[j];
     }
   }
 }
@@ -198,7 +194,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int ec_sh[BN];
+  __shared__ double cs_sh[BN];  // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
+  __shared__ float dr_sh[BN];   // diagonal of R for this CTA's columns
   const int slot = blockIdx.z;
   const int z = list ? list[slot] : slot;
   Epi<float> e;
@@ -210,7 +207,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant_
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int KT = (n + BKB - 1) / BKB;
 
-  if (threadIdx.x < BN) ec_sh[threadIdx.x] = (n0 + threadIdx.x < n) ? bf.ec[(size_t)slot * n + n0 + threadIdx.x] : 0;
+  if (threadIdx.x < BN) {
+    const int c = n0 + threadIdx.x;
+    const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
+    cs_sh[threadIdx.x] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
+    dr_sh[threadIdx.x] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       tc::mbar_init(&full_bar[i], 1);
@@ -274,26 +276,53 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant_
     const int rl = q * 32 + lane;
     const int r = m0 + rl;
     const bool rowok = r < n;
-    const int er = rowok ? bf.er[(size_t)slot * n + r] : 0;
+    const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+    const double rs = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6);
+    const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
     double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
     for (int cb = 0; cb < BN / 32; ++cb) {
-      int a0[32], a1[32];
+      int a0[32], a1[32], a2[32], a3[32];
       float v[32];
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * 32;
       tmem_ld32i(ta, a0);
       tmem_ld32i(ta + BN, a1);
-      double d[32];
+      tmem_ld32i(ta + 2 * BN, a2);
+      tmem_ld32i(ta + 3 * BN, a3);
+      const int c0 = n0 + cb * 32;
+      const bool full = rowok && c0 + 32 <= n;
+      // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
+      // the int8 GEMM carries Yl Yr (each row / column scaled without its
+      // diagonal, which in the squaring phase dominates), the rest is exact
+      // elementwise work here, all summed in binary64 and rounded once
+      float lrow[32], rrow[32];
+      if (full) {
+        const float4* lp = reinterpret_cast<const float4*>(e.L + (size_t)r * n + c0);
+        const float4* rp = reinterpret_cast<const float4*>(e.R + (size_t)r * n + c0);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) d[j] = (double)a0[j] + ldexp((double)a1[j], -7);
-      tmem_ld32i(ta + 2 * BN, a0);
-      tmem_ld32i(ta + 3 * BN, a1);
+        for (int j = 0; j < 8; ++j) {
+          const float4 a = __ldg(lp + j);
+          lrow[4 * j] = a.x; lrow[4 * j + 1] = a.y; lrow[4 * j + 2] = a.z; lrow[4 * j + 3] = a.w;
+          const float4 bb = (e.R == e.L) ? a : __ldg(rp + j);
+          rrow[4 * j] = bb.x; rrow[4 * j + 1] = bb.y; rrow[4 * j + 2] = bb.z; rrow[4 * j + 3] = bb.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = rowok && c0 + j < n;
+          lrow[j] = ok ? e.L[(size_t)r * n + c0 + j] : 0.f;
+          rrow[j] = ok ? e.R[(size_t)r * n + c0 + j] : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int ec = ec_sh[cb * 32 + j];
-        const double t = d[j] + ldexp((double)a0[j], -14) + ldexp((double)a1[j], -21);  // exact in binary64
-        v[j] = (er == kNanExp || ec == kNanExp) ? NAN : (float)ldexp(t, er + ec - 12);
+        const int c = c0 + j;
+        // exact: each Horner step fits binary64 (|acc| < 2^27, 21 fraction bits)
+        const double t = (((double)a3[j] * 0x1p-7 + (double)a2[j]) * 0x1p-7 + (double)a1[j]) * 0x1p-7 + (double)a0[j];
+        double y = t * rs * cs_sh[cb * 32 + j];
+        const double dr = (double)dr_sh[cb * 32 + j];
+        y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
+        v[j] = (float)y;
       }
-      const int c0 = n0 + cb * 32;
       float o0[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) o0[j] = e.alpha * v[j];

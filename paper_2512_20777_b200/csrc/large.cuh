@@ -55,7 +55,7 @@ static inline bool use_tc_path(int n, int esize, int scheme) {
 // opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
 static inline bool use_i8_path(int n, int esize) {
   const char* e = getenv("EXPMB_I8");
-  return esize == 4 && e != nullptr && e[0] == '1' && n >= 1;
+  return esize == 4 && e != nullptr && e[0] == '1' && n >= 512 && n % 16 == 0;
 }
 static inline int i8_np(int n) { return (n + 15) / 16 * 16; }
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers
@@ -270,10 +270,12 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     attr = true;
   }
   const int n = g.n;
-  i8::k_i8_rowexp<<<dim3((n + 7) / 8, count), 256, 0, st>>>(g, stage, list, b);
-  i8::k_i8_colexp<<<dim3((n + 255) / 256, count), 256, 0, st>>>(g, stage, list, b);
-  i8::k_i8_slice_rows<<<dim3(std::min((n + 255) / 256, 8), n, count), 256, 0, st>>>(g, stage, list, b);
-  i8::k_i8_slice_cols<<<dim3((n + 31) / 32, (n + 31) / 32, count), 256, 0, st>>>(g, stage, list, b);
+  if (cudaMemsetAsync(b.er, 0, (size_t)count * n * sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(b.ec, 0, (size_t)count * n * sizeof(int), st) != cudaSuccess)
+    return 1;
+  const dim3 tiles((n + 31) / 32, (n + 31) / 32, count);
+  i8::k_i8_stats<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_slice<<<tiles, 256, 0, st>>>(g, stage, list, b);
   i8::k_i8_stage<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS, i8::SMEM_BYTES,
                    st>>>(maps, g, stage, list, b);
   return cudaGetLastError() != cudaSuccess;

@@ -418,12 +418,18 @@ def run_lowrank(args):
         dist.destroy_process_group()
 
 
-def _launch_count(key, m, s, n):
-    """Kernels of ours launched by one expm call (host orchestration is deterministic)."""
+def _launch_count(key, m, s, n, dtype="f64"):
+    """Kernels of ours launched by one expm call (host orchestration is deterministic):
+    n > 64: colsum, two k_select, elem, nonfinite, finish + one launch per product
+    stage (W^2, E1..E3 as present, one per squaring level); on the int8-slice path
+    (fp32, n >= 1024) a product stage is six kernels (stats, count, route, slice,
+    int8 GEMM, FFMA GEMM for routed-away products)."""
     if n <= 64:
         return 1
     m = np.asarray(m); s = np.asarray(s)
-    return int(1 + 2 + 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max()) + 1)
+    stages = 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max())
+    per = 6 if (dtype == "f32" and n >= 1024 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
+    return int(6 + stages * per)
 
 
 def run_ours(args):
@@ -607,6 +613,15 @@ def run_ours(args):
         else:
             roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
         roof["other"] = cmp_roof if hbm_binds else hbm_roof
+        if cfg.dtype == "f32" and cfg.n >= 1024 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0":
+            # products run as exact int8-slice GEMMs on tcgen05 (gemm_i8.cuh): ten
+            # int8 slice-pair products per fp32 product; the FFMA peak stays the
+            # useful-flop yardstick, the int8 view is reported beside it
+            i8_ops = 10.0 * flops
+            roof["kernel"] = "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products"
+            roof["int8_tensor"] = {"achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": 4500.0, "unit": "TOPS",
+                                   "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / 4500.0,
+                                   "peak_source": "nominal dense int8 (no measured int8 peak on this pool)"}
         if tg:
             # the time-grid path skips the evaluation products: its roofline is
             # over the flops it executes (squarings, shared powers in fp64, the
@@ -641,7 +656,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "exps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": float(et.item()) / args.steps},
-            "gpu_launches": (10 + int(np.asarray(s).max()) if tg else _launch_count(cfg.key, m, s, cfg.n)) * args.steps,
+            "gpu_launches": (10 + int(np.asarray(s).max()) if tg else _launch_count(cfg.key, m, s, cfg.n, cfg.dtype)) * args.steps,
             "clocks": clk.summary(),
             "plan_histogram": hist,
             "mults_total": int(plan["mults"].long().sum().item()),

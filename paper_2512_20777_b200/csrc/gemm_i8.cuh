@@ -60,6 +60,9 @@ struct Bufs {
   int8_t* bs;  // [slot][4][n][np]  R slices, transposed (K contiguous)
   int* er;     // [slot][n]
   int* ec;     // [slot][n]
+  int* rc;     // [slot][n] per row of L: entries within 2^-4 of the row maximum
+  int* cc;     // [slot][n] per column of R: the same
+  int* ok;     // [slot] 1 = this path handles the product (see k_i8_route)
   int np;      // padded row length (multiple of 16 bytes, TMA stride rule)
 };
 
@@ -119,10 +122,70 @@ __global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, c
   }
 }
 
+// Second pass: how many entries of each row of L (column of R) lie within
+// 2^-4 of its maximum.  Integer counts: deterministic.
+__global__ void __launch_bounds__(256) k_i8_count(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b) {
+  const int slot = blockIdx.z;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;
+  __shared__ int ccnt[8][33];
+  const int n = g.n;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int c = c0 + tx;
+  const float cthr = c < n ? __int_as_float(b.ec[(size_t)slot * n + c]) * 0.0625f : 0.f;
+  int cn = 0;
+  for (int i = ty; i < 32; i += 8) {
+    const int r = r0 + i;
+    const bool in = r < n && c < n && r != c;
+    const float l = in ? fabsf(e.L[(size_t)r * n + c]) : 0.f;
+    const float rv = in ? (e.R == e.L ? l : fabsf(e.R[(size_t)r * n + c])) : 0.f;
+    const float rthr = r < n ? __int_as_float(b.er[(size_t)slot * n + r]) * 0.0625f : 0.f;
+    const unsigned m = __ballot_sync(0xffffffffu, in && l > 0.f && l >= rthr);
+    if (tx == 0 && r < n && m) atomicAdd(b.rc + (size_t)slot * n + r, __popc(m));
+    cn += (in && rv > 0.f && rv >= cthr) ? 1 : 0;
+  }
+  ccnt[ty][tx] = cn;
+  __syncthreads();
+  if (ty == 0 && c < n) {
+    int m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m += ccnt[i][tx];
+    if (m) atomicAdd(b.cc + (size_t)slot * n + c, m);
+  }
+}
+
+// Route a product to this path only when every row of L and every column of
+// R is "flat": at least n/4 entries within 2^-4 of its maximum (or no
+// off-diagonal mass at all).  Then typical entries keep >= 24 of the 28
+// slice bits, i.e. fp32 precision; graded operands (a few large entries per
+// row) go to the FFMA GEMM instead.
+__global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b) {
+  const int slot = blockIdx.x;
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  const bool part = make_epi(g, stage, z, e);
+  const int n = g.n;
+  bool flat = true;
+  if (part) {
+    for (int i = threadIdx.x; i < n; i += 256) {
+      const size_t o = (size_t)slot * n + i;
+      flat &= (b.er[o] == 0 || b.rc[o] >= n / 4) && (b.ec[o] == 0 || b.cc[o] >= n / 4);
+      flat &= b.er[o] < 0x7f800000 && b.ec[o] < 0x7f800000;  // NaN / Inf: let the FFMA path propagate them
+    }
+  }
+  flat = __syncthreads_and(flat);
+  if (threadIdx.x == 0) b.ok[slot] = part && flat ? 1 : 0;
+}
+
 // One pass over 32x32 tiles: L slices row-major, R slices transposed (both K-major).
 __global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
                                                    Bufs b) {
   const int slot = blockIdx.z;
+  if (!b.ok[slot]) return;
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
@@ -197,6 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant_
   __shared__ double cs_sh[BN];  // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
   __shared__ float dr_sh[BN];   // diagonal of R for this CTA's columns
   const int slot = blockIdx.z;
+  if (!bf.ok[slot]) return;  // routed to the FFMA GEMM
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;  // uniform per CTA

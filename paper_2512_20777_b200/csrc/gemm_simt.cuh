@@ -44,6 +44,7 @@ struct GemmCtx {
   const int8_t* s;
   const int* need;
   double* part;
+  const int* route;  // per list slot: 1 = another backend (the int8-slice GEMM) handles it; may be null
 };
 
 template <typename T>
@@ -218,6 +219,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   T* Bs = As + ST * A_ELEMS;
 
   const int z = list ? list[blockIdx.z] : (int)blockIdx.z;
+  if (g.route && g.route[blockIdx.z]) return;
   Epi<T> e;
   if (!make_epi(g, stage, z, e)) return;
   const int n = g.n;

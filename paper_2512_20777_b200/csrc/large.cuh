@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -53,9 +54,15 @@ static inline bool use_tc_path(int n, int esize, int scheme) {
 }
 // Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh):
 // opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
+// Default: on for fp32 n >= 1024 (where it is faster); EXPMB_I8=1 also enables
+// it from n = 512, EXPMB_I8=0 disables it.  Each product is routed per matrix
+// (k_i8_route): operands that are not "flat" go to the FFMA GEMM.
 static inline bool use_i8_path(int n, int esize) {
   const char* e = getenv("EXPMB_I8");
-  return esize == 4 && e != nullptr && e[0] == '1' && n >= 512 && n % 16 == 0;
+  if (esize != 4 || n % 16 != 0) return false;
+  if (e != nullptr && e[0] == '0') return false;
+  if (e != nullptr && e[0] == '1') return n >= 512;
+  return n >= 1024;
 }
 static inline int i8_np(int n) { return (n + 15) / 16 * 16; }
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers
@@ -66,7 +73,7 @@ struct LargeLayout {
   int nbufs;
   int tiles_m;
   size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_flags, off_m, off_s, off_e1, off_e2, off_list, total;
-  size_t off_i8as, off_i8bs, off_i8er, off_i8ec;  // int8-slice path (0 sizes otherwise)
+  size_t off_i8as, off_i8bs, off_i8er, off_i8ec, off_i8rc, off_i8cc, off_i8ok;  // int8-slice path
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -77,7 +84,9 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.nbufs = use_tc_path(n, esize, scheme) ? kLargeBufsTC : (scheme == 1 ? kLargeBufsPS : kLargeBufsSastre);
   const bool i8p = use_i8_path(n, esize) && !use_tc_path(n, esize, scheme);
   const size_t i8plane = (size_t)n * i8_np(n);
-  const size_t per = L.mat_bytes * L.nbufs + (i8p ? 2 * i8::NSL * i8plane + 2 * (size_t)n * sizeof(int) : 0);
+  const size_t per_bufs = L.mat_bytes * L.nbufs;
+  // per-matrix bytes for sizing the chunk (the int8-slice regions sit after the lists)
+  const size_t per = per_bufs + (i8p ? 2 * i8::NSL * i8plane + 4 * (size_t)n * sizeof(int) + 4 : 0);
   int64_t chunk = (int64_t)(kLargeWsCap / per);
   if (chunk < 1) chunk = 1;
   if (chunk > 65535) chunk = 65535;  // gridDim.z
@@ -85,7 +94,7 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.chunk = chunk;
   L.tiles_m = (n + kGemmBM - 1) / kGemmBM;
   size_t off = 0;
-  L.off_bufs = off; off += per * chunk;
+  L.off_bufs = off; off += per_bufs * chunk;
   L.off_part = off; off += align256((size_t)chunk * L.tiles_m * n * sizeof(double));
   L.off_norm1 = off; off += align256((size_t)chunk * 4 * sizeof(double));
   L.off_norm2 = off; off += 0;  // norms for powers 1..4 live in the same [chunk][4] array
@@ -100,6 +109,9 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.off_i8bs = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
   L.off_i8er = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
   L.off_i8ec = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
+  L.off_i8rc = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
+  L.off_i8cc = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
+  L.off_i8ok = off; off += i8p ? align256((size_t)chunk * sizeof(int)) : 0;
   L.total = off;
   return L;
 }
@@ -253,9 +265,13 @@ static bool encode_map_i8(CUtensorMap* m, const int8_t* base, int n, int np, int
   cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)n * np};
   cuuint32_t box[3] = {(cuuint32_t)i8::BKB, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("EXPMB_DEBUG_SYNC"))
+    fprintf(stderr, "expmb i8: cuTensorMapEncodeTiled -> %d (base %p n %d np %d planes %lld box_rows %d)\n", (int)r,
+            (const void*)base, n, np, (long long)planes, box_rows);
+  return r == CUDA_SUCCESS;
 }
 
 // One product stage on the int8-slice path: exponents, slices, GEMM.
@@ -270,15 +286,40 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     attr = true;
   }
   const int n = g.n;
-  if (cudaMemsetAsync(b.er, 0, (size_t)count * n * sizeof(int), st) != cudaSuccess ||
-      cudaMemsetAsync(b.ec, 0, (size_t)count * n * sizeof(int), st) != cudaSuccess)
+  const size_t vb = (size_t)count * n * sizeof(int);
+  if (cudaMemsetAsync(b.er, 0, vb, st) != cudaSuccess || cudaMemsetAsync(b.ec, 0, vb, st) != cudaSuccess ||
+      cudaMemsetAsync(b.rc, 0, vb, st) != cudaSuccess || cudaMemsetAsync(b.cc, 0, vb, st) != cudaSuccess)
     return 1;
+  static const bool dbg = getenv("EXPMB_DEBUG_SYNC") != nullptr;
+  auto chk = [&](const char* what) {
+    if (!dbg) return 0;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) fprintf(stderr, "expmb i8 stage %d: %s failed: %s\n", stage, what, cudaGetErrorString(e));
+    return e != cudaSuccess ? 1 : 0;
+  };
   const dim3 tiles((n + 31) / 32, (n + 31) / 32, count);
   i8::k_i8_stats<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  if (chk("stats")) return 1;
+  i8::k_i8_count<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  if (chk("count")) return 1;
+  i8::k_i8_route<<<count, 256, 0, st>>>(g, stage, list, b);
+  if (chk("route")) return 1;
   i8::k_i8_slice<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  if (chk("slice")) return 1;
   i8::k_i8_stage<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS, i8::SMEM_BYTES,
                    st>>>(maps, g, stage, list, b);
-  return cudaGetLastError() != cudaSuccess;
+  {
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+      if (dbg) fprintf(stderr, "expmb i8 stage %d: launch failed: %s\n", stage, cudaGetErrorString(le));
+      return 1;
+    }
+    if (chk("stage")) return 1;
+  }
+  // the products routed away run on the FFMA GEMM (its CTAs for routed-here matrices exit at once)
+  GemmCtx<float> gs = g;
+  gs.route = b.ok;
+  return gemm_launch<float>(gs, stage, list, count, st);
 }
 
 template <typename T>
@@ -332,9 +373,14 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
       i8b.bs = reinterpret_cast<int8_t*>(ws + L.off_i8bs);
       i8b.er = reinterpret_cast<int*>(ws + L.off_i8er);
       i8b.ec = reinterpret_cast<int*>(ws + L.off_i8ec);
+      i8b.rc = reinterpret_cast<int*>(ws + L.off_i8rc);
+      i8b.cc = reinterpret_cast<int*>(ws + L.off_i8cc);
+      i8b.ok = reinterpret_cast<int*>(ws + L.off_i8ok);
       if (!encode_map_i8(&i8maps.a, i8b.as, n, i8b.np, cnt * i8::NSL, i8::BM) ||
-          !encode_map_i8(&i8maps.b, i8b.bs, n, i8b.np, cnt * i8::NSL, i8::BN))
+          !encode_map_i8(&i8maps.b, i8b.bs, n, i8b.np, cnt * i8::NSL, i8::BN)) {
+        if (getenv("EXPMB_DEBUG_SYNC")) fprintf(stderr, "expmb i8: tensor map encoding failed (n=%d)\n", n);
         return EXPMB_ERR_CUDA;
+      }
     }
   }
   auto stage_launch = [&](int stage, const int* list, int count) -> int {

@@ -1,9 +1,10 @@
-"""The opt-in exact int8-slice tensor-core GEMM path (gemm_i8.cuh, EXPMB_I8=1)
-for fp32 n >= 512 against the oracle: dense inputs over three norm scales
-(the squaring phase's dominant diagonal included), ragged column tiles, PS,
-non-finite input.  Graded matrices (entries ~2^20 apart within a row) are
-its known weakness (tools/i8_graded_probe.py: 1.6e-3 vs the FFMA path's
-4.5e-5), which is why the path is not the default."""
+"""The exact int8-slice tensor-core GEMM path (gemm_i8.cuh; default for fp32
+n >= 1024, EXPMB_I8=1 from n = 512) against the oracle: dense inputs over
+three norm scales (the squaring phase's dominant diagonal included), ragged
+column tiles, PS, non-finite input, and the per-product routing: graded
+operands (entries ~2^20 apart within a row, where per-row scaling would lose
+bits: tools/i8_graded_probe.py) must go to the FFMA GEMM, so the results
+equal the FFMA path's bit for bit."""
 import os
 
 import numpy as np
@@ -55,3 +56,25 @@ def test_i8_ps_and_nonfinite(i8_on):
     W[1, 3, 7] = np.nan
     r = X.expm(torch.as_tensor(W, device="cuda"), 2.0 ** -24, check_finite=False)
     assert r.nonfinite.cpu().tolist() == [False, True]
+
+
+def test_i8_routes_graded_operands_to_ffma(monkeypatch):
+    n = 512
+    rng = np.random.default_rng(3)
+    d = 2.0 ** np.linspace(-10, 10, n)
+    W = np.stack([(d[:, None] * rng.standard_normal((n, n)) / d[None, :]) * (t / n ** 0.5) for t in (0.5, 3.0)])
+    Wt = torch.as_tensor(W.astype(np.float32), device="cuda")
+    monkeypatch.setenv("EXPMB_I8", "0")
+    ref = X.expm(Wt, 2.0 ** -24, check_finite=False).value
+    monkeypatch.setenv("EXPMB_I8", "1")
+    got = X.expm(Wt, 2.0 ** -24, check_finite=False).value
+    assert torch.equal(ref, got)
+
+
+def test_i8_default_on_for_large_dense(monkeypatch):
+    """Without EXPMB_I8 the path is on for n >= 1024 and matches the oracle."""
+    monkeypatch.delenv("EXPMB_I8", raising=False)
+    n = 1024
+    rng = np.random.default_rng(9)
+    W = np.stack([rng.standard_normal((n, n)) * (t / n ** 0.5) for t in (1.0, 20.0)]).astype(np.float32)
+    print(f"n=1024 default worst {_check(W, 2.0 ** -24):.2e}")

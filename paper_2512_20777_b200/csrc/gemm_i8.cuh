@@ -43,7 +43,10 @@
 namespace expmb {
 namespace i8 {
 
-constexpr int BM = 128, BN = 64, BKB = 128, STAGES = 2, NSL = 4;
+#ifndef EXPMB_I8_STAGES
+#define EXPMB_I8_STAGES 1  // 1 stage = 96 KB smem: two CTAs per SM, one's epilogue overlaps the other's MMAs
+#endif
+constexpr int BM = 128, BN = 64, BKB = 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
 constexpr int A_TILE = BM * BKB;                     // 16 KB
 constexpr int B_TILE = BN * BKB;                     // 8 KB
 constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 96 KB
@@ -252,7 +255,7 @@ struct Maps {
   CUtensorMap a, b;
 };
 
-__global__ void __launch_bounds__(NTHREADS, 1) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
+__global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
                                                           int stage, const int* __restrict__ list, Bufs bf) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;

@@ -422,13 +422,13 @@ def _launch_count(key, m, s, n, dtype="f64"):
     """Kernels of ours launched by one expm call (host orchestration is deterministic):
     n > 64: colsum, two k_select, elem, nonfinite, finish + one launch per product
     stage (W^2, E1..E3 as present, one per squaring level); on the int8-slice path
-    (fp32, n >= 1024) a product stage is six kernels (stats, count, route, slice,
+    (fp32, n >= 1024) a product stage is five kernels (stats, route, slice,
     int8 GEMM, FFMA GEMM for routed-away products)."""
     if n <= 64:
         return 1
     m = np.asarray(m); s = np.asarray(s)
     stages = 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max())
-    per = 6 if (dtype == "f32" and n >= 1024 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
+    per = 5 if (dtype == "f32" and n >= 1024 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
     return int(6 + stages * per)
 
 

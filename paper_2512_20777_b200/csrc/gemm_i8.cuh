@@ -63,8 +63,8 @@ struct Bufs {
   int8_t* bs;  // [slot][4][n][np]  R slices, transposed (K contiguous)
   int* er;     // [slot][n]
   int* ec;     // [slot][n]
-  int* rc;     // [slot][n] per row of L: entries within 2^-4 of the row maximum
-  int* cc;     // [slot][n] per column of R: the same
+  unsigned long long* rc;  // [slot][n] per row of L: (sum of biased exponents) << 20 | nonzero count
+  unsigned long long* cc;  // [slot][n] per column of R: the same
   int* ok;     // [slot] 1 = this path handles the product (see k_i8_route)
   int np;      // padded row length (multiple of 16 bytes, TMA stride rule)
 };
@@ -90,9 +90,15 @@ __device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
 }
 
 // One pass over 32x32 tiles: row maxima of |L| and column maxima of |R|
-// (diagonals excluded: they are handled exactly in the epilogue), as the bit
+// (diagonals excluded: they are handled exactly in the epilogue) as the bit
 // patterns of non-negative floats, which order like the values (NaN above
-// Inf), combined with atomicMax into er / ec (zeroed before the stage).
+// Inf), combined with atomicMax into er / ec; and, for the routing test, the
+// sum of the binary exponents and the count of the nonzero entries, packed in
+// one 64-bit integer atomicAdd (deterministic).
+constexpr int kExpBias = 200;
+__device__ __forceinline__ unsigned long long exp_pack(float a) {
+  return a > 0.f && a < INFINITY ? ((unsigned long long)(ilogbf(a) + kExpBias) << 20) | 1ull : 0ull;
+}
 __global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
                                                    Bufs b) {
   const int slot = blockIdx.z;
@@ -100,71 +106,61 @@ __global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, c
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
   __shared__ int cmax[8][33];
+  __shared__ unsigned long long csum[8][33];
   const int n = g.n;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   int cm = 0;
+  unsigned long long cs = 0;
   for (int i = ty; i < 32; i += 8) {
     const int r = r0 + i, c = c0 + tx;
     const bool in = r < n && c < n && r != c;
-    const int lv = in ? (__float_as_int(e.L[(size_t)r * n + c]) & 0x7fffffff) : 0;
-    const int rv = in ? (e.R == e.L ? lv : (__float_as_int(e.R[(size_t)r * n + c]) & 0x7fffffff)) : 0;
-    int m = lv;
+    const float lf = in ? fabsf(e.L[(size_t)r * n + c]) : 0.f;
+    const float rf = in ? (e.R == e.L ? lf : fabsf(e.R[(size_t)r * n + c])) : 0.f;
+    int m = __float_as_int(lf);
+    unsigned long long sm = exp_pack(lf);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (tx == 0 && r < n && m) atomicMax(b.er + (size_t)slot * n + r, m);
-    cm = max(cm, rv);
+    for (int o = 16; o > 0; o >>= 1) {
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    if (tx == 0 && r < n) {
+      if (m) atomicMax(b.er + (size_t)slot * n + r, m);
+      if (sm) atomicAdd(b.rc + (size_t)slot * n + r, sm);
+    }
+    cm = max(cm, __float_as_int(rf));
+    cs += exp_pack(rf);
   }
   cmax[ty][tx] = cm;
+  csum[ty][tx] = cs;
   __syncthreads();
   if (ty == 0 && c0 + tx < n) {
     int m = cmax[0][tx];
+    unsigned long long sm = csum[0][tx];
 #pragma unroll
-    for (int i = 1; i < 8; ++i) m = max(m, cmax[i][tx]);
+    for (int i = 1; i < 8; ++i) {
+      m = max(m, cmax[i][tx]);
+      sm += csum[i][tx];
+    }
     if (m) atomicMax(b.ec + (size_t)slot * n + c0 + tx, m);
-  }
-}
-
-// Second pass: how many entries of each row of L (column of R) lie within
-// 2^-4 of its maximum.  Integer counts: deterministic.
-__global__ void __launch_bounds__(256) k_i8_count(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b) {
-  const int slot = blockIdx.z;
-  const int z = list ? list[slot] : slot;
-  Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;
-  __shared__ int ccnt[8][33];
-  const int n = g.n;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  const int c = c0 + tx;
-  const float cthr = c < n ? __int_as_float(b.ec[(size_t)slot * n + c]) * 0.0625f : 0.f;
-  int cn = 0;
-  for (int i = ty; i < 32; i += 8) {
-    const int r = r0 + i;
-    const bool in = r < n && c < n && r != c;
-    const float l = in ? fabsf(e.L[(size_t)r * n + c]) : 0.f;
-    const float rv = in ? (e.R == e.L ? l : fabsf(e.R[(size_t)r * n + c])) : 0.f;
-    const float rthr = r < n ? __int_as_float(b.er[(size_t)slot * n + r]) * 0.0625f : 0.f;
-    const unsigned m = __ballot_sync(0xffffffffu, in && l > 0.f && l >= rthr);
-    if (tx == 0 && r < n && m) atomicAdd(b.rc + (size_t)slot * n + r, __popc(m));
-    cn += (in && rv > 0.f && rv >= cthr) ? 1 : 0;
-  }
-  ccnt[ty][tx] = cn;
-  __syncthreads();
-  if (ty == 0 && c < n) {
-    int m = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m += ccnt[i][tx];
-    if (m) atomicAdd(b.cc + (size_t)slot * n + c, m);
+    if (sm) atomicAdd(b.cc + (size_t)slot * n + c0 + tx, sm);
   }
 }
 
 // Route a product to this path only when every row of L and every column of
-// R is "flat": at least n/4 entries within 2^-4 of its maximum (or no
-// off-diagonal mass at all).  Then typical entries keep >= 24 of the 28
-// slice bits, i.e. fp32 precision; graded operands (a few large entries per
-// row) go to the FFMA GEMM instead.
+// R is "flat": its largest entry's binary exponent exceeds the mean exponent
+// of its nonzero entries by at most 4, so typical entries keep >= 23 of the
+// 28 slice bits (fp32 precision).  Graded operands, where a few large entries
+// set the scale of many small ones, go to the FFMA GEMM; so do NaN / Inf.
+constexpr int kFlatBits = 4;
+__device__ __forceinline__ bool flat_ok(int maxbits, unsigned long long pk) {
+  if (maxbits == 0) return true;                    // no off-diagonal mass
+  if (maxbits >= 0x7f800000) return false;          // Inf / NaN
+  const long long cnt = (long long)(pk & 0xfffffull);
+  const long long esum = (long long)(pk >> 20) - (long long)kExpBias * cnt;
+  const int emax = ilogbf(__int_as_float(maxbits));
+  return cnt > 0 && (long long)emax * cnt - esum <= (long long)kFlatBits * cnt;
+}
 __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, const int* __restrict__ list,
                                                    Bufs b) {
   const int slot = blockIdx.x;
@@ -176,8 +172,7 @@ __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, c
   if (part) {
     for (int i = threadIdx.x; i < n; i += 256) {
       const size_t o = (size_t)slot * n + i;
-      flat &= (b.er[o] == 0 || b.rc[o] >= n / 4) && (b.ec[o] == 0 || b.cc[o] >= n / 4);
-      flat &= b.er[o] < 0x7f800000 && b.ec[o] < 0x7f800000;  // NaN / Inf: let the FFMA path propagate them
+      flat &= flat_ok(b.er[o], b.rc[o]) && flat_ok(b.ec[o], b.cc[o]);
     }
   }
   flat = __syncthreads_and(flat);
@@ -397,9 +392,18 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
         const float cq = e.c[0][qq];
         if (cq == 0.f || !rowok) continue;
         const float* ip = e.in[qq] + (size_t)r * n + c0;
+        if (full) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
+          for (int j = 0; j < 32; j += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
+            o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
+            o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
+        }
       }
       if (e.d[0] != 0.f && r >= c0 && r < c0 + 32) {
 #pragma unroll
@@ -407,9 +411,16 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
           if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
       }
       if (rowok) {
+        float* op = e.out[0] + (size_t)r * n + c0;
+        if (full) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < n) e.out[0][(size_t)r * n + c0 + j] = o0[j];
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) op[j] = o0[j];
+        }
       }
       for (int k = 1; k < e.nout; ++k) {
         float ok[32];
@@ -419,9 +430,18 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
           const float cq = e.c[k][qq];
           if (cq == 0.f || !rowok) continue;
           const float* ip = e.in[qq] + (size_t)r * n + c0;
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+            for (int j = 0; j < 32; j += 4) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
+              ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
+              ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+          }
         }
         if (e.d[k] != 0.f && r >= c0 && r < c0 + 32) {
 #pragma unroll
@@ -429,9 +449,16 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
             if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
         }
         if (rowok) {
+          float* op = e.out[k] + (size_t)r * n + c0;
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < n) e.out[k][(size_t)r * n + c0 + j] = ok[j];
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < n) op[j] = ok[j];
+          }
         }
       }
       if (e.colnorm) {

@@ -86,7 +86,7 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   const size_t i8plane = (size_t)n * i8_np(n);
   const size_t per_bufs = L.mat_bytes * L.nbufs;
   // per-matrix bytes for sizing the chunk (the int8-slice regions sit after the lists)
-  const size_t per = per_bufs + (i8p ? 2 * i8::NSL * i8plane + 4 * (size_t)n * sizeof(int) + 4 : 0);
+  const size_t per = per_bufs + (i8p ? 2 * i8::NSL * i8plane + 2 * (size_t)n * sizeof(int) + 2 * (size_t)n * 8 + 4 : 0);
   int64_t chunk = (int64_t)(kLargeWsCap / per);
   if (chunk < 1) chunk = 1;
   if (chunk > 65535) chunk = 65535;  // gridDim.z
@@ -109,8 +109,8 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.off_i8bs = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
   L.off_i8er = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
   L.off_i8ec = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
-  L.off_i8rc = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
-  L.off_i8cc = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
+  L.off_i8rc = off; off += i8p ? align256((size_t)chunk * n * 8) : 0;
+  L.off_i8cc = off; off += i8p ? align256((size_t)chunk * n * 8) : 0;
   L.off_i8ok = off; off += i8p ? align256((size_t)chunk * sizeof(int)) : 0;
   L.total = off;
   return L;
@@ -288,7 +288,7 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
   const int n = g.n;
   const size_t vb = (size_t)count * n * sizeof(int);
   if (cudaMemsetAsync(b.er, 0, vb, st) != cudaSuccess || cudaMemsetAsync(b.ec, 0, vb, st) != cudaSuccess ||
-      cudaMemsetAsync(b.rc, 0, vb, st) != cudaSuccess || cudaMemsetAsync(b.cc, 0, vb, st) != cudaSuccess)
+      cudaMemsetAsync(b.rc, 0, 2 * vb, st) != cudaSuccess || cudaMemsetAsync(b.cc, 0, 2 * vb, st) != cudaSuccess)
     return 1;
   static const bool dbg = getenv("EXPMB_DEBUG_SYNC") != nullptr;
   auto chk = [&](const char* what) {
@@ -300,8 +300,6 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
   const dim3 tiles((n + 31) / 32, (n + 31) / 32, count);
   i8::k_i8_stats<<<tiles, 256, 0, st>>>(g, stage, list, b);
   if (chk("stats")) return 1;
-  i8::k_i8_count<<<tiles, 256, 0, st>>>(g, stage, list, b);
-  if (chk("count")) return 1;
   i8::k_i8_route<<<count, 256, 0, st>>>(g, stage, list, b);
   if (chk("route")) return 1;
   i8::k_i8_slice<<<tiles, 256, 0, st>>>(g, stage, list, b);
@@ -373,8 +371,8 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
       i8b.bs = reinterpret_cast<int8_t*>(ws + L.off_i8bs);
       i8b.er = reinterpret_cast<int*>(ws + L.off_i8er);
       i8b.ec = reinterpret_cast<int*>(ws + L.off_i8ec);
-      i8b.rc = reinterpret_cast<int*>(ws + L.off_i8rc);
-      i8b.cc = reinterpret_cast<int*>(ws + L.off_i8cc);
+      i8b.rc = reinterpret_cast<unsigned long long*>(ws + L.off_i8rc);
+      i8b.cc = reinterpret_cast<unsigned long long*>(ws + L.off_i8cc);
       i8b.ok = reinterpret_cast<int*>(ws + L.off_i8ok);
       if (!encode_map_i8(&i8maps.a, i8b.as, n, i8b.np, cnt * i8::NSL, i8::BM) ||
           !encode_map_i8(&i8maps.b, i8b.bs, n, i8b.np, cnt * i8::NSL, i8::BN)) {

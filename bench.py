@@ -618,10 +618,14 @@ def run_ours(args):
             # int8 slice-pair products per fp32 product; the FFMA peak stays the
             # useful-flop yardstick, the int8 view is reported beside it
             i8_ops = 10.0 * flops
-            roof["kernel"] = "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products"
-            roof["int8_tensor"] = {"achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": 4500.0, "unit": "TOPS",
-                                   "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / 4500.0,
-                                   "peak_source": "nominal dense int8 (no measured int8 peak on this pool)"}
+            ffma_view = dict(roof)
+            ffma_view.pop("other", None)
+            roof = {"bound": "tensor", "achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": 4500.0,
+                    "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / 4500.0, "traffic": None,
+                    "peak_source": "nominal dense int8 (no measured int8 peak on this pool)",
+                    "executed_int8_ops_per_launch": i8_ops,
+                    "kernel": "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products",
+                    "other": ffma_view}
         if tg:
             # the time-grid path skips the evaluation products: its roofline is
             # over the flops it executes (squarings, shared powers in fp64, the

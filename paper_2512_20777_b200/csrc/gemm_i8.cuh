@@ -105,45 +105,51 @@ __global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, c
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
-  __shared__ int cmax[8][33];
-  __shared__ unsigned long long csum[8][33];
-  const int n = g.n;
+  __shared__ int cmax[32][33];
+  __shared__ unsigned long long csum[32][33];
+  const int n = g.n;  // a multiple of 16 on this path: groups of 4 columns are all in or all out
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  int cm = 0;
-  unsigned long long cs = 0;
-  for (int i = ty; i < 32; i += 8) {
-    const int r = r0 + i, c = c0 + tx;
-    const bool in = r < n && c < n && r != c;
-    const float lf = in ? fabsf(e.L[(size_t)r * n + c]) : 0.f;
-    const float rf = in ? (e.R == e.L ? lf : fabsf(e.R[(size_t)r * n + c])) : 0.f;
-    int m = __float_as_int(lf);
-    unsigned long long sm = exp_pack(lf);
+  const int i = threadIdx.x / 8, q = threadIdx.x % 8;  // row i of the tile, columns 4q..4q+3
+  const int r = r0 + i, c = c0 + 4 * q;
+  float lf[4] = {0.f, 0.f, 0.f, 0.f}, rf[4] = {0.f, 0.f, 0.f, 0.f};
+  if (r < n && c < n) {
+    const float4 a = *reinterpret_cast<const float4*>(e.L + (size_t)r * n + c);
+    const float4 bb = e.R == e.L ? a : *reinterpret_cast<const float4*>(e.R + (size_t)r * n + c);
+    lf[0] = fabsf(a.x); lf[1] = fabsf(a.y); lf[2] = fabsf(a.z); lf[3] = fabsf(a.w);
+    rf[0] = fabsf(bb.x); rf[1] = fabsf(bb.y); rf[2] = fabsf(bb.z); rf[3] = fabsf(bb.w);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      sm += __shfl_xor_sync(0xffffffffu, sm, o);
-    }
-    if (tx == 0 && r < n) {
-      if (m) atomicMax(b.er + (size_t)slot * n + r, m);
-      if (sm) atomicAdd(b.rc + (size_t)slot * n + r, sm);
-    }
-    cm = max(cm, __float_as_int(rf));
-    cs += exp_pack(rf);
+    for (int u = 0; u < 4; ++u)
+      if (c + u == r) lf[u] = rf[u] = 0.f;  // diagonal: handled exactly in the epilogue
   }
-  cmax[ty][tx] = cm;
-  csum[ty][tx] = cs;
-  __syncthreads();
-  if (ty == 0 && c0 + tx < n) {
-    int m = cmax[0][tx];
-    unsigned long long sm = csum[0][tx];
+  int m = 0;
+  unsigned long long sm = 0;
 #pragma unroll
-    for (int i = 1; i < 8; ++i) {
-      m = max(m, cmax[i][tx]);
-      sm += csum[i][tx];
+  for (int u = 0; u < 4; ++u) {
+    m = max(m, __float_as_int(lf[u]));
+    sm += exp_pack(lf[u]);
+    cmax[i][4 * q + u] = __float_as_int(rf[u]);
+    csum[i][4 * q + u] = exp_pack(rf[u]);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {  // the 8 lanes sharing row i
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  if (q == 0 && r < n) {
+    if (m) atomicMax(b.er + (size_t)slot * n + r, m);
+    if (sm) atomicAdd(b.rc + (size_t)slot * n + r, sm);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && c0 + threadIdx.x < n) {
+    const int cc = threadIdx.x;
+    int mm = 0;
+    unsigned long long ss = 0;
+    for (int k = 0; k < 32; ++k) {
+      mm = max(mm, cmax[k][cc]);
+      ss += csum[k][cc];
     }
-    if (m) atomicMax(b.ec + (size_t)slot * n + c0 + tx, m);
-    if (sm) atomicAdd(b.cc + (size_t)slot * n + c0 + tx, sm);
+    if (mm) atomicMax(b.ec + (size_t)slot * n + c0 + cc, mm);
+    if (ss) atomicAdd(b.cc + (size_t)slot * n + c0 + cc, ss);
   }
 }
 
@@ -188,38 +194,52 @@ __global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, c
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
   __shared__ float tile[32][33];
-  const int n = g.n;
+  const int n = g.n;  // a multiple of 16 on this path
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const size_t plane = (size_t)n * b.np;
   int8_t* as = b.as + (size_t)slot * NSL * plane;
   int8_t* bs = b.bs + (size_t)slot * NSL * plane;
   const int* er = b.er + (size_t)slot * n;
   const int* ec = b.ec + (size_t)slot * n;
-  for (int i = ty; i < 32; i += 8) {
-    const int r = r0 + i, c = c0 + tx;
-    float x = 0.f, y = 0.f;
+  auto pack = [](const int8_t (&v)[4][4], int j) {  // plane j of four elements -> one 32-bit word
+    return (uint32_t)(uint8_t)v[0][j] | ((uint32_t)(uint8_t)v[1][j] << 8) | ((uint32_t)(uint8_t)v[2][j] << 16) |
+           ((uint32_t)(uint8_t)v[3][j] << 24);
+  };
+  {
+    // L row slices: row i, columns 4q..4q+3 (one float4 in, one 32-bit word per plane out)
+    const int i = threadIdx.x / 8, q = threadIdx.x % 8;
+    const int r = r0 + i, c = c0 + 4 * q;
+    float x[4] = {0.f, 0.f, 0.f, 0.f}, y[4] = {0.f, 0.f, 0.f, 0.f};
     if (r < n && c < n) {
-      x = e.L[(size_t)r * n + c];
-      y = e.R == e.L ? x : e.R[(size_t)r * n + c];
-    }
-    tile[i][tx] = (r == c) ? 0.f : y;
-    if (r < n && c < n) {
-      int8_t sl[4];
-      slice4(r == c ? 0.f : x, exp_of(__int_as_float(er[r])), sl);
+      const float4 a = *reinterpret_cast<const float4*>(e.L + (size_t)r * n + c);
+      const float4 bb = e.R == e.L ? a : *reinterpret_cast<const float4*>(e.R + (size_t)r * n + c);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      y[0] = bb.x; y[1] = bb.y; y[2] = bb.z; y[3] = bb.w;
 #pragma unroll
-      for (int j = 0; j < NSL; ++j) as[j * plane + (size_t)r * b.np + c] = sl[j];
+      for (int u = 0; u < 4; ++u)
+        if (c + u == r) x[u] = y[u] = 0.f;
+      const int ex = exp_of(__int_as_float(er[r]));
+      int8_t sl[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) slice4(x[u], ex, sl[u]);
+#pragma unroll
+      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + (size_t)r * b.np + c) = pack(sl, j);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tile[i][4 * q + u] = y[u];
   }
   __syncthreads();
-  // R[k][c] -> bs[j][c][k]: thread (tx, ty) writes column c = c0 + i, k = r0 + tx
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i, k = r0 + tx;
+  {
+    // R column slices, transposed: column ci, k = 4q..4q+3 of the tile
+    const int ci = threadIdx.x / 8, q = threadIdx.x % 8;
+    const int c = c0 + ci, k = r0 + 4 * q;
     if (c < n && k < n) {
-      int8_t sl[4];
-      slice4(tile[tx][i], exp_of(__int_as_float(ec[c])), sl);
+      const int ex = exp_of(__int_as_float(ec[c]));
+      int8_t sl[4][4];
 #pragma unroll
-      for (int j = 0; j < NSL; ++j) bs[j * plane + (size_t)c * b.np + k] = sl[j];
+      for (int u = 0; u < 4; ++u) slice4(tile[4 * q + u][ci], ex, sl[u]);
+#pragma unroll
+      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(bs + j * plane + (size_t)c * b.np + k) = pack(sl, j);
     }
   }
 }

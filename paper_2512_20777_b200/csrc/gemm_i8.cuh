@@ -266,6 +266,18 @@ __device__ __forceinline__ void tmem_ld32i(uint32_t taddr, int (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = (int)r[j];
 }
 
+__device__ __forceinline__ void tmem_ld16i(uint32_t taddr, int (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = (int)r[j];
+}
+
 struct Maps {
   CUtensorMap a, b;
 };
@@ -352,131 +364,137 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
     tc::mma_commit(&tmem_bar);
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
-    tc::mbar_wait(&tmem_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+    // 16-column chunks keep the live arrays small enough for 2 CTAs/SM
+    // without spills.
+    constexpr int CW = 16;
     const int q = warp & 3;
     const int rl = q * 32 + lane;
     const int r = m0 + rl;
     const bool rowok = r < n;
+    // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
+    // the int8 GEMM carries Yl Yr (each row / column scaled without its
+    // diagonal, which in the squaring phase dominates), the rest is exact
+    // elementwise work here, all summed in binary64 and rounded once.  The
+    // operand rows of the first chunk are fetched while the MMAs still run.
+    float lrow[CW], rrow[CW];
+#define I8_LOAD_ROWS(C0)                                                                       \
+  do {                                                                                         \
+    const int c0_ = (C0);                                                                      \
+    if (rowok && c0_ + CW <= n) {                                                              \
+      const float4* lp = reinterpret_cast<const float4*>(e.L + (size_t)r * n + c0_);           \
+      const float4* rp = reinterpret_cast<const float4*>(e.R + (size_t)r * n + c0_);           \
+      _Pragma("unroll") for (int j = 0; j < CW / 4; ++j) {                                     \
+        const float4 a = __ldg(lp + j);                                                        \
+        lrow[4 * j] = a.x; lrow[4 * j + 1] = a.y; lrow[4 * j + 2] = a.z; lrow[4 * j + 3] = a.w; \
+        const float4 bb = (e.R == e.L) ? a : __ldg(rp + j);                                    \
+        rrow[4 * j] = bb.x; rrow[4 * j + 1] = bb.y; rrow[4 * j + 2] = bb.z; rrow[4 * j + 3] = bb.w; \
+      }                                                                                        \
+    } else {                                                                                   \
+      _Pragma("unroll") for (int j = 0; j < CW; ++j) {                                         \
+        const bool ok_ = rowok && c0_ + j < n;                                                 \
+        lrow[j] = ok_ ? e.L[(size_t)r * n + c0_ + j] : 0.f;                                     \
+        rrow[j] = ok_ ? e.R[(size_t)r * n + c0_ + j] : 0.f;                                     \
+      }                                                                                        \
+    }                                                                                          \
+  } while (0)
+    I8_LOAD_ROWS(n0);
     const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
     const double rs = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6);
     const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
+    tc::mbar_wait(&tmem_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
     double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
-    for (int cb = 0; cb < BN / 32; ++cb) {
-      int a0[32], a1[32], a2[32], a3[32];
-      float v[32];
-      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * 32;
-      tmem_ld32i(ta, a0);
-      tmem_ld32i(ta + BN, a1);
-      tmem_ld32i(ta + 2 * BN, a2);
-      tmem_ld32i(ta + 3 * BN, a3);
-      const int c0 = n0 + cb * 32;
-      const bool full = rowok && c0 + 32 <= n;
-      // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
-      // the int8 GEMM carries Yl Yr (each row / column scaled without its
-      // diagonal, which in the squaring phase dominates), the rest is exact
-      // elementwise work here, all summed in binary64 and rounded once
-      float lrow[32], rrow[32];
-      if (full) {
-        const float4* lp = reinterpret_cast<const float4*>(e.L + (size_t)r * n + c0);
-        const float4* rp = reinterpret_cast<const float4*>(e.R + (size_t)r * n + c0);
+#pragma unroll 1
+    for (int cb = 0; cb < BN / CW; ++cb) {
+      int a0[CW], a1[CW], a2[CW], a3[CW];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
+      tmem_ld16i(ta, a0);
+      tmem_ld16i(ta + BN, a1);
+      tmem_ld16i(ta + 2 * BN, a2);
+      tmem_ld16i(ta + 3 * BN, a3);
+      const int c0 = n0 + cb * CW;
+      const bool full = rowok && c0 + CW <= n;
+      if (cb > 0) I8_LOAD_ROWS(c0);
+      float o0[CW];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 a = __ldg(lp + j);
-          lrow[4 * j] = a.x; lrow[4 * j + 1] = a.y; lrow[4 * j + 2] = a.z; lrow[4 * j + 3] = a.w;
-          const float4 bb = (e.R == e.L) ? a : __ldg(rp + j);
-          rrow[4 * j] = bb.x; rrow[4 * j + 1] = bb.y; rrow[4 * j + 2] = bb.z; rrow[4 * j + 3] = bb.w;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = rowok && c0 + j < n;
-          lrow[j] = ok ? e.L[(size_t)r * n + c0 + j] : 0.f;
-          rrow[j] = ok ? e.R[(size_t)r * n + c0 + j] : 0.f;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < CW; ++j) {
         const int c = c0 + j;
         // exact: each Horner step fits binary64 (|acc| < 2^27, 21 fraction bits)
         const double t = (((double)a3[j] * 0x1p-7 + (double)a2[j]) * 0x1p-7 + (double)a1[j]) * 0x1p-7 + (double)a0[j];
-        double y = t * rs * cs_sh[cb * 32 + j];
-        const double dr = (double)dr_sh[cb * 32 + j];
+        double y = t * rs * cs_sh[cb * CW + j];
+        const double dr = (double)dr_sh[cb * CW + j];
         y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
-        v[j] = (float)y;
+        o0[j] = e.alpha * (float)y;
       }
-      float o0[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) o0[j] = e.alpha * v[j];
       for (int qq = 0; qq < e.nin; ++qq) {
         const float cq = e.c[0][qq];
         if (cq == 0.f || !rowok) continue;
         const float* ip = e.in[qq] + (size_t)r * n + c0;
         if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
+          for (int j = 0; j < CW; j += 4) {
             const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
             o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
             o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < CW; ++j)
             if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
         }
       }
-      if (e.d[0] != 0.f && r >= c0 && r < c0 + 32) {
+      if (e.d[0] != 0.f && r >= c0 && r < c0 + CW) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < CW; ++j)
           if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
       }
       if (rowok) {
         float* op = e.out[0] + (size_t)r * n + c0;
         if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
+          for (int j = 0; j < CW; j += 4)
             *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < CW; ++j)
             if (c0 + j < n) op[j] = o0[j];
         }
       }
       for (int k = 1; k < e.nout; ++k) {
-        float ok[32];
+        float ok[CW];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ok[j] = o0[j];
+        for (int j = 0; j < CW; ++j) ok[j] = o0[j];
         for (int qq = 0; qq < e.nin; ++qq) {
           const float cq = e.c[k][qq];
           if (cq == 0.f || !rowok) continue;
           const float* ip = e.in[qq] + (size_t)r * n + c0;
           if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
+            for (int j = 0; j < CW; j += 4) {
               const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
               ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
               ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < CW; ++j)
               if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
           }
         }
-        if (e.d[k] != 0.f && r >= c0 && r < c0 + 32) {
+        if (e.d[k] != 0.f && r >= c0 && r < c0 + CW) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < CW; ++j)
             if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
         }
         if (rowok) {
           float* op = e.out[k] + (size_t)r * n + c0;
           if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
+            for (int j = 0; j < CW; j += 4)
               *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < CW; ++j)
               if (c0 + j < n) op[j] = ok[j];
           }
         }
@@ -484,9 +502,9 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
       if (e.colnorm) {
         // deterministic column abs-sums of this 128-row tile (select.py:193)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
+        for (int j = 0; j < CW; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (rl < 32 && c0 + rl < n) {
+        if (rl < CW && c0 + rl < n) {
           double a = 0.0;
           for (int rr = 0; rr < BM; ++rr) a += red[rl * BM + rr];
           g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + c0 + rl] = a;
@@ -494,6 +512,7 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
     }
+#undef I8_LOAD_ROWS
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

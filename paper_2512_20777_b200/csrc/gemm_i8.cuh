@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
   } while (0)
     I8_LOAD_ROWS(n0);
     const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
-    const double rs = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6);
+    const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
     const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
     tc::mbar_wait(&tmem_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -419,9 +419,11 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
         const int c = c0 + j;
-        // exact: each Horner step fits binary64 (|acc| < 2^27, 21 fraction bits)
-        const double t = (((double)a3[j] * 0x1p-7 + (double)a2[j]) * 0x1p-7 + (double)a1[j]) * 0x1p-7 + (double)a0[j];
-        double y = t * rs * cs_sh[cb * CW + j];
+        // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49) and a
+        // single int -> binary64 conversion (the conversion unit was the hot pipe)
+        const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
+                            (long long)a3[j];
+        double y = (double)T * rs21 * cs_sh[cb * CW + j];
         const double dr = (double)dr_sh[cb * CW + j];
         y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
         o0[j] = e.alpha * (float)y;

@@ -27,7 +27,7 @@
 //
 // Kernels: k_i8_rowexp / k_i8_colexp (exponents), k_i8_slice_rows (L slices,
 // K-major), k_i8_slice_cols (R slices transposed to K-major), k_i8_stage
-// (TMA 128B-swizzled ring of 4 L slices + 4 R slices per k-tile, one thread
+// (TMA 64B-swizzled 2-stage ring of 4 L slices + 4 R slices per k-tile, one thread
 // issuing the ten pair MMAs per 32-byte k-step into four int32 TMEM
 // accumulators, four epilogue warps applying the stage's fused linear
 // combination exactly as gemm_simt.cuh's epilogue does).
@@ -43,13 +43,34 @@
 namespace expmb {
 namespace i8 {
 
-#ifndef EXPMB_I8_STAGES
-#define EXPMB_I8_STAGES 1  // 1 stage = 96 KB smem: two CTAs per SM, one's epilogue overlaps the other's MMAs
+// k-tiles of 64 bytes with the 64B swizzle: a stage (4 L + 4 R slices) is
+// 48 KB, so two stages per CTA and two CTAs per SM fit (TMA of the next
+// k-tile overlaps this one's MMAs, and one CTA's epilogue the other's MMAs).
+#ifndef EXPMB_I8_BK64
+#define EXPMB_I8_BK64 1
 #endif
-constexpr int BM = 128, BN = 64, BKB = 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
-constexpr int A_TILE = BM * BKB;                     // 16 KB
-constexpr int B_TILE = BN * BKB;                     // 8 KB
-constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 96 KB
+#ifndef EXPMB_I8_STAGES
+#define EXPMB_I8_STAGES (EXPMB_I8_BK64 ? 2 : 1)
+#endif
+constexpr int BM = 128, BN = 64, BKB = EXPMB_I8_BK64 ? 64 : 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
+constexpr bool kSw64 = BKB == 64;
+// UMMA shared-memory descriptor, K-major: 64B swizzle (8-row atoms of 512 B) or 128B (1024 B)
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
+  if constexpr (!kSw64) {
+    return tc::kmajor_desc(saddr);
+  } else {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3fff);
+    d |= (uint64_t)(16 >> 4) << 16;   // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;  // SBO: next 8-row group
+    d |= (uint64_t)1 << 46;           // descriptor version (sm100)
+    d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+    return d;
+  }
+}
+constexpr int A_TILE = BM * BKB;                     // 8 KB (64B swizzle)
+constexpr int B_TILE = BN * BKB;                     // 4 KB
+constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 48 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
 constexpr int NTHREADS = 192;                         // w0 TMA, w1 MMA/TMEM, w2..w5 epilogue
 constexpr uint32_t TMEM_COLS = 4 * BN;                // one int32 accumulator per level
@@ -282,7 +303,7 @@ struct Maps {
   CUtensorMap a, b;
 };
 
-__global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
+__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1)) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
                                                           int stage, const int* __restrict__ list, Bufs bf) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;
@@ -353,8 +374,8 @@ __global__ void __launch_bounds__(NTHREADS, (STAGES == 1 ? 2 : 1)) k_i8_stage(co
 #pragma unroll
           for (int i = 0; i <= lv; ++i) {
             const int j = lv - i;
-            const uint64_t a = tc::kmajor_desc(base + i * A_TILE + k * 32);
-            const uint64_t bd = tc::kmajor_desc(base + NSL * A_TILE + j * B_TILE + k * 32);
+            const uint64_t a = kdesc(base + i * A_TILE + k * 32);
+            const uint64_t bd = kdesc(base + NSL * A_TILE + j * B_TILE + k * 32);
             mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
           }
         }

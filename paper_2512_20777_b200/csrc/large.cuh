@@ -266,7 +266,9 @@ static bool encode_map_i8(CUtensorMap* m, const int8_t* base, int n, int np, int
   cuuint32_t box[3] = {(cuuint32_t)i8::BKB, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         i8::kSw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS && getenv("EXPMB_DEBUG_SYNC"))
     fprintf(stderr, "expmb i8: cuTensorMapEncodeTiled -> %d (base %p n %d np %d planes %lld box_rows %d)\n", (int)r,

@@ -131,3 +131,22 @@ def test_host_selector_golden(golden):
         code = _lib.EXPMB_SASTRE if scheme == "sastre" else _lib.EXPMB_PS
         m, s, e1, e2, _ = _lib.select_host(norms, float(golden["eps"][i]), code)
         assert (m, s) == (golden["m"][i], golden["s"][i]), golden["names"][i]
+
+
+def test_int8_slice_workspace_switch(monkeypatch):
+    """The int8-slice path (fp32, n >= 1024 by default) adds its slice planes
+    and statistics to the large-n workspace; EXPMB_I8=0 removes them."""
+    L = _lib.lib()
+    monkeypatch.delenv("EXPMB_I8", raising=False)
+    on = L.expmb_workspace_bytes(8, 1024, _lib.EXPMB_F32, _lib.EXPMB_SASTRE)
+    monkeypatch.setenv("EXPMB_I8", "0")
+    off = L.expmb_workspace_bytes(8, 1024, _lib.EXPMB_F32, _lib.EXPMB_SASTRE)
+    # 8 slice planes of n x n bytes per matrix at least
+    assert on - off >= 8 * 8 * 1024 * 1024
+    monkeypatch.delenv("EXPMB_I8", raising=False)
+    # fp64 and small orders never use it
+    assert L.expmb_workspace_bytes(8, 1024, _lib.EXPMB_F64, 0) == L.expmb_workspace_bytes(8, 1024, _lib.EXPMB_F64, 0)
+    monkeypatch.setenv("EXPMB_I8", "0")
+    small_off = L.expmb_workspace_bytes(8, 256, _lib.EXPMB_F32, 0)
+    monkeypatch.delenv("EXPMB_I8", raising=False)
+    assert L.expmb_workspace_bytes(8, 256, _lib.EXPMB_F32, 0) == small_off

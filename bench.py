@@ -422,13 +422,13 @@ def _launch_count(key, m, s, n, dtype="f64"):
     """Kernels of ours launched by one expm call (host orchestration is deterministic):
     n > 64: colsum, two k_select, elem, nonfinite, finish + one launch per product
     stage (W^2, E1..E3 as present, one per squaring level); on the int8-slice path
-    (fp32, n >= 1024) a product stage is five kernels (stats, route, slice,
+    (fp32, n >= 512) a product stage is five kernels (stats, route, slice,
     int8 GEMM, FFMA GEMM for routed-away products)."""
     if n <= 64:
         return 1
     m = np.asarray(m); s = np.asarray(s)
     stages = 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max())
-    per = 5 if (dtype == "f32" and n >= 1024 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
+    per = 5 if (dtype == "f32" and n >= 512 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
     return int(6 + stages * per)
 
 
@@ -613,7 +613,7 @@ def run_ours(args):
         else:
             roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
         roof["other"] = cmp_roof if hbm_binds else hbm_roof
-        if cfg.dtype == "f32" and cfg.n >= 1024 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0":
+        if cfg.dtype == "f32" and cfg.n >= 512 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0":
             # products run as exact int8-slice GEMMs on tcgen05 (gemm_i8.cuh): ten
             # int8 slice-pair products per fp32 product; the FFMA peak stays the
             # useful-flop yardstick, the int8 view is reported beside it

@@ -23,7 +23,7 @@
 // / column, so entries far below their row's maximum keep fewer bits than in
 // fp32 -- on graded matrices (entries ~2^20 apart within a row) the error is
 // 30x the FFMA path's (tools/i8_graded_probe.py).  Hence opt-in (EXPMB_I8=1,
-// fp32, n >= 512, n % 16 == 0), not the default.
+// fp32, n % 16 == 0).
 //
 // Kernels: k_i8_rowexp / k_i8_colexp (exponents), k_i8_slice_rows (L slices,
 // K-major), k_i8_slice_cols (R slices transposed to K-major), k_i8_stage

@@ -54,15 +54,16 @@ static inline bool use_tc_path(int n, int esize, int scheme) {
 }
 // Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh):
 // opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
-// Default: on for fp32 n >= 1024 (where it is faster); EXPMB_I8=1 also enables
-// it from n = 512, EXPMB_I8=0 disables it.  Each product is routed per matrix
+// Default: on for fp32 n >= 512 (measured crossover, tools/i8_crossover.py:
+// 1.07x at 512, 1.38x at 768, 1.67x at 1024, 2.1x at 1536, 0.88x at 384);
+// EXPMB_I8=1 also enables it from n = 256, EXPMB_I8=0 disables it.  Each product is routed per matrix
 // (k_i8_route): operands that are not "flat" go to the FFMA GEMM.
 static inline bool use_i8_path(int n, int esize) {
   const char* e = getenv("EXPMB_I8");
   if (esize != 4 || n % 16 != 0) return false;
   if (e != nullptr && e[0] == '0') return false;
-  if (e != nullptr && e[0] == '1') return n >= 512;
-  return n >= 1024;
+  if (e != nullptr && e[0] == '1') return n >= 256;
+  return n >= 512;
 }
 static inline int i8_np(int n) { return (n + 15) / 16 * 16; }
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers

@@ -1,5 +1,5 @@
 """The exact int8-slice tensor-core GEMM path (gemm_i8.cuh; default for fp32
-n >= 1024, EXPMB_I8=1 from n = 512) against the oracle: dense inputs over
+n >= 512, EXPMB_I8=1 from n = 256) against the oracle: dense inputs over
 three norm scales (the squaring phase's dominant diagonal included), ragged
 column tiles, PS, non-finite input, and the per-product routing: graded
 operands (entries ~2^20 apart within a row, where per-row scaling would lose
@@ -72,7 +72,7 @@ def test_i8_routes_graded_operands_to_ffma(monkeypatch):
 
 
 def test_i8_default_on_for_large_dense(monkeypatch):
-    """Without EXPMB_I8 the path is on for n >= 1024 and matches the oracle."""
+    """Without EXPMB_I8 the path is on for n >= 512 and matches the oracle."""
     monkeypatch.delenv("EXPMB_I8", raising=False)
     n = 1024
     rng = np.random.default_rng(9)

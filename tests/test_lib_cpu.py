@@ -134,7 +134,7 @@ def test_host_selector_golden(golden):
 
 
 def test_int8_slice_workspace_switch(monkeypatch):
-    """The int8-slice path (fp32, n >= 1024 by default) adds its slice planes
+    """The int8-slice path (fp32, n >= 512 by default) adds its slice planes
     and statistics to the large-n workspace; EXPMB_I8=0 removes them."""
     L = _lib.lib()
     monkeypatch.delenv("EXPMB_I8", raising=False)

@@ -267,10 +267,14 @@ class HostPipeline:
         s_in, s_comp, s_out = self.streams
         s_in.wait_stream(torch.cuda.current_stream(self.dev))
         comp_handle = s_comp.cuda_stream
+        # every host->device copy is queued first: for n > 64 the library reads
+        # each chunk's plans back (one host sync per call), and the copy engine
+        # must not wait for that
         for a, b, wp, xp, ptrs, ev_in, ev_c in self._chunks:
             with torch.cuda.stream(s_in):
                 self.Wd[a:b].copy_(Wf[a:b], non_blocking=True)
                 ev_in.record(s_in)
+        for a, b, wp, xp, ptrs, ev_in, ev_c in self._chunks:
             s_comp.wait_event(ev_in)
             rc = L.expmb_expm(wp, xp, b - a, n, self._dt, float(eps), code, *ptrs, wsp, wsb, comp_handle)
             if rc != 0:

@@ -367,6 +367,10 @@ __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 
       tc::mbar_wait(&full_bar[st], (kt / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t base = tc::smem_u32(sm + st * STAGE_BYTES);
+      // descriptors built once per stage; the slice / k-step offsets go into
+      // the 16-byte-unit address field (smem < 256 KB: no carry out of it)
+      const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
+      const uint32_t acc0 = (kt > 0) ? 1u : 0u;
 #pragma unroll
       for (int k = 0; k < BKB / 32; ++k) {
 #pragma unroll
@@ -374,9 +378,9 @@ __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 
 #pragma unroll
           for (int i = 0; i <= lv; ++i) {
             const int j = lv - i;
-            const uint64_t a = kdesc(base + i * A_TILE + k * 32);
-            const uint64_t bd = kdesc(base + NSL * A_TILE + j * B_TILE + k * 32);
-            mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
+            const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + k * 32) >> 4);
+            mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (k > 0 || i > 0) ? 1u : acc0);
           }
         }
       }

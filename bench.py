@@ -330,7 +330,14 @@ def run_lowrank(args):
     with ClockSampler(local) as clk:
         time.sleep(0.05)
         clk.mark("start")
-        torch.cuda._sleep(int(min(args.steps, 200) * 400_000))
+        # (busy-wait: the SM clock stays up; ~0.5 ms per step covers the host's
+        # per-call overhead)
+        torch.cuda._sleep(int(2_000_000 + min(args.steps, 200) * 1_000_000))
+        # one untimed step right after the hold: the first kernel after a
+        # memory-idle spin runs ~2x slow (measured: C2 204 vs 80 us, C1 333 vs
+        # 145 us), an artifact of the hold, not of the step
+        l2_flush()
+        step()
         for i in range(args.steps):
             l2_flush()
             evs[i][0].record(stream)
@@ -501,7 +508,14 @@ def run_ours(args):
         # hold the device briefly so the host queues all K steps ahead of it:
         # the per-step events then bracket device work only (host launch cost
         # is what the e2e number below measures)
-        torch.cuda._sleep(int(min(args.steps, 200) * 400_000))
+        # (busy-wait: the SM clock stays up; ~0.5 ms per step covers the host's
+        # per-call overhead)
+        torch.cuda._sleep(int(2_000_000 + min(args.steps, 200) * 1_000_000))
+        # one untimed step right after the hold: the first kernel after a
+        # memory-idle spin runs ~2x slow (measured: C2 204 vs 80 us, C1 333 vs
+        # 145 us), an artifact of the hold, not of the step
+        l2_flush()
+        step()
         for i in range(args.steps):
             l2_flush()
             evs[i][0].record(stream)
@@ -510,6 +524,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         clk.mark("end")
     step_ms = [a.elapsed_time(b) for a, b in evs]
+    if os.environ.get("BENCH_STEP_TIMES"):
+        print("step ms:", " ".join(f"{x:.4f}" for x in step_ms), file=sys.stderr)
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)

@@ -100,6 +100,22 @@ int expmb_select_host(const double* norms, double eps, int scheme,
                       int* m, int* s, double* e1, double* e2);
 
 /*
+ * Host buffers in, host buffers out (the reference's calling convention,
+ * engine.py:119-152), pipelined: the batch is cut into `chunks` pieces (on
+ * multiples of 4 matrices); every host->device copy is queued on `s_in`, each
+ * chunk's expmb_expm runs on `s_comp` after its copy, and its result is
+ * copied back on `s_out` while later chunks compute.  W_host / X_host should
+ * be pinned (cudaHostAlloc) for the copies to overlap; W_dev / X_dev are
+ * [batch,n,n] device staging buffers; the plan outputs are device arrays as
+ * in expmb_expm.  Returns after queuing; synchronise `s_out` (after
+ * `s_comp`) before reading X_host.
+ */
+int expmb_expm_pipelined(const void* W_host, void* X_host, void* W_dev, void* X_dev, int64_t batch, int32_t n,
+                         int dtype, double eps, int scheme, int8_t* m, int8_t* s, double* e1, double* e2,
+                         double* norms, int32_t* mults, uint8_t* nonfinite, int chunks, void* workspace,
+                         size_t workspace_bytes, void* s_in, void* s_comp, void* s_out);
+
+/*
  * Batched low-rank exponential.  Replaces engine.py:198-257 (expm_lowrank)
  * with the LowRankPair checks of engine.py:166-181: for W = A1 A2 returns
  * e^W = I + A1 psi(V) A2, V = A2 A1, psi(x) = sum_{i<=m} x^i/(i+1)!, the

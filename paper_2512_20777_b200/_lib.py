@@ -37,6 +37,7 @@ EXPORTS = (
     "expmb_select_lowrank_host",
     "expmb_timegrid_workspace_bytes",
     "expmb_expm_timegrid",
+    "expmb_expm_pipelined",
 )
 
 LR_BAD_INPUT, LR_NONFINITE, LR_NO_ORDER = 1, 2, 4
@@ -91,6 +92,12 @@ def lib() -> ctypes.CDLL:
         c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
         c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
         c.c_void_p, c.c_size_t, c.c_void_p,
+    ]
+    L.expmb_expm_pipelined.restype = c.c_int
+    L.expmb_expm_pipelined.argtypes = [
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+        c.c_int, c.c_void_p, c.c_size_t, c.c_void_p, c.c_void_p, c.c_void_p,
     ]
     _lib = L
     return L

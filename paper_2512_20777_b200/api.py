@@ -224,6 +224,7 @@ class HostPipeline:
         self.pd = {k: torch.empty(v.shape, dtype=v.dtype, device=self.dev) for k, v in self.host.items()}
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
         c = max(1, min(int(chunks), B)) if B else 1
+        self._nchunks = c
         # chunk bounds on multiples of 4 matrices keep every slice 16-byte aligned
         self.bounds = sorted({min(B, ((B * k) // c) // 4 * 4) for k in range(c)} | {B})
         if self.bounds[0] != 0:
@@ -266,23 +267,15 @@ class HostPipeline:
         wsp, wsb = self._ws.data_ptr(), self._wsb[code]
         s_in, s_comp, s_out = self.streams
         s_in.wait_stream(torch.cuda.current_stream(self.dev))
-        comp_handle = s_comp.cuda_stream
-        # every host->device copy is queued first: for n > 64 the library reads
-        # each chunk's plans back (one host sync per call), and the copy engine
-        # must not wait for that
-        for a, b, wp, xp, ptrs, ev_in, ev_c in self._chunks:
-            with torch.cuda.stream(s_in):
-                self.Wd[a:b].copy_(Wf[a:b], non_blocking=True)
-                ev_in.record(s_in)
-        for a, b, wp, xp, ptrs, ev_in, ev_c in self._chunks:
-            s_comp.wait_event(ev_in)
-            rc = L.expmb_expm(wp, xp, b - a, n, self._dt, float(eps), code, *ptrs, wsp, wsb, comp_handle)
-            if rc != 0:
-                _raise_rc(rc)
-            ev_c.record(s_comp)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_c)
-                self.out[a:b].copy_(self.Xd[a:b], non_blocking=True)
+        # the chunk loop runs in C (expmb_expm_pipelined): every host->device
+        # copy queued first, each chunk's expm on s_comp after its copy, its
+        # result copied back on s_out while later chunks compute
+        p = [self.pd[k].data_ptr() for k in ("m", "s", "e1", "e2", "norms", "mults", "nonfinite")]
+        rc = L.expmb_expm_pipelined(Wf.data_ptr(), self.out.data_ptr(), self.Wd.data_ptr(), self.Xd.data_ptr(),
+                                    self.B, n, self._dt, float(eps), code, *p, self._nchunks, wsp, wsb,
+                                    s_in.cuda_stream, s_comp.cuda_stream, s_out.cuda_stream)
+        if rc != 0:
+            _raise_rc(rc)
         with torch.cuda.stream(s_out):  # the small plan arrays: one copy each, after the last chunk
             s_out.wait_stream(s_comp)
             for k, v in self.host.items():

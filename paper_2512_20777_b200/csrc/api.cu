@@ -317,6 +317,64 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
   return large_expm(W, X, batch, n, dtype, eps, scheme, po, workspace, st);
 }
 
+int expmb_expm_pipelined(const void* W_host, void* X_host, void* W_dev, void* X_dev, int64_t batch, int32_t n,
+                         int dtype, double eps, int scheme, int8_t* m, int8_t* s, double* e1, double* e2,
+                         double* norms, int32_t* mults, uint8_t* nonfinite, int chunks, void* workspace,
+                         size_t workspace_bytes, void* s_in, void* s_comp, void* s_out) {
+  if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
+  if (n < 1 || batch < 0) return EXPMB_ERR_SHAPE;
+  if (batch == 0) return EXPMB_OK;
+  if (chunks < 1) chunks = 1;
+  if (chunks > 256) chunks = 256;
+  const size_t esz = dtype == EXPMB_F32 ? 4 : 8;
+  const size_t mat = (size_t)n * n * esz;
+  cudaStream_t si = (cudaStream_t)s_in, sc = (cudaStream_t)s_comp, so = (cudaStream_t)s_out;
+  // chunk bounds on multiples of 4 matrices (16-byte aligned slices)
+  int64_t bounds[257];
+  int nb = 0;
+  bounds[nb++] = 0;
+  for (int c = 1; c < chunks; ++c) {
+    const int64_t b = (batch * c / chunks) / 4 * 4;
+    if (b > bounds[nb - 1] && b < batch) bounds[nb++] = b;
+  }
+  bounds[nb++] = batch;
+  const int nch = nb - 1;
+  cudaEvent_t ev_in[256], ev_c[256];
+  for (int c = 0; c < nch; ++c) {
+    if (cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+  }
+  int rc = EXPMB_OK;
+  // every host->device copy first (the large-n path reads plans back per call)
+  for (int c = 0; c < nch && rc == EXPMB_OK; ++c) {
+    const size_t off = (size_t)bounds[c] * mat, bytes = (size_t)(bounds[c + 1] - bounds[c]) * mat;
+    if (cudaMemcpyAsync((char*)W_dev + off, (const char*)W_host + off, bytes, cudaMemcpyHostToDevice, si) !=
+            cudaSuccess ||
+        cudaEventRecord(ev_in[c], si) != cudaSuccess)
+      rc = EXPMB_ERR_CUDA;
+  }
+  for (int c = 0; c < nch && rc == EXPMB_OK; ++c) {
+    const int64_t a = bounds[c], cnt = bounds[c + 1] - bounds[c];
+    const size_t off = (size_t)a * mat, bytes = (size_t)cnt * mat;
+    if (cudaStreamWaitEvent(sc, ev_in[c], 0) != cudaSuccess) { rc = EXPMB_ERR_CUDA; break; }
+    rc = expmb_expm((const char*)W_dev + off, (char*)X_dev + off, cnt, n, dtype, eps, scheme, m ? m + a : nullptr,
+                    s ? s + a : nullptr, e1 ? e1 + a : nullptr, e2 ? e2 + a : nullptr,
+                    norms ? norms + 2 * a : nullptr, mults ? mults + a : nullptr,
+                    nonfinite ? nonfinite + a : nullptr, workspace, workspace_bytes, s_comp);
+    if (rc != EXPMB_OK) break;
+    if (cudaEventRecord(ev_c[c], sc) != cudaSuccess || cudaStreamWaitEvent(so, ev_c[c], 0) != cudaSuccess ||
+        cudaMemcpyAsync((char*)X_host + off, (const char*)X_dev + off, bytes, cudaMemcpyDeviceToHost, so) !=
+            cudaSuccess)
+      rc = EXPMB_ERR_CUDA;
+  }
+  for (int c = 0; c < nch; ++c) {  // released once their work completes
+    cudaEventDestroy(ev_in[c]);
+    cudaEventDestroy(ev_c[c]);
+  }
+  return rc;
+}
+
 int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int* m, double* e1, double* e2) {
   int mm = 0;
   double a = 0.0, b = 0.0;

@@ -472,3 +472,17 @@ def test_cuda_graph_capture_and_replay():
     torch.cuda.synchronize()
     ref2 = X.expm_lowrank(X.LowRankPair(a1.clone(), a2.clone()), 2.0 ** -53)
     assert torch.equal(xo, ref2.value)
+
+
+@pytest.mark.parametrize("n,B,dtype", [(80, 7, torch.float64), (600, 5, torch.float32), (16, 1001, torch.float32)])
+def test_expm_host_pageable_ragged(n, B, dtype):
+    """expm_host (the C pipelined entry) with pageable input, batch sizes that
+    are not multiples of the chunking (4-matrix alignment), the large-n path
+    (and the int8-slice path at n = 600): identical to the device call."""
+    rng = np.random.default_rng(n + B)
+    W = torch.as_tensor((rng.standard_normal((B, n, n)) * (3.0 / n ** 0.5)).astype(
+        np.float32 if dtype == torch.float32 else np.float64))
+    host = X.expm_host(W, 2.0 ** -24 if dtype == torch.float32 else 1e-12)
+    dev = X.expm(W.cuda(), 2.0 ** -24 if dtype == torch.float32 else 1e-12)
+    assert torch.equal(host.value, dev.value.cpu())
+    assert torch.equal(host.plan.s, dev.plan.s.cpu()) and torch.equal(host.mults, dev.mults.cpu())

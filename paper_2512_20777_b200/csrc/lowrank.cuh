@@ -113,8 +113,10 @@ template <typename T, int TP>
 struct Lr {
   static constexpr int NT = 256;
   static constexpr int NC = 64;       // column / row / k chunk of the n-sized dimensions
-  static constexpr int LDP = TP + 1;  // t x t tiles and the A1 row tile
-  static constexpr int LDC = NC + 1;  // A2 / Y chunks
+  // fp64: strides = 8 banks mod 32 so the DMMA fragment walks of phase 3 are
+  // conflict-free; fp32: odd strides for the FMA walks
+  static constexpr int LDP = sizeof(T) == 8 ? TP + 4 : TP + 1;  // t x t tiles and the A1 row tile
+  static constexpr int LDC = sizeof(T) == 8 ? NC + 4 : NC + 1;  // A2 / Y chunks
   static constexpr int kSlot = TP * LDP;
   // slot 0 = psi, 1..6 = V^p, 7 = scratch
   static constexpr int kSA = 8 * kSlot;
@@ -352,6 +354,46 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
               SB[rr * L::LDP + b] = (rr < rcn && b < t) ? a1[(size_t)(r0 + rr) * t + b] : T(0);
             }
             __syncthreads();
+            if constexpr (sizeof(T) == 8) {
+              // fp64: the 64x64 tile on DMMA -- warp w owns rows 8w..8w+7,
+              // all eight 8-column tiles; k = TP in steps of 4
+              const int w = tid / 32, g = (tid % 32) / 4, q = tid % 4;
+              double d[8][2];
+#pragma unroll
+              for (int C = 0; C < 8; ++C) d[C][0] = d[C][1] = 0.0;
+#pragma unroll
+              for (int s4 = 0; s4 < TP / 4; ++s4) {
+                const double av = SB[(8 * w + g) * L::LDP + 4 * s4 + q];
+#pragma unroll
+                for (int C = 0; C < 8; ++C) {
+                  const double bv = SY[(4 * s4 + q) * L::LDC + 8 * C + g];
+                  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                               : "+d"(d[C][0]), "+d"(d[C][1])
+                               : "d"(av), "d"(bv));
+                }
+              }
+              const int row = r0 + 8 * w + g;
+              if (row < n) {
+#pragma unroll
+                for (int C = 0; C < 8; ++C) {
+                  const int col = c0 + 8 * C + 2 * q;
+                  const double v0 = (row == col) ? d[C][0] + 1.0 : d[C][0];
+                  const double v1 = (row == col + 1) ? d[C][1] + 1.0 : d[C][1];
+                  double* xp = x + (size_t)row * n + col;
+                  if (col + 1 < n && (n % 2) == 0 && (((uintptr_t)x) & 15) == 0) {  // 16-byte aligned pair
+                    *reinterpret_cast<double2*>(xp) = make_double2(v0, v1);
+                    bo |= !isfinite(v0) || !isfinite(v1);
+                  } else if (col < n) {
+                    xp[0] = v0;
+                    bo |= !isfinite(v0);
+                    if (col + 1 < n) {
+                      xp[1] = v1;
+                      bo |= !isfinite(v1);
+                    }
+                  }
+                }
+              }
+            } else {
             T o[4][4];
 #pragma unroll
             for (int ii = 0; ii < 4; ++ii)
@@ -383,6 +425,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
                 }
               }
             }
+            }  // fp32 FMA tile
             __syncthreads();
           }
         }

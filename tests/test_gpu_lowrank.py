@@ -243,3 +243,14 @@ def test_lowrank_kernel_variants_agree(tmp_path, env):
     assert np.array_equal(outs["default"][1], outs[env][1])
     err = _rel1(outs["default"][0], outs[env][0])
     assert err.max() <= 1e-12, err.max()
+
+
+def test_lowrank_leading_batch_dims():
+    rng = np.random.default_rng(77)
+    A1, A2 = _gen(rng, 6, 40, 5, 0.2, 3.0)
+    a1 = torch.as_tensor(A1, device="cuda").reshape(2, 3, 40, 5)
+    a2 = torch.as_tensor(A2, device="cuda").reshape(2, 3, 5, 40)
+    r = X.expm_lowrank(X.LowRankPair(a1, a2), 1e-10)
+    assert r.value.shape == (2, 3, 40, 40) and r.plan.m.shape == (2, 3)
+    flat = X.expm_lowrank(X.LowRankPair(a1.reshape(6, 40, 5), a2.reshape(6, 5, 40)), 1e-10)
+    assert torch.equal(r.value.reshape(6, 40, 40), flat.value)

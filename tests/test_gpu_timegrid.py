@@ -83,3 +83,12 @@ def test_timegrid_errors():
         X.expm_timegrid(A * 1e30, torch.tensor([1e10]), 1e-6)
     r = X.expm_timegrid(A, torch.zeros(0), 1e-6)
     assert r.value.shape == (0, 80, 80)
+
+
+def test_timegrid_negative_times_ps_fp32():
+    """Negative times (the inverse flow e^{-tA}) and the PS scheme on the shared-power path."""
+    rng = np.random.default_rng(23)
+    n = 128
+    A = (rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32)
+    t = np.array([-3.0, -1.25, -0.01, 0.5, 2.75], np.float32)
+    _check(A, t, 2.0 ** -24, "ps", torch.float32, 1e-5)

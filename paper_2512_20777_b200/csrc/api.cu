@@ -171,10 +171,11 @@ static int launch_lowrank_warp(const T* A1, const T* A2, T* X, int64_t batch, in
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
-static int launch_lowrank_dmma(const double* A1, const double* A2, double* X, int64_t batch, double eps, LrOut po,
-                               cudaStream_t st) {
+template <bool FULL>
+static int launch_lowrank_dmma(const double* A1, const double* A2, double* X, int64_t batch, int n, int t,
+                               double eps, LrOut po, cudaStream_t st) {
   using L = LrD;
-  auto kern = expm_lowrank_dmma_kernel;
+  auto kern = expm_lowrank_dmma_kernel<FULL>;
   static int occ = -1;
   if (occ < 0) {
     if (L::kSmem > 48 * 1024 &&
@@ -188,7 +189,7 @@ static int launch_lowrank_dmma(const double* A1, const double* A2, double* X, in
   const int64_t ctas = (batch + L::WARPS - 1) / L::WARPS;
   const int64_t persistent = (int64_t)sm_count() * occ;
   const int grid = (int)(ctas < persistent ? ctas : persistent);
-  kern<<<grid, L::NT, L::kSmem, st>>>(A1, A2, X, batch, log2(eps), po);
+  kern<<<grid, L::NT, L::kSmem, st>>>(A1, A2, X, batch, n, t, log2(eps), po);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
@@ -199,12 +200,14 @@ static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n
   static const bool no_dmma = getenv("EXPMB_LR_NO_DMMA") != nullptr;
   // the warp kernels use 16-byte vector accesses of the factors / result
   const bool a16 = (((uintptr_t)A1 | (uintptr_t)A2 | (uintptr_t)X) % 16) == 0;
-  if (!cta_only && a16 && t <= 8 && n <= 64) {
-    if (t == 8 && n == 64) {
-      if constexpr (sizeof(T) == 8)
-        if (!no_dmma) return launch_lowrank_dmma((const double*)A1, (const double*)A2, (double*)X, batch, eps, po, st);
-      return launch_lowrank_warp<T, true>(A1, A2, X, batch, n, t, eps, po, st);
+  if constexpr (sizeof(T) == 8)
+    if (!cta_only && !no_dmma && t <= 8 && n <= 64) {
+      if (a16 && t == 8 && n == 64)
+        return launch_lowrank_dmma<true>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
+      return launch_lowrank_dmma<false>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
     }
+  if (!cta_only && a16 && t <= 8 && n <= 64) {
+    if (t == 8 && n == 64) return launch_lowrank_warp<T, true>(A1, A2, X, batch, n, t, eps, po, st);
     return launch_lowrank_warp<T, false>(A1, A2, X, batch, n, t, eps, po, st);
   }
   if (t <= 8) return launch_lowrank<T, 8>(A1, A2, X, batch, n, t, eps, po, st);

@@ -860,10 +860,16 @@ __device__ __forceinline__ void lr_mm8(const double* A, const double* B, int g, 
 
 __device__ __forceinline__ int hi_abs(double v) { return __double2hiint(v) & 0x7fffffff; }
 
-__global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __restrict__ A1,
+// FULL: n = 64, t = 8 with 16-byte vector accesses.  Otherwise any n <= 64,
+// t <= 8: the factors are zero-padded to 64 x 8 / 8 x 64 in shared memory
+// (the padding stays exactly zero through V, psi(V) and Y, so every product
+// is the padded one), only the ceil(n/8)^2 output tiles are computed, and
+// loads / stores are scalar (no alignment requirement).
+template <bool FULL>
+__global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double* __restrict__ A1,
                                                                 const double* __restrict__ A2,
-                                                                double* __restrict__ X, int64_t batch,
-                                                                double log_eps, LrOut po) {
+                                                                double* __restrict__ X, int64_t batch, int n,
+                                                                int t, double log_eps, LrOut po) {
   using L = LrD;
   extern __shared__ __align__(16) unsigned char lrd_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -874,27 +880,59 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
   double* P = base + L::kP;
   const int own = lr_sw8(g, 2 * q);  // this lane's entry pair in every t x t tile
   const int64_t nw = (int64_t)gridDim.x * L::WARPS;
+  const int nt = FULL ? 512 : n * t, nn = FULL ? 4096 : n * n;
+  const int nT = FULL ? 8 : (n + 7) >> 3;  // output tiles per dimension
+  const float inv_t = 1.0f / (float)t, inv_n = 1.0f / (float)n;
+  if (!FULL) {
+    for (int i = lane; i < L::kP; i += 32) base[i] = 0.0;
+    __syncwarp();
+  }
   // the factors of matrix mat + nw are loaded into registers while matrix
-  // mat is computed (16 x 16-byte loads in flight per lane)
+  // mat is computed (16 loads in flight per lane)
   double2 ra[8], rb[8];
   auto fetch = [&](int64_t mm) {
-    const double* a1 = A1 + (size_t)mm * 512;
-    const double* a2 = A2 + (size_t)mm * 512;
+    const double* a1 = A1 + (size_t)mm * nt;
+    const double* a2 = A2 + (size_t)mm * nt;
+    if (FULL) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) ra[j] = __ldcs(reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j)));
+      for (int j = 0; j < 8; ++j) ra[j] = __ldcs(reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j)));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) rb[j] = __ldcs(reinterpret_cast<const double2*>(a2 + 64 * j + 2 * lane));
+      for (int j = 0; j < 8; ++j) rb[j] = __ldcs(reinterpret_cast<const double2*>(a2 + 64 * j + 2 * lane));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i0 = lane + 64 * j, i1 = i0 + 32;
+        ra[j].x = i0 < nt ? __ldcs(a1 + i0) : 0.0;
+        ra[j].y = i1 < nt ? __ldcs(a1 + i1) : 0.0;
+        rb[j].x = i0 < nt ? __ldcs(a2 + i0) : 0.0;
+        rb[j].y = i1 < nt ? __ldcs(a2 + i1) : 0.0;
+      }
+    }
   };
   int64_t mat = (int64_t)blockIdx.x * L::WARPS + w;
   if (mat < batch) fetch(mat);
   for (; mat < batch; mat += nw) {
-    double* x = X + (size_t)mat * 4096;
+    double* x = X + (size_t)mat * nn;
     int hx1 = 0, hx2 = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int p = lane + 32 * j;
-      *reinterpret_cast<double2*>(sA1 + lr_sw8(p >> 2, 2 * (p & 3))) = ra[j];
-      *reinterpret_cast<double2*>(sY + j * L::LDY + 2 * lane) = rb[j];
+      if (FULL) {
+        const int p = lane + 32 * j;
+        *reinterpret_cast<double2*>(sA1 + lr_sw8(p >> 2, 2 * (p & 3))) = ra[j];
+        *reinterpret_cast<double2*>(sY + j * L::LDY + 2 * lane) = rb[j];
+      } else {
+        // element i of the n x t / t x n factors -> (row, col); the float
+        // quotient is exact enough (i < 512, fractional gap >= 1/128)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 64 * j + 32 * h;
+          if (i < nt) {
+            const int r1 = (int)(((float)i + 0.5f) * inv_t), r2 = (int)(((float)i + 0.5f) * inv_n);
+            sA1[lr_sw8(r1, i - r1 * t)] = h ? ra[j].y : ra[j].x;
+            sY[r2 * L::LDY + (i - r2 * n)] = h ? rb[j].y : rb[j].x;
+          }
+        }
+      }
       hx1 = max(hx1, max(hi_abs(ra[j].x), hi_abs(ra[j].y)));
       hx2 = max(hx2, max(hi_abs(rb[j].x), hi_abs(rb[j].y)));
     }
@@ -913,7 +951,8 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
       // V = A2 A1: 16 k-steps of 4
       double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-      for (int s = 0; s < 16; ++s) lr_dmma(v0, v1, sY[g * L::LDY + 4 * s + q], sA1[lr_sw8(4 * s + q, g)]);
+      for (int s = 0; s < 16; ++s)
+        if (FULL || 4 * s < n) lr_dmma(v0, v1, sY[g * L::LDY + 4 * s + q], sA1[lr_sw8(4 * s + q, g)]);
       double* V = P + L::kSlot;
       *reinterpret_cast<double2*>(V + own) = make_double2(v0, v1);
       __syncwarp();
@@ -1027,7 +1066,7 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
           yb1[C] = sY[(q + 4) * L::LDY + 8 * C + g];
         }
         bool bo = false;
-        if (safe) {
+        if (FULL && safe) {
 #pragma unroll 2
           for (int R = 0; R < 8; ++R) {
             const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
@@ -1043,17 +1082,26 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
           }
         } else {
 #pragma unroll 1
-          for (int R = 0; R < 8; ++R) {
-            const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
-            double* xr = x + (8 * R + g) * 64 + 2 * q;
+          for (int R = 0; R < nT; ++R) {
+            const int row = 8 * R + g;
+            const double a0 = sA1[lr_sw8(row, q)], a1v = sA1[lr_sw8(row, q + 4)];
+            double* xr = x + row * (FULL ? 64 : n) + 2 * q;
 #pragma unroll
             for (int C = 0; C < 8; ++C) {
-              double d0 = (R == C && dg0) ? 1.0 : 0.0;
-              double d1 = (R == C && dg1) ? 1.0 : 0.0;
-              lr_dmma(d0, d1, a0, yb0[C]);
-              lr_dmma(d0, d1, a1v, yb1[C]);
-              *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
-              bo |= !isfinite(d0) || !isfinite(d1);
+              if (C < nT) {
+                double d0 = (R == C && dg0) ? 1.0 : 0.0;
+                double d1 = (R == C && dg1) ? 1.0 : 0.0;
+                lr_dmma(d0, d1, a0, yb0[C]);
+                lr_dmma(d0, d1, a1v, yb1[C]);
+                if (FULL) {
+                  *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
+                } else if (row < n) {
+                  const int col = 8 * C + 2 * q;
+                  if (col < n) __stcs(xr + 8 * C, d0);
+                  if (col + 1 < n) __stcs(xr + 8 * C + 1, d1);
+                }
+                if (!safe) bo |= !isfinite(d0) || !isfinite(d1);
+              }
             }
           }
         }
@@ -1062,7 +1110,7 @@ __global__ void __launch_bounds__(128) expm_lowrank_dmma_kernel(const double* __
       }
     }
     if (flags && !wrote)
-      for (int i = lane; i < 4096; i += 32) x[i] = NAN;
+      for (int i = lane; i < nn; i += 32) x[i] = NAN;
     if (lane == 0) {
       if (po.m) po.m[mat] = (int8_t)m;
       if (po.e1) po.e1[mat] = e1;

@@ -118,11 +118,14 @@ struct Lr {
   static constexpr int LDP = sizeof(T) == 8 ? TP + 4 : TP + 1;  // t x t tiles and the A1 row tile
   static constexpr int LDC = sizeof(T) == 8 ? NC + 4 : NC + 1;  // A2 / Y chunks
   static constexpr int kSlot = TP * LDP;
-  // slot 0 = psi, 1..6 = V^p, 7 = scratch
-  static constexpr int kSA = 8 * kSlot;
+  // slot 0 = psi, 1..6 = V^p, 7 = scratch.  The factor chunks SA / SB and
+  // the Y chunk SY alias slots 2.. : phase 1 is done with them before V^2 is
+  // formed, and phase 3 needs only slot 0 (psi) -- halving the footprint
+  // for t = 32 buys a second resident CTA per SM
+  static constexpr int kSA = 2 * kSlot;
   static constexpr int kSB = kSA + TP * LDC;
   static constexpr int kSY = kSB + NC * LDP;
-  static constexpr int kEnd = kSY + TP * LDC;
+  static constexpr int kEnd = (kSY + TP * LDC) > 8 * kSlot ? (kSY + TP * LDC) : 8 * kSlot;
   static constexpr size_t kSmem = ((kEnd * sizeof(T) + 15) / 16) * 16 + 16 * sizeof(double);
 };
 
@@ -174,10 +177,34 @@ __device__ int lr_select_warp0(const T* V, const T* V2, double log_eps, double* 
   return rc;
 }
 
+// fp64 DMMA (m8n8k4) accumulate: (d0, d1) += a b for one lane's fragments
+__device__ __forceinline__ void lr_dmma_acc(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // C = A B for TP x TP shared tiles.
 template <typename T, int TP>
 __device__ void lr_mm(T* C, const T* A, const T* B) {
   using L = Lr<T, TP>;
+  if constexpr (sizeof(T) == 8) {
+    // fp64: 8x8 output tiles on DMMA (m8n8k4), warp w takes tiles w, w + 8, ...
+    const int w = threadIdx.x >> 5, g = (threadIdx.x >> 2) & 7, q = threadIdx.x & 3;
+    constexpr int NTL = TP / 8;
+    for (int tile = w; tile < NTL * NTL; tile += L::NT / 32) {
+      const int R = tile / NTL, Cc = tile % NTL;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int s4 = 0; s4 < TP / 4; ++s4)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(d0), "+d"(d1)
+                     : "d"(A[(8 * R + g) * L::LDP + 4 * s4 + q]), "d"(B[(4 * s4 + q) * L::LDP + 8 * Cc + g]));
+      C[(8 * R + g) * L::LDP + 8 * Cc + 2 * q] = d0;
+      C[(8 * R + g) * L::LDP + 8 * Cc + 2 * q + 1] = d1;
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < TP * TP; e += L::NT) {
     const int r = e / TP, c = e % TP;
     T acc = 0;
@@ -192,8 +219,12 @@ __device__ void lr_fill_nan(T* x, size_t nn) {
   for (size_t i = threadIdx.x; i < nn; i += Lr<T, TP>::NT) x[i] = (T)NAN;
 }
 
+#ifndef LR_T32_MINB
+#define LR_T32_MINB 3
+#endif
+
 template <typename T, int TP>
-__global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
+__global__ void __launch_bounds__(256, (TP <= 16 ? 4 : LR_T32_MINB)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
                                                            T* __restrict__ X, int64_t batch, int n, int t,
                                                            double log_eps, LrOut po) {
   using L = Lr<T, TP>;
@@ -220,6 +251,9 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0;
     const int g = NE >= 256 ? 0 : tid / NE;
+    constexpr int NTL = TP / 8;
+    const int dw = tid >> 5, dg = (tid >> 2) & 7, dq = tid & 3;
+    double dv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     bool bad = false;
     for (int k0 = 0; k0 < n; k0 += L::NC) {
       const int kc = min(L::NC, n - k0);
@@ -242,6 +276,20 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
         SB[kk * L::LDP + b] = v;
       }
       __syncthreads();
+      if constexpr (sizeof(T) == 8) {
+        // fp64: 8x8 tiles of V on DMMA, warp w owns tiles w and w + 8
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int tile = dw + 8 * i;
+          if (tile < NTL * NTL) {
+            const int TR = tile / NTL, TC = tile % NTL;
+#pragma unroll 4
+            for (int s4 = 0; s4 < L::NC / 4; ++s4)
+              lr_dmma_acc(dv[i][0], dv[i][1], SA[(8 * TR + dg) * L::LDC + 4 * s4 + dq],
+                          SB[(4 * s4 + dq) * L::LDP + 8 * TC + dg]);
+          }
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int e = NE >= 256 ? tid + 256 * r : tid % NE;
@@ -250,9 +298,20 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
         for (int kk = g; kk < L::NC; kk += G) s = fma(SA[a * L::LDC + kk], SB[kk * L::LDP + b], s);
         acc[r] = s;
       }
+      }
       __syncthreads();
     }
-    if (G > 1) {
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int tile = dw + 8 * i;
+        if (tile < NTL * NTL) {
+          const int TR = tile / NTL, TC = tile % NTL;
+          V[(8 * TR + dg) * L::LDP + 8 * TC + 2 * dq] = dv[i][0];
+          V[(8 * TR + dg) * L::LDP + 8 * TC + 2 * dq + 1] = dv[i][1];
+        }
+      }
+    } else if (G > 1) {
       SY[tid] = acc[0];
       __syncthreads();
       if (tid < NE) {
@@ -339,12 +398,25 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? 4 : 1)) expm_lowrank_kernel(c
             SA[a * L::LDC + jj] = (a < t && jj < cc) ? a2[(size_t)a * n + c0 + jj] : T(0);
           }
           __syncthreads();
+          if constexpr (sizeof(T) == 8) {
+            // fp64: Y = psi A2 chunk on DMMA, (TP/8) x 8 tiles over 8 warps
+            for (int tile = dw; tile < NTL * 8; tile += 8) {
+              const int TR = tile >> 3, TC = tile & 7;
+              double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+              for (int s4 = 0; s4 < TP / 4; ++s4)
+                lr_dmma_acc(y0, y1, Q[(8 * TR + dg) * L::LDP + 4 * s4 + dq], SA[(4 * s4 + dq) * L::LDC + 8 * TC + dg]);
+              SY[(8 * TR + dg) * L::LDC + 8 * TC + 2 * dq] = y0;
+              SY[(8 * TR + dg) * L::LDC + 8 * TC + 2 * dq + 1] = y1;
+            }
+          } else {
           for (int e = tid; e < TP * L::NC; e += L::NT) {
             const int b = e / L::NC, jj = e % L::NC;
             T s = 0;
 #pragma unroll 8
             for (int a = 0; a < TP; ++a) s = fma(Q[b * L::LDP + a], SA[a * L::LDC + jj], s);
             SY[b * L::LDC + jj] = s;
+          }
           }
           __syncthreads();
           for (int r0 = 0; r0 < n; r0 += L::NC) {

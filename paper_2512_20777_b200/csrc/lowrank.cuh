@@ -219,12 +219,15 @@ __device__ void lr_fill_nan(T* x, size_t nn) {
   for (size_t i = threadIdx.x; i < nn; i += Lr<T, TP>::NT) x[i] = (T)NAN;
 }
 
+#ifndef LR_T16_MINB
+#define LR_T16_MINB 4
+#endif
 #ifndef LR_T32_MINB
 #define LR_T32_MINB 3
 #endif
 
 template <typename T, int TP>
-__global__ void __launch_bounds__(256, (TP <= 16 ? 4 : LR_T32_MINB)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
+__global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
                                                            T* __restrict__ X, int64_t batch, int n, int t,
                                                            double log_eps, LrOut po) {
   using L = Lr<T, TP>;

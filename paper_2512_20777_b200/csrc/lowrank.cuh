@@ -374,12 +374,23 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
             lr_mm<T, TP>(S7, Q, P + j * L::kSlot);
             __syncthreads();
           }
-          for (int e = tid; e < NE; e += L::NT) {
-            const int off = (e / TP) * L::LDP + e % TP;
-            T q = (e / TP == e % TP) ? (T)lr_inv_fact(lo + 1) : T(0);
-            for (int tt = 1; tt <= hi - lo; ++tt)
-              q = fma((T)lr_inv_fact(lo + tt + 1), P[tt * L::kSlot + off], q);
-            Q[off] = (r < k - 1) ? S7[off] + q : q;
+          // coefficients c_{lo+1..hi+1} hoisted (hi - lo <= j <= 6), the
+          // element loop unrolled over a thread's NE / NT entries
+          T cf[7];
+#pragma unroll
+          for (int tt = 0; tt < 7; ++tt) cf[tt] = tt <= hi - lo ? (T)lr_inv_fact(lo + tt + 1) : T(0);
+          constexpr int EPT = (NE + L::NT - 1) / L::NT;
+#pragma unroll
+          for (int u = 0; u < EPT; ++u) {
+            const int e = tid + u * L::NT;
+            if (NE % L::NT == 0 || e < NE) {
+              const int er = e / TP, ec = e % TP, off = er * L::LDP + ec;
+              T q = er == ec ? cf[0] : T(0);
+#pragma unroll
+              for (int tt = 1; tt < 7; ++tt)
+                if (tt <= hi - lo) q = fma(cf[tt], P[tt * L::kSlot + off], q);
+              Q[off] = (r < k - 1) ? S7[off] + q : q;
+            }
           }
           __syncthreads();
         }

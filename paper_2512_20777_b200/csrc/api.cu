@@ -171,11 +171,11 @@ static int launch_lowrank_warp(const T* A1, const T* A2, T* X, int64_t batch, in
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
-template <bool FULL>
-static int launch_lowrank_dmma(const double* A1, const double* A2, double* X, int64_t batch, int n, int t,
+template <typename TI, bool FULL>
+static int launch_lowrank_dmma(const TI* A1, const TI* A2, TI* X, int64_t batch, int n, int t,
                                double eps, LrOut po, cudaStream_t st) {
   using L = LrD;
-  auto kern = expm_lowrank_dmma_kernel<FULL>;
+  auto kern = expm_lowrank_dmma_kernel<TI, FULL>;
   static int occ = -1;
   if (occ < 0) {
     if (L::kSmem > 48 * 1024 &&
@@ -200,12 +200,13 @@ static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n
   static const bool no_dmma = getenv("EXPMB_LR_NO_DMMA") != nullptr;
   // the warp kernels use 16-byte vector accesses of the factors / result
   const bool a16 = (((uintptr_t)A1 | (uintptr_t)A2 | (uintptr_t)X) % 16) == 0;
-  if constexpr (sizeof(T) == 8)
-    if (!cta_only && !no_dmma && t <= 8 && n <= 64) {
-      if (a16 && t == 8 && n == 64)
-        return launch_lowrank_dmma<true>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
-      return launch_lowrank_dmma<false>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);
-    }
+  // fp64 on DMMA; fp32 stays on the FFMA warp kernel (measured faster:
+  // 97 vs 177 us at n = 64, t = 8 through the binary64 DMMA kernel)
+  if (!cta_only && !no_dmma && t <= 8 && n <= 64 && (sizeof(T) == 8 || getenv("EXPMB_LR_F32_DMMA"))) {
+    if constexpr (sizeof(T) == 8)
+      if (a16 && t == 8 && n == 64) return launch_lowrank_dmma<T, true>(A1, A2, X, batch, n, t, eps, po, st);
+    return launch_lowrank_dmma<T, false>(A1, A2, X, batch, n, t, eps, po, st);
+  }
   if (!cta_only && a16 && t <= 8 && n <= 64) {
     if (t == 8 && n == 64) return launch_lowrank_warp<T, true>(A1, A2, X, batch, n, t, eps, po, st);
     return launch_lowrank_warp<T, false>(A1, A2, X, batch, n, t, eps, po, st);

@@ -951,11 +951,15 @@ __device__ __forceinline__ int hi_abs(double v) { return __double2hiint(v) & 0x7
 // (the padding stays exactly zero through V, psi(V) and Y, so every product
 // is the padded one), only the ceil(n/8)^2 output tiles are computed, and
 // loads / stores are scalar (no alignment requirement).
-template <bool FULL>
-__global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double* __restrict__ A1,
-                                                                const double* __restrict__ A2,
-                                                                double* __restrict__ X, int64_t batch, int n,
+// TI = float: fp32 factors / result, computed in binary64 on the same DMMA
+// path (the products are exact-er than the fp32 reference's; the result is
+// rounded once on the store, and the overflow bound uses the fp32 range).
+template <typename TI, bool FULL>
+__global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const TI* __restrict__ A1,
+                                                                const TI* __restrict__ A2,
+                                                                TI* __restrict__ X, int64_t batch, int n,
                                                                 int t, double log_eps, LrOut po) {
+  static_assert(!FULL || sizeof(TI) == 8, "the vector-load variant is fp64 only");
   using L = LrD;
   extern __shared__ __align__(16) unsigned char lrd_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -977,9 +981,9 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
   // mat is computed (16 loads in flight per lane)
   double2 ra[8], rb[8];
   auto fetch = [&](int64_t mm) {
-    const double* a1 = A1 + (size_t)mm * nt;
-    const double* a2 = A2 + (size_t)mm * nt;
-    if (FULL) {
+    const TI* a1 = A1 + (size_t)mm * nt;
+    const TI* a2 = A2 + (size_t)mm * nt;
+    if constexpr (FULL) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) ra[j] = __ldcs(reinterpret_cast<const double2*>(a1 + 2 * (lane + 32 * j)));
 #pragma unroll
@@ -988,21 +992,21 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int i0 = lane + 64 * j, i1 = i0 + 32;
-        ra[j].x = i0 < nt ? __ldcs(a1 + i0) : 0.0;
-        ra[j].y = i1 < nt ? __ldcs(a1 + i1) : 0.0;
-        rb[j].x = i0 < nt ? __ldcs(a2 + i0) : 0.0;
-        rb[j].y = i1 < nt ? __ldcs(a2 + i1) : 0.0;
+        ra[j].x = i0 < nt ? (double)__ldcs(a1 + i0) : 0.0;
+        ra[j].y = i1 < nt ? (double)__ldcs(a1 + i1) : 0.0;
+        rb[j].x = i0 < nt ? (double)__ldcs(a2 + i0) : 0.0;
+        rb[j].y = i1 < nt ? (double)__ldcs(a2 + i1) : 0.0;
       }
     }
   };
   int64_t mat = (int64_t)blockIdx.x * L::WARPS + w;
   if (mat < batch) fetch(mat);
   for (; mat < batch; mat += nw) {
-    double* x = X + (size_t)mat * nn;
+    TI* x = X + (size_t)mat * nn;
     int hx1 = 0, hx2 = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (FULL) {
+      if constexpr (FULL) {
         const int p = lane + 32 * j;
         *reinterpret_cast<double2*>(sA1 + lr_sw8(p >> 2, 2 * (p & 3))) = ra[j];
         *reinterpret_cast<double2*>(sY + j * L::LDY + 2 * lane) = rb[j];
@@ -1143,7 +1147,7 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) hy = max(hy, __shfl_xor_sync(0xffffffffu, hy, o));
         const int eA = (hx1 >> 20) - 1023, eY = (hy >> 20) - 1023;
-        const bool safe = eA + eY + 5 < 1000;
+        const bool safe = eA + eY + 5 < (sizeof(TI) == 8 ? 1000 : 120);
         // ---- out = I + A1 Y (128 DMMA), Y as B fragments ----
         double yb0[8], yb1[8];
 #pragma unroll
@@ -1156,7 +1160,7 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
 #pragma unroll 2
           for (int R = 0; R < 8; ++R) {
             const double a0 = sA1[lr_sw8(8 * R + g, q)], a1v = sA1[lr_sw8(8 * R + g, q + 4)];
-            double* xr = x + (8 * R + g) * 64 + 2 * q;
+            double* xr = reinterpret_cast<double*>(x) + (8 * R + g) * 64 + 2 * q;
 #pragma unroll
             for (int C = 0; C < 8; ++C) {
               double d0 = (R == C && dg0) ? 1.0 : 0.0;
@@ -1171,7 +1175,7 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
           for (int R = 0; R < nT; ++R) {
             const int row = 8 * R + g;
             const double a0 = sA1[lr_sw8(row, q)], a1v = sA1[lr_sw8(row, q + 4)];
-            double* xr = x + row * (FULL ? 64 : n) + 2 * q;
+            TI* xr = x + row * (FULL ? 64 : n) + 2 * q;
 #pragma unroll
             for (int C = 0; C < 8; ++C) {
               if (C < nT) {
@@ -1179,14 +1183,15 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
                 double d1 = (R == C && dg1) ? 1.0 : 0.0;
                 lr_dmma(d0, d1, a0, yb0[C]);
                 lr_dmma(d0, d1, a1v, yb1[C]);
-                if (FULL) {
+                const TI o0 = (TI)d0, o1 = (TI)d1;
+                if constexpr (FULL) {
                   *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
                 } else if (row < n) {
                   const int col = 8 * C + 2 * q;
-                  if (col < n) __stcs(xr + 8 * C, d0);
-                  if (col + 1 < n) __stcs(xr + 8 * C + 1, d1);
+                  if (col < n) __stcs(xr + 8 * C, o0);
+                  if (col + 1 < n) __stcs(xr + 8 * C + 1, o1);
                 }
-                if (!safe) bo |= !isfinite(d0) || !isfinite(d1);
+                if (!safe) bo |= !isfinite(o0) || !isfinite(o1);
               }
             }
           }
@@ -1196,7 +1201,7 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const double*
       }
     }
     if (flags && !wrote)
-      for (int i = lane; i < nn; i += 32) x[i] = NAN;
+      for (int i = lane; i < nn; i += 32) x[i] = (TI)NAN;
     if (lane == 0) {
       if (po.m) po.m[mat] = (int8_t)m;
       if (po.e1) po.e1[mat] = e1;

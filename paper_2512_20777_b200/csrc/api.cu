@@ -128,11 +128,11 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
 using namespace expmb;
 
 // Low-rank path (engine.py:198-257): one CTA per matrix, grid-strided.
-template <typename T, int TP>
-static int launch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n, int t, double eps, LrOut po,
+template <typename T, int TP, typename TI = T>
+static int launch_lowrank(const TI* A1, const TI* A2, TI* X, int64_t batch, int n, int t, double eps, LrOut po,
                           cudaStream_t st) {
   using L = Lr<T, TP>;
-  auto kern = expm_lowrank_kernel<T, TP>;
+  auto kern = expm_lowrank_kernel<T, TP, TI>;
   static int occ = -1;
   if (occ < 0) {
     if (L::kSmem > 48 * 1024 &&
@@ -212,6 +212,13 @@ static int dispatch_lowrank(const T* A1, const T* A2, T* X, int64_t batch, int n
     return launch_lowrank_warp<T, false>(A1, A2, X, batch, n, t, eps, po, st);
   }
   if (t <= 8) return launch_lowrank<T, 8>(A1, A2, X, batch, n, t, eps, po, st);
+  // fp32 t > 8: binary64 compute on the DMMA path (faster than the fp32 FFMA
+  // instantiation, which EXPMB_LR_F32_FMA keeps for A/B)
+  static const bool f32_fma = getenv("EXPMB_LR_F32_FMA") != nullptr;
+  if (sizeof(T) == 4 && !f32_fma) {
+    if (t <= 16) return launch_lowrank<double, 16, T>(A1, A2, X, batch, n, t, eps, po, st);
+    return launch_lowrank<double, 32, T>(A1, A2, X, batch, n, t, eps, po, st);
+  }
   if (t <= 16) return launch_lowrank<T, 16>(A1, A2, X, batch, n, t, eps, po, st);
   return launch_lowrank<T, 32>(A1, A2, X, batch, n, t, eps, po, st);
 }

@@ -226,9 +226,11 @@ __device__ void lr_fill_nan(T* x, size_t nn) {
 #define LR_T32_MINB 3
 #endif
 
-template <typename T, int TP>
-__global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) expm_lowrank_kernel(const T* __restrict__ A1, const T* __restrict__ A2,
-                                                           T* __restrict__ X, int64_t batch, int n, int t,
+// TI: the factor / result type (T = double, TI = float: fp32 I/O computed
+// in binary64 on the DMMA path, rounded once on the store)
+template <typename T, int TP, typename TI = T>
+__global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) expm_lowrank_kernel(const TI* __restrict__ A1, const TI* __restrict__ A2,
+                                                           TI* __restrict__ X, int64_t batch, int n, int t,
                                                            double log_eps, LrOut po) {
   using L = Lr<T, TP>;
   extern __shared__ __align__(16) unsigned char lr_smem[];
@@ -244,9 +246,9 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
   const size_t nn = (size_t)n * n;
 
   for (int64_t mat = blockIdx.x; mat < batch; mat += gridDim.x) {
-    const T* a1 = A1 + (size_t)mat * n * t;
-    const T* a2 = A2 + (size_t)mat * t * n;
-    T* x = X + (size_t)mat * nn;
+    const TI* a1 = A1 + (size_t)mat * n * t;
+    const TI* a2 = A2 + (size_t)mat * t * n;
+    TI* x = X + (size_t)mat * nn;
     T* V = P + L::kSlot;
 
     // ---- phase 1: V = A2 A1 ----------------------------------------------
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
         const int a = idx / L::NC, kk = idx % L::NC;
         T v = 0;
         if (a < t && kk < kc) {
-          v = a2[(size_t)a * n + k0 + kk];
+          v = (T)a2[(size_t)a * n + k0 + kk];
           bad |= !lr_finite(v);
         }
         SA[a * L::LDC + kk] = v;
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
         const int kk = idx / TP, b = idx % TP;
         T v = 0;
         if (b < t && kk < kc) {
-          v = a1[(size_t)(k0 + kk) * t + b];
+          v = (T)a1[(size_t)(k0 + kk) * t + b];
           bad |= !lr_finite(v);
         }
         SB[kk * L::LDP + b] = v;
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
       }
     }
     if (flags) {
-      lr_fill_nan<T, TP>(x, nn);
+      lr_fill_nan<TI, TP>(x, nn);
     } else {
       T* Q = P;
       T* S7 = P + 7 * L::kSlot;
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
       for (int e = tid; e < NE; e += L::NT) bq |= !lr_finite(Q[(e / TP) * L::LDP + e % TP]);
       if (__syncthreads_or(bq)) {
         flags = kLrNonFinite;
-        lr_fill_nan<T, TP>(x, nn);
+        lr_fill_nan<TI, TP>(x, nn);
       } else {
         // ---- phase 3: out = I + A1 (psi A2) ---------------------------------
         const int tx = tid % 16, ty = tid / 16;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
           const int cc = min(L::NC, n - c0);
           for (int idx = tid; idx < TP * L::NC; idx += L::NT) {
             const int a = idx / L::NC, jj = idx % L::NC;
-            SA[a * L::LDC + jj] = (a < t && jj < cc) ? a2[(size_t)a * n + c0 + jj] : T(0);
+            SA[a * L::LDC + jj] = (a < t && jj < cc) ? (T)a2[(size_t)a * n + c0 + jj] : T(0);
           }
           __syncthreads();
           if constexpr (sizeof(T) == 8) {
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
             const int rcn = min(L::NC, n - r0);
             for (int idx = tid; idx < L::NC * TP; idx += L::NT) {
               const int rr = idx / TP, b = idx % TP;
-              SB[rr * L::LDP + b] = (rr < rcn && b < t) ? a1[(size_t)(r0 + rr) * t + b] : T(0);
+              SB[rr * L::LDP + b] = (rr < rcn && b < t) ? (T)a1[(size_t)(r0 + rr) * t + b] : T(0);
             }
             __syncthreads();
             if constexpr (sizeof(T) == 8) {
@@ -465,16 +467,18 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
                   const int col = c0 + 8 * C + 2 * q;
                   const double v0 = (row == col) ? d[C][0] + 1.0 : d[C][0];
                   const double v1 = (row == col + 1) ? d[C][1] + 1.0 : d[C][1];
-                  double* xp = x + (size_t)row * n + col;
-                  if (col + 1 < n && (n % 2) == 0 && (((uintptr_t)x) & 15) == 0) {  // 16-byte aligned pair
+                  TI* xp = x + (size_t)row * n + col;
+                  const TI o0 = (TI)v0, o1 = (TI)v1;
+                  if (sizeof(TI) == 8 && col + 1 < n && (n % 2) == 0 && (((uintptr_t)x) & 15) == 0) {
+                    // 16-byte aligned pair
                     *reinterpret_cast<double2*>(xp) = make_double2(v0, v1);
                     bo |= !isfinite(v0) || !isfinite(v1);
                   } else if (col < n) {
-                    xp[0] = v0;
-                    bo |= !isfinite(v0);
+                    xp[0] = o0;
+                    bo |= !isfinite(o0);
                     if (col + 1 < n) {
-                      xp[1] = v1;
-                      bo |= !isfinite(v1);
+                      xp[1] = o1;
+                      bo |= !isfinite(o1);
                     }
                   }
                 }

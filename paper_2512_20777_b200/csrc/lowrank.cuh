@@ -977,6 +977,7 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const TI* __r
   const int nt = FULL ? 512 : n * t, nn = FULL ? 4096 : n * n;
   const int nT = FULL ? 8 : (n + 7) >> 3;  // output tiles per dimension
   const float inv_t = 1.0f / (float)t, inv_n = 1.0f / (float)n;
+  const bool vec = !FULL && (n & 7) == 0 && ((uintptr_t)X & (2 * sizeof(TI) - 1)) == 0;
   if (!FULL) {
     for (int i = lane; i < L::kP; i += 32) base[i] = 0.0;
     __syncwarp();
@@ -1190,6 +1191,11 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const TI* __r
                 const TI o0 = (TI)d0, o1 = (TI)d1;
                 if constexpr (FULL) {
                   *reinterpret_cast<double2*>(xr + 8 * C) = make_double2(d0, d1);
+                } else if (vec) {  // n % 8 == 0, aligned: every entry valid, pair stores
+                  if constexpr (sizeof(TI) == 8)
+                    __stcs(reinterpret_cast<double2*>(xr + 8 * C), make_double2(d0, d1));
+                  else
+                    __stcs(reinterpret_cast<float2*>(xr + 8 * C), make_float2(o0, o1));
                 } else if (row < n) {
                   const int col = 8 * C + 2 * q;
                   if (col < n) __stcs(xr + 8 * C, o0);

@@ -104,7 +104,7 @@ def test_lowrank_golden_fp32(lowrank_golden):
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_lowrank_ragged_shapes(dtype):
     rng = np.random.default_rng(7)
-    for n, t in ((1, 1), (7, 5), (8, 8), (63, 1), (64, 8), (65, 9), (100, 16), (129, 17), (200, 32), (96, 31)):
+    for n, t in ((1, 1), (7, 5), (8, 8), (32, 4), (48, 3), (24, 8), (63, 1), (64, 8), (65, 9), (100, 16), (129, 17), (200, 32), (96, 31)):
         A1, A2 = _gen(rng, 3, n, t, 0.05, 2.0 if dtype == torch.float32 else 6.0)
         eps = 1e-8 if dtype == torch.float64 else 2.0 ** -24
         r = _run(A1, A2, eps, dtype)

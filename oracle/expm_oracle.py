@@ -384,6 +384,60 @@ def near_threshold(norm1: float, norm2: float, eps: float, scheme: str = SCHEME_
     return False
 
 
+def plan_from_power_norms(norms: dict, eps: float, scheme: str = SCHEME_SASTRE):
+    """The (m, s) that select.py:164-220 picks from given power norms
+    ``norms[p] = ||W^p||_1`` (p = 1..4 as the ladder needs them; no products)."""
+    tables = PS_TABLES if scheme == SCHEME_PS else SASTRE_TABLES
+    if norms[1] == 0.0:
+        return (0, 0)
+    log_eps = math.log2(eps)
+    lw = {p: _log2(v) for p, v in norms.items()}
+    l1 = l2 = math.inf
+    m = tables.orders[-1]
+    for i, m_i in enumerate(tables.orders):
+        m = m_i
+        j, k = tables.block_pows[i], tables.block_counts[i]
+        lc1, lc2 = tables.log_tails[2 * i], tables.log_tails[2 * i + 1]
+        if m_i == 1:
+            l1, l2 = lc1 + 2 * lw[1], lc2 + 3 * lw[1]
+        elif scheme == SCHEME_PS:
+            l1, l2 = lc1 + k * lw[j] + lw[1], lc2 + k * lw[j] + lw[2]
+        else:
+            l1, l2 = lc1 + k * lw[j], lc2 + k * lw[j]
+            if j * k == m_i:
+                l1 += lw[1]
+                l2 += lw[2]
+            else:
+                l2 += lw[1]
+        if float(np.logaddexp2(l1, l2)) <= log_eps:
+            return (m, 0)
+    s = 0
+    for tt, l in ((1, l1), (2, l2)):
+        if l == -math.inf:
+            continue
+        s = max(s, math.ceil((l - log_eps) / (m + tt)))
+    return (m, min(s, MAX_SCALING))
+
+
+def near_threshold_powers(W, eps: float, scheme: str = SCHEME_SASTRE, margin: float = 1e-4) -> bool:
+    """``near_threshold`` for either scheme from the matrix itself: the plan
+    flips if any power norm ||W^p||_1 (p = 1..4 for PS, 1..2 for Sastre)
+    moves by ``margin`` log2 units."""
+    W = np.asarray(W, np.float64)
+    P, norms = W, {1: one_norm(W)}
+    for p in range(2, (4 if scheme == SCHEME_PS else 2) + 1):
+        P = P @ W
+        norms[p] = one_norm(P)
+    base = plan_from_power_norms(norms, eps, scheme)
+    for p in norms:
+        for d in (-margin, margin):
+            nn = dict(norms)
+            nn[p] = norms[p] * 2.0 ** d
+            if plan_from_power_norms(nn, eps, scheme) != base:
+                return True
+    return False
+
+
 def _plan_from_norms(norm1: float, norm2: float, eps: float):
     """Sastre ladder of select.py:180-219 on given norms (no products)."""
     if norm1 == 0.0:

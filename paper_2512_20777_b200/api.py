@@ -92,9 +92,10 @@ def _launch(W: torch.Tensor, X: torch.Tensor, eps: float, scheme_code: int,
     def p(t):
         return None if t is None else t.data_ptr()
 
-    rc = L.expmb_expm(W.data_ptr(), X.data_ptr(), B, n, dt, float(eps), scheme_code,
-                      p(m), p(s), p(e1), p(e2), p(norms), p(mults), p(nonfinite),
-                      p(ws), int(wsb), stream)
+    with torch.cuda.device(W.device):  # the library launches on the current device
+        rc = L.expmb_expm(W.data_ptr(), X.data_ptr(), B, n, dt, float(eps), scheme_code,
+                          p(m), p(s), p(e1), p(e2), p(norms), p(mults), p(nonfinite),
+                          p(ws), int(wsb), stream)
     if rc != 0:
         _raise_rc(rc)
 
@@ -124,6 +125,27 @@ def _(W, eps, scheme):
             W.new_empty(B, dtype=torch.float64), W.new_empty(B, dtype=torch.float64),
             W.new_empty(B, 2, dtype=torch.float64), W.new_empty(B, dtype=torch.int32),
             W.new_empty(B, dtype=torch.uint8))
+
+
+_PLAN_SPEC = {"m": (torch.int8, 1), "s": (torch.int8, 1), "e1": (torch.float64, 1), "e2": (torch.float64, 1),
+              "norms": (torch.float64, 2), "mults": (torch.int32, 1), "nonfinite": (torch.uint8, 1),
+              "flags": (torch.uint8, 1)}
+
+
+def _check_plan(plan: dict | None, B: int, device: torch.device, keys) -> dict:
+    """Caller-provided plan tensors are written through raw pointers: check
+    dtype, size, device and contiguity before any launch."""
+    plan = plan or {}
+    for k, v in plan.items():
+        if k not in keys:
+            raise MatrixError(f"unknown plan key {k!r}; expected {sorted(keys)}")
+        if v is None:
+            continue
+        dt, per = _PLAN_SPEC[k]
+        if (not isinstance(v, torch.Tensor) or v.dtype != dt or v.numel() != B * per or v.device != device
+                or not v.is_contiguous()):
+            raise MatrixError(f"plan[{k!r}] must be a contiguous {dt} tensor of {B * per} elements on {device}")
+    return plan
 
 
 def _validate(W: torch.Tensor, eps: float, scheme: str, allow_baseline: bool = False) -> tuple[torch.Tensor, int]:
@@ -193,9 +215,9 @@ def expm_into(W: torch.Tensor, X: torch.Tensor, eps: float, scheme: str = SCHEME
     into the plan tensors of ``plan`` (keys m, s, e1, e2, norms, mults, nonfinite).
     No host synchronisation for n <= 64."""
     Wc, code = _validate(W, eps, scheme, allow_baseline=True)
-    if X.shape != W.shape or X.dtype != W.dtype or not X.is_contiguous():
-        raise MatrixError("X must be a contiguous tensor shaped and typed like W")
-    plan = plan or {}
+    if X.shape != W.shape or X.dtype != W.dtype or not X.is_contiguous() or X.device != W.device:
+        raise MatrixError("X must be a contiguous tensor shaped and typed like W, on W's device")
+    plan = _check_plan(plan, Wc.shape[0], W.device, ("m", "s", "e1", "e2", "norms", "mults", "nonfinite"))
     _launch(Wc, X.view(Wc.shape), eps, code, plan.get("m"), plan.get("s"), plan.get("e1"),
             plan.get("e2"), plan.get("norms"), plan.get("mults"), plan.get("nonfinite"))
 
@@ -223,7 +245,7 @@ class HostPipeline:
         self.Xd = torch.empty_like(self.Wd)
         self.pd = {k: torch.empty(v.shape, dtype=v.dtype, device=self.dev) for k, v in self.host.items()}
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
-        c = max(1, min(int(chunks), B)) if B else 1
+        c = max(1, min(int(chunks), B, 256)) if B else 1  # expmb_expm_pipelined caps chunks at 256
         self._nchunks = c
         # chunk bounds on multiples of 4 matrices keep every slice 16-byte aligned
         self.bounds = sorted({min(B, ((B * k) // c) // 4 * 4) for k in range(c)} | {B})
@@ -271,9 +293,10 @@ class HostPipeline:
         # copy queued first, each chunk's expm on s_comp after its copy, its
         # result copied back on s_out while later chunks compute
         p = [self.pd[k].data_ptr() for k in ("m", "s", "e1", "e2", "norms", "mults", "nonfinite")]
-        rc = L.expmb_expm_pipelined(Wf.data_ptr(), self.out.data_ptr(), self.Wd.data_ptr(), self.Xd.data_ptr(),
-                                    self.B, n, self._dt, float(eps), code, *p, self._nchunks, wsp, wsb,
-                                    s_in.cuda_stream, s_comp.cuda_stream, s_out.cuda_stream)
+        with torch.cuda.device(self.dev):
+            rc = L.expmb_expm_pipelined(Wf.data_ptr(), self.out.data_ptr(), self.Wd.data_ptr(), self.Xd.data_ptr(),
+                                        self.B, n, self._dt, float(eps), code, *p, self._nchunks, wsp, wsb,
+                                        s_in.cuda_stream, s_comp.cuda_stream, s_out.cuda_stream)
         if rc != 0:
             _raise_rc(rc)
         with torch.cuda.stream(s_out):  # the small plan arrays: one copy each, after the last chunk
@@ -368,9 +391,10 @@ def _expm_lowrank_op(A1: torch.Tensor, A2: torch.Tensor, eps: float) -> tuple[
     flags = torch.empty(B, dtype=torch.uint8, device=dev)
     L = _lib.lib()
     dt = _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64
-    rc = L.expmb_expm_lowrank(A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t, dt, float(eps),
-                              m.data_ptr(), e1.data_ptr(), e2.data_ptr(), norms.data_ptr(), mults.data_ptr(),
-                              flags.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    with torch.cuda.device(dev):
+        rc = L.expmb_expm_lowrank(A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t, dt, float(eps),
+                                  m.data_ptr(), e1.data_ptr(), e2.data_ptr(), norms.data_ptr(), mults.data_ptr(),
+                                  flags.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
     return X, m, e1, e2, norms, mults, flags
@@ -433,16 +457,20 @@ def expm_lowrank_into(A1: torch.Tensor, A2: torch.Tensor, X: torch.Tensor, eps: 
     if X.shape != (B, n, n) or X.dtype != A1.dtype or not (A1.is_contiguous() and A2.is_contiguous()
                                                              and X.is_contiguous()):
         raise MatrixError("X must be contiguous [B, n, n] of the factors' dtype; factors contiguous")
+    if A1.device.type != "cuda" or A2.device != A1.device or X.device != A1.device:
+        raise MatrixError("A1, A2 and X must be on the same CUDA device")
     check_tolerance(eps, A1.dtype)
-    plan = plan or {}
+    plan = _check_plan(plan, B, A1.device, ("m", "e1", "e2", "norms", "mults", "flags"))
 
     def p(k):
         v = plan.get(k)
         return None if v is None else v.data_ptr()
-    rc = _lib.lib().expmb_expm_lowrank(
-        A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t,
-        _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64, float(eps),
-        p("m"), p("e1"), p("e2"), p("norms"), p("mults"), p("flags"), torch.cuda.current_stream(A1.device).cuda_stream)
+    with torch.cuda.device(A1.device):
+        rc = _lib.lib().expmb_expm_lowrank(
+            A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t,
+            _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64, float(eps),
+            p("m"), p("e1"), p("e2"), p("norms"), p("mults"), p("flags"),
+            torch.cuda.current_stream(A1.device).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
 
@@ -476,7 +504,13 @@ def expm_timegrid(A: torch.Tensor, times: torch.Tensor, eps: float, scheme: str 
     t = torch.as_tensor(times).to(device=A.device, dtype=A.dtype).reshape(-1).contiguous()
     K = t.shape[0]
     dev = A.device
+    if out is not None and (not isinstance(out, torch.Tensor) or tuple(out.shape) != (K, n, n)
+                            or out.dtype != A.dtype or out.device != dev or not out.is_contiguous()
+                            or out.data_ptr() % 16):
+        raise MatrixError(f"out must be a contiguous, 16-byte aligned ({K}, {n}, {n}) {A.dtype} tensor on {dev}")
     X = out if out is not None else torch.empty(K, n, n, dtype=A.dtype, device=dev)
+    if plan is not None:
+        _check_plan(plan, K, dev, ("m", "s", "e1", "e2", "norms", "mults", "nonfinite"))
     if plan is None:
         plan = {"m": torch.empty(K, dtype=torch.int8, device=dev), "s": torch.empty(K, dtype=torch.int8, device=dev),
                 "e1": torch.empty(K, dtype=torch.float64, device=dev),
@@ -487,15 +521,19 @@ def expm_timegrid(A: torch.Tensor, times: torch.Tensor, eps: float, scheme: str 
     L = _lib.lib()
     dt = _lib.EXPMB_F32 if A.dtype == torch.float32 else _lib.EXPMB_F64
     wsb = int(L.expmb_timegrid_workspace_bytes(K, n, dt))
+    if workspace is not None and (not isinstance(workspace, torch.Tensor) or workspace.dtype != torch.uint8
+                                  or workspace.device != dev or not workspace.is_contiguous()):
+        raise MatrixError(f"workspace must be a contiguous uint8 tensor on {dev}")
     if workspace is None or workspace.numel() < wsb:
         workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
 
     def p(k):
         v = plan.get(k)
         return None if v is None else v.data_ptr()
-    rc = L.expmb_expm_timegrid(A.data_ptr(), t.data_ptr(), X.data_ptr(), K, n, dt, float(eps), _SCHEMES[scheme],
-                               p("m"), p("s"), p("e1"), p("e2"), p("norms"), p("mults"), p("nonfinite"),
-                               workspace.data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream)
+    with torch.cuda.device(dev):
+        rc = L.expmb_expm_timegrid(A.data_ptr(), t.data_ptr(), X.data_ptr(), K, n, dt, float(eps), _SCHEMES[scheme],
+                                   p("m"), p("s"), p("e1"), p("e2"), p("norms"), p("mults"), p("nonfinite"),
+                                   workspace.data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
     bad = plan["nonfinite"].bool() if plan.get("nonfinite") is not None else torch.zeros(K, dtype=torch.bool,

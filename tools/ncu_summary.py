@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Summarise an ncu --set full report into the text committed under profiles/.
 
-usage: python tools/ncu_summary.py report.ncu-rep kernel_substring out.txt [note]
+usage: python tools/ncu_summary.py report.ncu-rep kernel_substring out.txt [note] [units_per_launch]
+
+units_per_launch (e.g. matrices per launch) adds warp instructions per unit.
 """
 import csv
 import io
@@ -22,6 +24,12 @@ KEYS = [
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
     "smsp__inst_executed.sum",
     "launch__registers_per_thread",
     "launch__grid_size",
@@ -41,6 +49,7 @@ def raw(rep):
 def main():
     rep, ksub, outp = sys.argv[1:4]
     note = sys.argv[4] if len(sys.argv) > 4 else ""
+    units = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
     hdr, units, vals = raw(rep)
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
@@ -48,6 +57,8 @@ def main():
     for k in KEYS:
         if k in d:
             lines.append(f"{k:70s} {d[k]:>16s} {u.get(k, '')}")
+    if units > 0 and "smsp__inst_executed.sum" in d:
+        lines.append(f"{'warp instructions per unit':70s} {float(d['smsp__inst_executed.sum'].replace(',', '')) / units:16.1f}")
     stalls = [(k, d[k]) for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
     stalls = sorted(stalls, key=lambda kv: -float(kv[1].replace(",", "") or 0))
     tot = sum(float(v.replace(",", "") or 0) for _, v in stalls) or 1

@@ -5,17 +5,22 @@
 
 One "step" = one call of the hot path (expm over the whole batch of the
 config).  Default workload: BASELINE.json configs[1] = C2 (65536 x 16x16 fp32
-skew-symmetric, tol 2^-24).  Under torchrun (N > 1) every rank exponentiates
-its own batch (global indices rank*B .. rank*B+B-1; weak scaling, no
-collective on the data path); the step time is the max over ranks.
+skew-symmetric, tol 2^-24); the same line carries ``per_config`` with C1, C3,
+C4 and C5 measured the same way (fewer steps).  Under torchrun (N > 1) the
+config's fixed global batch is split into rank-ordered shards
+(shard.shard_range; strong scaling, ``--scaling weak`` gives every rank a full
+batch), with no collective on the data path; the step time is the max over
+ranks of device time, and ``e2e_gather`` repeats the step with the final NCCL
+gather of every result into rank 0.
 
 Printed JSON line (rank 0):
-  value       whole-job exps/s with inputs resident in HBM (device-timed)
-  e2e         exps/s through the public API from pinned host memory, H2D of W
-              and D2H of e^W + plan inside the timed region
-  roofline    dominant kernel vs its bound (HBM bytes and useful FLOPs)
-  cpu_baseline the CPU oracle port timed on this host (bounded sample)
-`--impl reference` times the reference algorithm's CPU port (oracle/) instead.
+  value        whole-job exps/s with inputs resident in HBM (device-timed)
+  e2e          exps/s through the public API from pinned host memory, H2D of W
+               and D2H of e^W + plan inside the timed region
+  roofline     dominant kernel vs its bound (HBM bytes or useful FLOPs)
+  cpu_baseline the reference's CPU path on this host (the unmodified expmkit
+               from baseline/_ref, else the oracle port)
+`--impl reference` times that CPU path alone, on the same config.
 """
 
 from __future__ import annotations
@@ -55,7 +60,10 @@ def _make_l2_flush(flush):
         if read_back:
             torch.sum(flush, dim=0, keepdim=True, out=sink)
     return l2_flush
-CPU_SAMPLE = {"C1": 1024, "C2": 16384, "C3": 48, "C4": 6, "C5": 3}
+# matrices per CPU-baseline sample (our line) and per reference-arm step:
+# the whole batch where it finishes in about a second, bounded samples above
+CPU_SAMPLE = {"C1": 1024, "C2": 65536, "C3": 512, "C4": 6, "C5": 3}
+REF_STEP = {"C1": 1024, "C2": 65536, "C3": 256, "C4": 2, "C5": 1}
 
 
 def _peaks():
@@ -75,6 +83,15 @@ def _peaks():
                 out[d["pipe"]] = float(d["tflops"])
     out.setdefault("ffma_fp32", 74.4)
     out.setdefault("dfma_fp64", 37.2)
+    # fp64: the faster of the two fp64 pipes (DFMA, DMMA tensor core) -- the
+    # products run on DMMA
+    fp64 = {k: v for k, v in out.items() if k.startswith(("dfma_fp64", "dmma_")) and isinstance(v, float)}
+    out["fp64_src"] = max(fp64, key=fp64.get)
+    out["fp64"] = fp64[out["fp64_src"]]
+    if "tcgen05_i8_m128n256" in out:
+        out["i8_tops"], out["i8_src"] = out["tcgen05_i8_m128n256"], "profiles/peaks.json tcgen05_i8_m128n256 (tools/peaks.cu, measured on B200)"
+    else:
+        out["i8_tops"], out["i8_src"] = 4500.0, "nominal dense int8 (tcgen05 i8 probe not yet run)"
     return out
 
 
@@ -156,8 +173,30 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU side (the oracle port of the reference algorithm) -- rank 0 only
+# CPU side (the reference's own CPU path) -- rank 0 only
 # ---------------------------------------------------------------------------
+
+_CPU = {}  # the sample a forked worker pool reads (copy-on-write, no pickling)
+
+
+def reference_impl():
+    """The CPU implementation the baselines time: the UNMODIFIED reference
+    package ``expmkit`` installed under baseline/_ref (pip --target, see
+    DESIGN.md) when present -- kind "reference" -- else the oracle's
+    restatement of it (oracle/expm_oracle.py, pinned bit-exactly to the
+    reference's outputs) -- kind "port"."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "expmkit")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+        try:
+            import expmkit
+            return "reference", expmkit
+        except Exception:
+            pass
+    from oracle import expm_oracle
+    return "port", expm_oracle
+
 
 def _cpu_worker_init():
     # one BLAS thread per worker process (the pool supplies the parallelism;
@@ -169,39 +208,59 @@ def _cpu_worker_init():
         pass
 
 
-def _cpu_chunk(args):
-    W, eps = args
-    from oracle import expm_oracle as O
-    for i in range(W.shape[0]):
-        O.expm(W[i], eps)
-    return W.shape[0]
+def _cpu_range(args):
+    """expm (engine.py:119-152) on matrices [lo, hi) of the forked sample."""
+    lo, hi = args
+    kind, mod = reference_impl()
+    W, eps = _CPU["W"], _CPU["eps"]
+    if kind == "reference":
+        for i in range(lo, hi):
+            mod.expm(mod.Matrix(W[i]), eps, "sastre")
+    else:
+        for i in range(lo, hi):
+            mod.expm(W[i], eps)
+    return hi - lo
 
 
-def cpu_reference_rate(key: str, count: int | None = None, cores: int | None = None):
-    """exps/s of the reference algorithm (oracle port, binary64 as the reference)
-    on `count` matrices of config `key`, sharded over a process pool the way
-    the reference's own harness shards (bench.py:303-306)."""
+def cpu_reference_rate(key: str, count: int | None = None, cores: int | None = None, repeats: int = 1):
+    """exps/s of the reference's CPU path (binary64, as the reference computes
+    every dtype) on the first ``count`` matrices of config ``key``.  Orders
+    <= 256: a forked process pool with one BLAS thread per worker, the
+    reference harness's own sharding (bench.py:303-306); larger orders: one
+    process, BLAS threads on every core.  Returns (rates per repeat, cores,
+    kind, sample description)."""
+    import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
     cfg = WL.CONFIGS[key]
-    count = count or CPU_SAMPLE[key]
+    count = min(cfg.batch, count or CPU_SAMPLE[key])
     cores = cores or os.cpu_count() or 1
-    W = WL.generate(key, indices=np.arange(count)).astype(np.float64)
-    if cfg.n >= 256:
-        # large orders: one process, BLAS threads on every core (BASELINE.md mode 1)
-        t0 = time.perf_counter()
-        done = _cpu_chunk((W, cfg.eps))
-        dt = time.perf_counter() - t0
-        mode = "serial expm loop, multithreaded BLAS"
-    else:
-        # small orders: process pool, one BLAS thread each (reference bench.py:303-306; mode 2)
-        pieces = np.array_split(W, max(1, min(count, cores * 4)))
-        with ProcessPoolExecutor(max_workers=cores, initializer=_cpu_worker_init) as pool:
-            list(pool.map(_cpu_chunk, [(pieces[0][:1], cfg.eps)] * min(cores, 2)))  # warm workers
+    kind, _ = reference_impl()
+    _CPU["W"] = WL.generate(key, indices=np.arange(count)).astype(np.float64)
+    _CPU["eps"] = cfg.eps
+    rates = []
+    if cfg.n > 256:
+        for _ in range(repeats):
             t0 = time.perf_counter()
-            done = sum(pool.map(_cpu_chunk, [(p, cfg.eps) for p in pieces]))
-            dt = time.perf_counter() - t0
-        mode = f"process pool x{cores}, 1 BLAS thread each"
-    return done / dt, cores, f"{done} matrices of {key} ({cfg.n}x{cfg.n}, fp64 as the reference computes; {mode})"
+            done = _cpu_range((0, count))
+            rates.append(done / (time.perf_counter() - t0))
+        mode = "one process, multithreaded BLAS"
+        used = cores
+    else:
+        step = max(1, min(256, -(-count // (cores * 4))))
+        ranges = [(a, min(count, a + step)) for a in range(0, count, step)]
+        with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork"),
+                                 initializer=_cpu_worker_init) as pool:
+            list(pool.map(_cpu_range, [(0, 1)] * cores))  # warm every worker (imports)
+            for _ in range(repeats):
+                t0 = time.perf_counter()
+                done = sum(pool.map(_cpu_range, ranges))
+                rates.append(done / (time.perf_counter() - t0))
+        mode = f"fork pool x{cores}, 1 BLAS thread each (reference bench.py:303-306)"
+        used = cores
+    what = "unmodified expmkit from baseline/_ref" if kind == "reference" else "oracle port of expmkit"
+    sample = (f"{count} of {cfg.batch} matrices of {key} ({cfg.n}x{cfg.n}, binary64 as the reference computes; "
+              f"{what}; {mode})")
+    return rates, used, kind, sample
 
 
 # ---------------------------------------------------------------------------
@@ -216,29 +275,33 @@ def _dist_env():
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (the unmodified expmkit from baseline/_ref, else the oracle port) on this
+    host's cores, on the same config / metric as our arm.  Each step
+    exponentiates REF_STEP[config] matrices of the config (C1, C2: the whole
+    batch, so the config is the same; larger orders: a bounded sample)."""
     ws, rank, _ = _dist_env()
     if rank != 0:
         return
     cfg = WL.CONFIGS[args.config]
-    count = CPU_SAMPLE[args.config]
-    for _ in range(args.warmup):
-        cpu_reference_rate(args.config, max(1, count // 8))
-    rates = []
+    count = REF_STEP[args.config]
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        r, cores, sample = cpu_reference_rate(args.config, count)
-        rates.append(r)
+    rates, cores, kind, sample = cpu_reference_rate(args.config, count, repeats=args.warmup + args.steps)
     wall = time.perf_counter() - t0
+    rates = rates[args.warmup:]
     value = statistics.median(rates)
     line = {
         "impl": "reference", "metric": "matrix exponentials/s", "value": value, "unit": "exps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ms_per_step": 1e3 * count / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
         "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch": cfg.batch, "n": cfg.n, "eps": cfg.eps,
-                   "parallelism": "cpu process pool (reference bench.py:303-306)"},
-        "cpu_baseline": {"value": value, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample},
+                   "matrices_per_step": count, "same_config": count == cfg.batch,
+                   "parallelism": "cpu process pool (reference bench.py:303-306)" if cfg.n <= 256
+                   else "one process, multithreaded BLAS"},
+        "cpu_baseline": {"value": value, "unit": "exps/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "exps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
 
@@ -249,9 +312,12 @@ def run_reference(args):
 
 def _cpu_lr_chunk(args):
     A1, A2, eps = args
-    from oracle import expm_oracle as O
+    kind, mod = reference_impl()
     for i in range(A1.shape[0]):
-        O.expm_lowrank(A1[i], A2[i], eps)
+        if kind == "reference":
+            mod.expm_lowrank(mod.LowRankPair(A1[i], A2[i]), eps)
+        else:
+            mod.expm_lowrank(A1[i], A2[i], eps)
     return A1.shape[0]
 
 
@@ -267,7 +333,10 @@ def cpu_lowrank_rate(count: int = 4096, cores: int | None = None):
         t0 = time.perf_counter()
         done = sum(pool.map(_cpu_lr_chunk, [(A1[p], A2[p], eps) for p in parts]))
         dt = time.perf_counter() - t0
-    return done / dt, cores, f"{done} pairs of LR (n 64, t 8, fp64; process pool x{cores}, 1 BLAS thread each)"
+    kind, _ = reference_impl()
+    return done / dt, cores, (f"{done} pairs of LR (n 64, t 8, fp64; "
+                              f"{'unmodified expmkit' if kind == 'reference' else 'oracle port'}; "
+                              f"process pool x{cores}, 1 BLAS thread each)")
 
 
 def run_lowrank(args):
@@ -291,7 +360,8 @@ def run_lowrank(args):
         line = dict(base, impl="reference", value=value, n_gpus=args.gpus,
                     ms_per_step=1e3 * (time.perf_counter() - t0) / max(1, args.steps),
                     config={"workload": f"LR: {cfg.desc}", "batch": cfg.batch, "n": n, "t": t, "eps": cfg.eps},
-                    cpu_baseline={"value": value, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample},
+                    cpu_baseline={"value": value, "unit": "exps/s", "cores": cores, "kind": reference_impl()[0],
+                                  "sample": sample},
                     e2e={"value": value, "unit": "exps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
         print(json.dumps(line), flush=True)
         return
@@ -405,7 +475,7 @@ def run_lowrank(args):
         cpu = None
         if not args.no_cpu_baseline and ws == 1:  # the CPU baseline is an N=1 measurement
             r, cores, sample = cpu_lowrank_rate()
-            cpu = {"value": r, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample}
+            cpu = {"value": r, "unit": "exps/s", "cores": cores, "kind": reference_impl()[0], "sample": sample}
         hist = {}
         for mm in ms_.tolist():
             hist[str(mm)] = hist.get(str(mm), 0) + 1
@@ -439,28 +509,50 @@ def _launch_count(key, m, s, n, dtype="f64"):
     return int(6 + stages * per)
 
 
-def run_ours(args):
+def _shard_indices(cfg, rank: int, ws: int, scaling: str, batch: int = 0) -> np.ndarray:
+    """Global indices of this rank's matrices.  Strong (the
+    default): the config's fixed global batch split into contiguous rank-ordered
+    shards (shard.shard_range; C3: disjoint time points).  Weak: every rank
+    exponentiates a full batch of its own (indices rank*B ..)."""
+    from paper_2512_20777_b200.shard import shard_range
+    if scaling == "strong":
+        lo, hi = shard_range(rank, ws, batch or cfg.batch)
+        return np.arange(lo, hi)
+    B = batch or cfg.batch
+    idx = np.arange(rank * B, (rank + 1) * B)
+    return idx % cfg.batch if cfg.key == "C3" else idx
+
+
+def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool = False):
+    """Device-timed and end-to-end throughput of one config on this rank's shard;
+    the JSON dict on rank 0 (None elsewhere)."""
     import torch
     import torch.distributed as dist
     import paper_2512_20777_b200 as XP
+    from paper_2512_20777_b200.shard import gather_to_rank0, max_over_ranks
 
     ws, rank, local = _dist_env()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    cfg = WL.CONFIGS[args.config]
-    B = args.batch or cfg.batch
+    cfg = WL.CONFIGS[key]
     dtype = torch.float32 if cfg.dtype == "f32" else torch.float64
     esz = 4 if cfg.dtype == "f32" else 8
-    # this rank's shard of the global batch (seeded chunks -> independent of N)
-    if cfg.key == "C3":
-        idx = np.arange(B) % cfg.batch
+    idx = _shard_indices(cfg, rank, ws, args.scaling, args.batch)
+    B = len(idx)
+    G = B * ws if args.scaling == "weak" else (args.batch or cfg.batch)
+    tg = timegrid and cfg.key == "C3"
+    if tg:
+        # time-grid path (SURVEY 8(f) rank 3): inputs are A and this rank's times only
+        A_h, t_all = WL.c3_factors()
+        A_h, t_h = torch.from_numpy(A_h), torch.from_numpy(t_all[idx % cfg.batch])
+        A_d, t_d = A_h.to(dev), t_h.to(dev)
+        tg_ws = torch.empty(max(1, int(XP._lib.lib().expmb_timegrid_workspace_bytes(B, cfg.n, 0))),
+                            dtype=torch.uint8, device=dev)
+        Wh = None
+        Xd = torch.empty(B, cfg.n, cfg.n, dtype=dtype, device=dev)
     else:
-        idx = np.arange(rank * B, (rank + 1) * B)
-    Wh = torch.from_numpy(WL.generate(cfg.key, indices=idx))
-    W = Wh.to(dev)
-    Xd = torch.empty_like(W)
+        Wh = torch.from_numpy(WL.generate(cfg.key, indices=idx))
+        W = Wh.to(dev)
+        Xd = torch.empty_like(W)
     plan = {"m": torch.empty(B, dtype=torch.int8, device=dev), "s": torch.empty(B, dtype=torch.int8, device=dev),
             "e1": torch.empty(B, dtype=torch.float64, device=dev), "e2": torch.empty(B, dtype=torch.float64, device=dev),
             "norms": torch.empty(B, 2, dtype=torch.float64, device=dev),
@@ -470,16 +562,6 @@ def run_ours(args):
     l2_flush = _make_l2_flush(flush)
     stream = torch.cuda.current_stream(dev)
 
-    tg = bool(getattr(args, "timegrid", False)) and cfg.key == "C3"
-    if tg:
-        # time-grid path: inputs are A and the times only
-        A_h, t_all = WL.c3_factors()
-        A_h, t_h = torch.from_numpy(A_h), torch.from_numpy(t_all[idx])
-        A_d, t_d = A_h.to(dev), t_h.to(dev)
-        tg_ws = torch.empty(max(1, int(XP._lib.lib().expmb_timegrid_workspace_bytes(B, cfg.n, 0))),
-                            dtype=torch.uint8, device=dev)
-        del W
-
     def step():
         if tg:
             XP.expm_timegrid(A_d, t_d, cfg.eps, args.scheme, check_finite=False, out=Xd, plan=plan,
@@ -487,7 +569,7 @@ def run_ours(args):
         else:
             XP.expm_into(W, Xd, cfg.eps, args.scheme, plan)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     torch.cuda.synchronize()
     m = plan["m"].cpu().numpy(); s = plan["s"].cpu().numpy()
@@ -498,43 +580,51 @@ def run_ours(args):
         flops = WL.useful_flops(m, s, cfg.n, args.scheme)
 
     # ---- device-timed steps, L2 flushed between steps ----------------------
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        time.sleep(0.05)  # let the sampler start
-        clk.mark("start")
-        # hold the device briefly so the host queues all K steps ahead of it:
-        # the per-step events then bracket device work only (host launch cost
-        # is what the e2e number below measures)
-        # (busy-wait: the SM clock stays up; ~0.5 ms per step covers the host's
-        # per-call overhead)
-        torch.cuda._sleep(int(2_000_000 + min(args.steps, 200) * 1_000_000))
-        # one untimed step right after the hold: the first kernel after a
-        # memory-idle spin runs ~2x slow (measured: C2 204 vs 80 us, C1 333 vs
-        # 145 us), an artifact of the hold, not of the step
-        l2_flush()
-        step()
-        for i in range(args.steps):
-            l2_flush()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-        clk.mark("end")
-    step_ms = [a.elapsed_time(b) for a, b in evs]
+        with ClockSampler(local) as clk:
+            time.sleep(0.05)  # let the sampler start
+            clk.mark("start")
+            # hold the device briefly so the host queues all K steps ahead of it:
+            # the per-step events then bracket device work only (host launch cost
+            # is what the e2e number below measures); busy-wait keeps the SM clock up
+            torch.cuda._sleep(int(2_000_000 + min(k, 200) * 1_000_000))
+            # one untimed step right after the hold: the first kernel after a
+            # memory-idle spin runs ~2x slow (measured: C2 204 vs 80 us), an
+            # artifact of the hold, not of the step
+            l2_flush()
+            fn()
+            for i in range(k):
+                l2_flush()
+                evs[i][0].record(stream)
+                fn()
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+            clk.mark("end")
+        ms = [a.elapsed_time(b) for a, b in evs]
+        tot = max_over_ranks(sum(ms), dev) if ws > 1 else sum(ms)
+        return tot / k, ms, clk.summary()
+
+    ms_per_step, step_ms, clocks = timed(step, steps)
     if os.environ.get("BENCH_STEP_TIMES"):
-        print("step ms:", " ".join(f"{x:.4f}" for x in step_ms), file=sys.stderr)
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+        print(f"{key} step ms:", " ".join(f"{x:.4f}" for x in step_ms), file=sys.stderr)
+    value = G / (ms_per_step * 1e-3)
+
+    # ---- with the final NCCL gather of e^W to rank 0 (N > 1) ---------------
+    gather = None
     if ws > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms = float(tot.item())
-    ms_per_step = total_ms / args.steps
-    value = ws * B / (ms_per_step * 1e-3)
+        def step_gather():
+            step()
+            gather_to_rank0(Xd, G)
+        g_ms, _, _ = timed(step_gather, max(2, steps // 2))
+        gather = {"value": G / (g_ms * 1e-3), "unit": "exps/s", "ms_per_step": g_ms,
+                  "gather_bytes": G * cfg.n * cfg.n * esz,
+                  "what": "each step + dist.gather of every rank's e^W into rank 0 (NCCL, rank order)"}
 
     # ---- end-to-end through the public API from pinned host memory --------
-    # HostPipeline: H2D of W, expm, D2H of e^W + plan, chunked over 3 streams
     if tg:
         Ap, tp_ = A_h.pin_memory(), t_h.pin_memory()
         Xp = torch.empty(B, cfg.n, cfg.n, dtype=dtype, pin_memory=True)
@@ -556,8 +646,8 @@ def run_ours(args):
         Wp = None
     else:
         Wp = Wh.pin_memory()
-        # chunked so copies overlap compute (measured on B200, tools/e2e_large_probe.py:
-        # C4 1056 -> 1231 exps/s at 4 chunks, C3 61.6k -> 85.1k and C5 305 -> 358 at 8)
+        # chunked so copies overlap compute (tools/e2e_large_probe.py: C4 1056 ->
+        # 1231 exps/s at 4 chunks, C3 61.6k -> 85.1k and C5 305 -> 358 at 8)
         pipe = XP.HostPipeline(B, cfg.n, dtype, chunks=8 if (cfg.n <= 64 or B >= 128) else 4, device=dev)
 
     def e2e_step():
@@ -565,123 +655,144 @@ def run_ours(args):
 
     for _ in range(2):
         e2e_step()
+    torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     e2e_ms = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2e_step()
         torch.cuda.synchronize()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = ws * B / (float(et.item()) / args.steps * 1e-3)
-    h2d = pipe.h2d_bytes
-    d2h = pipe.d2h_bytes
+    e2e_t = max_over_ranks(sum(e2e_ms), dev) / steps if ws > 1 else sum(e2e_ms) / steps
+    e2e = {"value": G / (e2e_t * 1e-3), "unit": "exps/s", "h2d_bytes_per_step": pipe.h2d_bytes,
+           "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": e2e_t}
+    mults_total = int(plan["mults"].long().sum().item())
+    del pipe, Wp, Xd, plan, flush
+    if not tg:
+        del W, Wh
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
 
-    gather_ms = None
-    if ws > 1:
-        # the final rank-ordered gather of results to rank 0 (reported, not in the step)
-        from paper_2512_20777_b200.shard import gather_to_rank0
-        dist.barrier()
-        torch.cuda.synchronize()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        full = gather_to_rank0(Xd, ws * B)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        from paper_2512_20777_b200.shard import max_over_ranks
-        gather_ms = max_over_ranks(g0.elapsed_time(g1), dev)
-        del full
+    pk = _peaks()
+    hbm_bytes = 2 * B * cfg.n * cfg.n * esz
+    tflops = flops / (ms_per_step * 1e-3) / 1e12
+    gbs = hbm_bytes / (ms_per_step * 1e-3) / 1e9
+    cpeak, cpeak_name = (pk["ffma_fp32"], "ffma_fp32") if cfg.dtype == "f32" else (pk["fp64"], pk["fp64_src"])
+    t_hbm = hbm_bytes / (pk["hbm_gbs"] * 1e9)
+    t_cmp = flops / (cpeak * 1e12)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.key}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    hbm_roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["hbm_src"],
+                "algorithmic_bytes_per_launch": hbm_bytes}
+    cmp_roof = {"bound": "fp32_ffma" if cfg.dtype == "f32" else "fp64", "achieved": tflops,
+                "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
+                "peak_source": f"profiles/peaks.json {cpeak_name} (tools/peaks.cu, measured on B200)",
+                "useful_flops_per_launch": flops}
+    # fp32 n <= 16 runs its products as 3xTF32 mma.sync (3 x 1.648e9 TC flops
+    # at 266.6 TF/s = 18.5 us < the 20.5 us HBM floor): the binding roofline is
+    # HBM.  Elsewhere: the larger of the two lower bounds.
+    tc_products = cfg.dtype == "f32" and cfg.n <= 16 and args.scheme == "sastre"
+    hbm_binds = t_hbm >= t_cmp or tc_products
+    roof = dict(hbm_roof if hbm_binds else cmp_roof)
+    if cfg.n <= 16:
+        roof["kernel"] = "expm_fused_kernel<float,16,...> (3xTF32 mma.sync)" if tc_products else "expm_fused_kernel"
+    elif cfg.n <= 64:
+        roof["kernel"] = "expm_dmma_kernel (DMMA)" if cfg.dtype == "f64" else "expm_fused_kernel"
+    else:
+        roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
+    roof["other"] = cmp_roof if hbm_binds else hbm_roof
+    if (cfg.dtype == "f32" and cfg.n >= 512 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0"
+            and not tg):
+        # products run as exact int8-slice GEMMs on tcgen05 (gemm_i8.cuh): ten
+        # int8 slice-pair products per fp32 product; the FFMA peak stays the
+        # useful-flop yardstick, the int8 view is reported beside it
+        i8_ops = 10.0 * flops
+        ffma_view = dict(roof)
+        ffma_view.pop("other", None)
+        ipk, isrc = pk["i8_tops"], pk["i8_src"]
+        roof = {"bound": "tensor", "achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": ipk,
+                "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / ipk, "traffic": None,
+                "peak_source": isrc, "executed_int8_ops_per_launch": i8_ops,
+                "kernel": "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products",
+                "other": ffma_view}
+    if tg:
+        # the time-grid path skips the evaluation products: its roofline is over
+        # the flops it executes (squarings, shared powers in fp64, the fused
+        # combination); useful_flops stays the reference's ledger
+        n3 = 2.0 * cfg.n ** 3
+        ex_flops = float(np.asarray(s, np.int64).sum()) * n3 + 15 * n3 + B * 16 * 2.0 * cfg.n ** 2
+        ex_tf = ex_flops / (ms_per_step * 1e-3) / 1e12
+        roof = {"bound": "fp32_ffma", "achieved": ex_tf, "peak": cpeak, "unit": "TFLOP/s", "frac": ex_tf / cpeak,
+                "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
+                "executed_flops_per_launch": ex_flops, "traffic": None,
+                "kernel": "gemm_stage_kernel (FFMA2) squarings + k_tg_combine",
+                "other": {"reference_ledger_flops_per_launch": flops, "ledger_tflops": tflops}}
+    cpu_line = None
+    if cpu and ws == 1:  # the CPU baseline is an N=1 measurement
+        rates, cores, kind, sample = cpu_reference_rate(cfg.key)
+        cpu_line = {"value": rates[0], "unit": "exps/s", "cores": cores, "kind": kind, "sample": sample}
+    hist = {}
+    for mm, ss in zip(m.tolist(), s.tolist()):
+        hist[f"{mm},{ss}"] = hist.get(f"{mm},{ss}", 0) + 1
+    launches = (10 + int(np.asarray(s).max())) if tg else _launch_count(cfg.key, m, s, cfg.n, cfg.dtype)
+    return {
+        "metric": "matrix exponentials/s", "value": value, "unit": "exps/s", "n_gpus": ws,
+        "steps": steps, "warmup": max(3, warmup), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
+        "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch_per_gpu": B, "global_batch": G,
+                   "n": cfg.n, "eps": cfg.eps, "scheme": args.scheme, "l2": "flushed between steps (252 MB write)",
+                   "path": "time grid: shared powers + per-time squarings (expm_timegrid)" if tg else "batched expm",
+                   "timing": "per-step CUDA events around each call, host queue primed (device held by a sleep "
+                             "before the first step), max over ranks",
+                   "parallelism": (f"{args.scaling} scaling: " + ("fixed global batch split into rank-ordered "
+                                   "shards" if args.scaling == "strong" else "a full batch per rank")
+                                   + f" x{ws}, no collective on the hot path")},
+        "useful_tflops": tflops, "hbm_gbs": gbs,
+        "roofline": roof,
+        "cpu_baseline": cpu_line,
+        "e2e": e2e,
+        "e2e_gather": gather,
+        "gpu_launches": launches * steps,
+        "clocks": clocks,
+        "plan_histogram": hist,
+        "mults_total": mults_total,
+    }
 
+
+PER_CONFIG = {"C1": (10, 3), "C3": (5, 3), "C4": (4, 3), "C5": (3, 3)}  # (steps, warmup) of the side lines
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = measure(args.config, args, args.steps, args.warmup, cpu=not args.no_cpu_baseline,
+                   timegrid=bool(args.timegrid))
+    if args.per_config and args.config == "C2" and not args.timegrid:
+        # the other BASELINE.json configs, each measured the same way (fewer steps)
+        per = {}
+        for key, (k, w) in PER_CONFIG.items():
+            r = measure(key, args, k, w, cpu=not args.no_cpu_baseline)
+            if rank == 0:
+                per[key] = {f: r[f] for f in ("value", "ms_per_step", "steps", "useful_tflops", "hbm_gbs",
+                                              "roofline", "e2e", "e2e_gather", "cpu_baseline", "clocks",
+                                              "gpu_launches", "plan_histogram")}
+                per[key]["config"] = r["config"]["workload"]
+                per[key]["global_batch"] = r["config"]["global_batch"]
+        if rank == 0:
+            line["per_config"] = per
     if rank == 0:
-        pk = _peaks()
-        hbm_bytes = 2 * B * cfg.n * cfg.n * esz
-        tflops = flops / (ms_per_step * 1e-3) / 1e12
-        gbs = hbm_bytes / (ms_per_step * 1e-3) / 1e9
-        cpeak = pk["ffma_fp32"] if cfg.dtype == "f32" else pk["dfma_fp64"]
-        t_hbm = hbm_bytes / (pk["hbm_gbs"] * 1e9)
-        t_cmp = flops / (cpeak * 1e12)
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.key}.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        hbm_roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["hbm_src"],
-                    "algorithmic_bytes_per_launch": hbm_bytes}
-        cmp_roof = {"bound": "fp32_ffma" if cfg.dtype == "f32" else "fp64_dfma", "achieved": tflops,
-                    "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
-                    "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
-                    "useful_flops_per_launch": flops}
-        # fp32 n <= 16 runs its products as 3xTF32 mma.sync (3 x 1.648e9 TC flops
-        # at 266.6 TF/s = 18.5 us < the 20.5 us HBM floor): the binding
-        # roofline is HBM.  Elsewhere: the larger of the two lower bounds.
-        tc_products = cfg.dtype == "f32" and cfg.n <= 16 and args.scheme == "sastre"
-        hbm_binds = t_hbm >= t_cmp or tc_products
-        roof = dict(hbm_roof if hbm_binds else cmp_roof)
-        if cfg.n <= 16:
-            roof["kernel"] = "expm_fused_kernel<float,16,2,8,0,2,2> (3xTF32 mma.sync)" if tc_products else "expm_fused_kernel"
-        elif cfg.n <= 64:
-            roof["kernel"] = "expm_dmma_kernel (DMMA)" if cfg.dtype == "f64" else "expm_fused_kernel"
-        else:
-            roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
-        roof["other"] = cmp_roof if hbm_binds else hbm_roof
-        if cfg.dtype == "f32" and cfg.n >= 512 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0":
-            # products run as exact int8-slice GEMMs on tcgen05 (gemm_i8.cuh): ten
-            # int8 slice-pair products per fp32 product; the FFMA peak stays the
-            # useful-flop yardstick, the int8 view is reported beside it
-            i8_ops = 10.0 * flops
-            ffma_view = dict(roof)
-            ffma_view.pop("other", None)
-            roof = {"bound": "tensor", "achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": 4500.0,
-                    "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / 4500.0, "traffic": None,
-                    "peak_source": "nominal dense int8 (no measured int8 peak on this pool)",
-                    "executed_int8_ops_per_launch": i8_ops,
-                    "kernel": "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products",
-                    "other": ffma_view}
-        if tg:
-            # the time-grid path skips the evaluation products: its roofline is
-            # over the flops it executes (squarings, shared powers in fp64, the
-            # fused combination); useful_flops stays the reference's ledger
-            n3 = 2.0 * cfg.n ** 3
-            ex_flops = float(np.asarray(s, np.int64).sum()) * n3 + 15 * n3 + B * 16 * 2.0 * cfg.n ** 2
-            ex_tf = ex_flops / (ms_per_step * 1e-3) / 1e12
-            roof = {"bound": "fp32_ffma", "achieved": ex_tf, "peak": cpeak, "unit": "TFLOP/s", "frac": ex_tf / cpeak,
-                    "peak_source": "profiles/peaks.json (tools/peaks.cu, measured on B200)",
-                    "executed_flops_per_launch": ex_flops, "traffic": None,
-                    "kernel": "gemm_stage_kernel (FFMA2) squarings + k_tg_combine",
-                    "other": {"reference_ledger_flops_per_launch": flops, "ledger_tflops": tflops}}
-        cpu = None
-        if not args.no_cpu_baseline and ws == 1:  # the CPU baseline is an N=1 measurement
-            r, cores, sample = cpu_reference_rate(cfg.key)
-            cpu = {"value": r, "unit": "exps/s", "cores": cores, "kind": "port", "sample": sample}
-        hist = {}
-        for mm, ss in zip(m.tolist(), s.tolist()):
-            hist[f"{mm},{ss}"] = hist.get(f"{mm},{ss}", 0) + 1
-        line = {
-            "metric": "matrix exponentials/s", "value": value, "unit": "exps/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": cfg.dtype, "data": "synthetic (seeded, SURVEY.md 8(d) recipe)",
-            "config": {"workload": f"{cfg.key}: {cfg.desc}", "batch_per_gpu": B, "global_batch": ws * B,
-                       "n": cfg.n, "eps": cfg.eps, "scheme": args.scheme, "l2": "flushed between steps (252 MB write)",
-                       "path": "time grid: shared powers + per-time squarings (expm_timegrid)" if tg else "batched expm",
-                       "timing": "per-step CUDA events around each call, host queue primed (device held by a sleep before the first step)",
-                       "parallelism": f"batch-sharded x{ws}, no collective on the hot path"},
-            "useful_tflops": tflops, "hbm_gbs": gbs,
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "exps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": float(et.item()) / args.steps},
-            "gpu_launches": (10 + int(np.asarray(s).max()) if tg else _launch_count(cfg.key, m, s, cfg.n, cfg.dtype)) * args.steps,
-            "clocks": clk.summary(),
-            "plan_histogram": hist,
-            "mults_total": int(plan["mults"].long().sum().item()),
-            "gather_ms": gather_ms,
-        }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
@@ -701,7 +812,12 @@ def main():
     ap.add_argument("--timegrid", action="store_true",
                     help="C3 through expm_timegrid (one A, many t_k: shared powers, SURVEY 8(f) rank 3)")
     ap.add_argument("--scheme", default="sastre", choices=["sastre", "ps", "baseline"],
-                    help="evaluation route (baseline = Alg. 1, the paper's comparator; n <= 64)")
+                    help="evaluation route (baseline = Alg. 1, the paper's comparator)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's global batch split over the ranks (default); weak: a batch per rank")
+    ap.add_argument("--per-config", dest="per_config", action="store_true", default=True,
+                    help="with the default C2 line, also measure C1, C3, C4, C5 into 'per_config' (default)")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false")
     args = ap.parse_args()
     if args.config == "LR":
         run_lowrank(args)

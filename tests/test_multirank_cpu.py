@@ -63,3 +63,57 @@ def test_gloo_world2_gather_and_max(gb):
     assert t == 2.0
     assert full.shape == (gb, 3, 3)
     assert np.array_equal(full[:, 0, 0], np.arange(gb, dtype=np.float64))
+
+
+def _work_worker(rank, world, port, gb, out_q):
+    """Each rank regenerates ITS shard of C1 from the shared seeds (bench.py's
+    strong-scaling shard, no data shipped), exponentiates it, and the results
+    come home to rank 0 in rank order.  The CPU oracle stands in for the GPU
+    kernel (no device here); the GPU analogue is tests/test_gpu_shards.py."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import bench
+    from oracle import expm_oracle as O
+    from paper_2512_20777_b200 import workloads as WL
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = WL.CONFIGS["C1"]
+    idx = bench._shard_indices(cfg, rank, world, "strong", gb)
+    W = WL.generate("C1", indices=idx)
+    vals = np.stack([O.expm(W[i], cfg.eps).value for i in range(len(idx))]) if len(idx) else np.zeros((0, 64, 64))
+    full = gather_to_rank0(torch.from_numpy(vals), gb)
+    if rank == 0:
+        out_q.put(full.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_work_equals_serial(world):
+    """'parallel == serial, bit-identical' (reference tests/test_bench.py:165-173)."""
+    from oracle import expm_oracle as O
+    from paper_2512_20777_b200 import workloads as WL
+    gb = 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_work_worker, args=(r, world, port, gb, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W = WL.generate("C1", indices=np.arange(gb))
+    serial = np.stack([O.expm(W[i], WL.CONFIGS["C1"].eps).value for i in range(gb)])
+    assert full.shape == serial.shape and np.array_equal(full, serial)
+
+
+def test_bench_shard_indices():
+    import bench
+    from paper_2512_20777_b200 import workloads as WL
+    for key in ("C2", "C3", "C5"):
+        cfg = WL.CONFIGS[key]
+        for world in (1, 2, 4, 8):
+            parts = [bench._shard_indices(cfg, r, world, "strong") for r in range(world)]
+            assert np.array_equal(np.concatenate(parts), np.arange(cfg.batch))
+            weak = [bench._shard_indices(cfg, r, world, "weak") for r in range(world)]
+            assert all(len(w) == cfg.batch for w in weak)

@@ -1,7 +1,11 @@
 // Pipe-peak microbenchmarks for the roofline denominators of this repo:
-// FFMA (fp32 SIMT), DFMA (fp64 SIMT), DMMA (mma.sync m8n8k4 f64) and
-// mma.sync m16n8k8 tf32.  Prints one JSON line per pipe.
+// FFMA (fp32 SIMT), DFMA (fp64 SIMT), DMMA (mma.sync m8n8k4 f64),
+// mma.sync m16n8k8 tf32, and the 5th-generation tensor core through
+// tcgen05.mma (kind::i8 and kind::tf32, M = 128, N = 256, operands resident in
+// shared memory, accumulators in TMEM, one issuing thread per CTA, one CTA per
+// SM).  Prints one JSON line per pipe.
 #include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 #define ITERS 4096
@@ -81,6 +85,71 @@ __global__ void k_tf32(float* out) {
   if (s == 1.2345f) out[0] = s;
 }
 
+// ---- tcgen05.mma throughput: operands stay in shared memory (128B-swizzled,
+// K-major), so the tensor pipe is the only thing measured ----
+constexpr int TC_M = 128, TC_N = 256, TC_KB = 128;  // 128-byte k-tile: 4 (i8) / 4 (tf32) MMAs per tile
+constexpr int TC_SMEM = (TC_M + TC_N) * TC_KB + 1024;
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t kdesc128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+template <int KIND>  // 0 = i8 (K = 32 per MMA), 1 = tf32 (K = 8 per MMA)
+__global__ void __launch_bounds__(128, 1) k_tcgen05(int iters, int* out) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  for (int i = threadIdx.x; i < (TC_M + TC_N) * TC_KB / 4; i += blockDim.x) reinterpret_cast<int*>(sm)[i] = 0x01010101 * (i & 3);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&tbase)), "r"(TC_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tbase;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = KIND == 0 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24))
+                                     : ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24));
+    const uint64_t ad = kdesc128(s_u32(sm)), bd = kdesc128(s_u32(sm + TC_M * TC_KB));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t a = ad + (uint64_t)((k * 32) >> 4), b = bd + (uint64_t)((k * 32) >> 4);
+        const uint32_t acc = (it | k) ? 1u : 0u;
+        if (KIND == 0)
+          asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+        else
+          asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(&bar)) : "memory");
+    asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W_%=;\n}\n" ::"r"(s_u32(&bar)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (v == 0x12345678u) out[0] = (int)v;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
+  }
+}
+
 template <typename K>
 float timeit(K launch) {
   cudaEvent_t e0, e1;
@@ -122,6 +191,19 @@ int main() {
   printf("{\"pipe\": \"dmma_m8n8k4_fp64\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 512 / (t * 1e-3) / 1e12, t);
   t = timeit([&] { k_tf32<<<blocks, threads>>>(fo); });
   printf("{\"pipe\": \"mma_sync_m16n8k8_tf32\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 2048 / (t * 1e-3) / 1e12, t);
+  {
+    int* io; cudaMalloc(&io, 64);
+    cudaFuncSetAttribute(k_tcgen05<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(k_tcgen05<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    const int it = 4096;
+    t = timeit([&] { k_tcgen05<0><<<sms, 128, TC_SMEM>>>(it, io); });
+    printf("{\"pipe\": \"tcgen05_i8_m128n256\", \"tops\": %.1f, \"tflops\": %.1f, \"ms\": %.3f}\n",
+           (double)sms * it * 4 * 2.0 * TC_M * TC_N * 32 / (t * 1e-3) / 1e12,
+           (double)sms * it * 4 * 2.0 * TC_M * TC_N * 32 / (t * 1e-3) / 1e12, t);
+    t = timeit([&] { k_tcgen05<1><<<sms, 128, TC_SMEM>>>(it, io); });
+    printf("{\"pipe\": \"tcgen05_tf32_m128n256\", \"tflops\": %.1f, \"ms\": %.3f}\n",
+           (double)sms * it * 4 * 2.0 * TC_M * TC_N * 8 / (t * 1e-3) / 1e12, t);
+  }
   printf("{\"sms\": %d, \"clock_khz\": %d}\n", sms, clk);
   return 0;
 }

@@ -85,6 +85,9 @@ def _peaks():
     out.setdefault("dfma_fp64", 37.2)
     # fp64: the faster of the two fp64 pipes (DFMA, DMMA tensor core) -- the
     # products run on DMMA
+    fp32 = {k: v for k, v in out.items() if k.startswith(("ffma_fp32", "ffma2_fp32")) and isinstance(v, float)}
+    out["fp32_src"] = max(fp32, key=fp32.get)
+    out["fp32"] = fp32[out["fp32_src"]]
     fp64 = {k: v for k, v in out.items() if k.startswith(("dfma_fp64", "dmma_")) and isinstance(v, float)}
     out["fp64_src"] = max(fp64, key=fp64.get)
     out["fp64"] = fp64[out["fp64_src"]]
@@ -681,7 +684,7 @@ def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool =
     hbm_bytes = 2 * B * cfg.n * cfg.n * esz
     tflops = flops / (ms_per_step * 1e-3) / 1e12
     gbs = hbm_bytes / (ms_per_step * 1e-3) / 1e9
-    cpeak, cpeak_name = (pk["ffma_fp32"], "ffma_fp32") if cfg.dtype == "f32" else (pk["fp64"], pk["fp64_src"])
+    cpeak, cpeak_name = (pk["fp32"], pk["fp32_src"]) if cfg.dtype == "f32" else (pk["fp64"], pk["fp64_src"])
     t_hbm = hbm_bytes / (pk["hbm_gbs"] * 1e9)
     t_cmp = flops / (cpeak * 1e12)
     traffic = None

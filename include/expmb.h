@@ -12,9 +12,11 @@
  *  - Every pointer argument of expmb_expm is DEVICE memory owned by the caller
  *    (the library never allocates; scratch comes from `workspace`).
  *  - Matrices are row-major, contiguous, [batch][n][n], dtype fp32 or fp64.
- *  - All work is enqueued on `stream` (a cudaStream_t passed as void*); the
- *    call does not synchronise the device except where noted (large-n
- *    path: one small device->host copy of the per-matrix plans).
+ *  - All work is enqueued on `stream` (a cudaStream_t passed as void*); no
+ *    call synchronises the host or the device (every path, every n: the
+ *    large-n pipeline buckets matrices by their (m, s) on the device and
+ *    every stage reads its slot count from device memory), so the calls are
+ *    capturable in CUDA graphs.
  *  - Errors in arguments are returned synchronously as negative codes
  *    (mapped by the Python layer to ToleranceError / MatrixError, exactly
  *    like select.py:72-79, matrix.py:52-55, engine.py:137).  Numerical
@@ -160,7 +162,7 @@ int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int*
  *   A          [n,n] device; t [K] device (same dtype); X [K,n,n] device
  *   m..nonfinite, scheme, eps: as expmb_expm (per time point)
  *   workspace  expmb_timegrid_workspace_bytes(K, n, dtype) bytes
- * One small device->host copy of the plans (n > 64), as the large-n path.
+ * No host synchronisation (the squaring buckets are formed on the device).
  */
 size_t expmb_timegrid_workspace_bytes(int64_t K, int32_t n, int dtype);
 int expmb_expm_timegrid(const void* A, const void* t, void* X, int64_t K, int32_t n, int dtype, double eps,

@@ -213,7 +213,7 @@ def expm_into(W: torch.Tensor, X: torch.Tensor, eps: float, scheme: str = SCHEME
     """Allocation-free variant for steady-state loops and CUDA graphs:
     writes e^W into the preallocated ``X`` (same shape/dtype) and, if given,
     into the plan tensors of ``plan`` (keys m, s, e1, e2, norms, mults, nonfinite).
-    No host synchronisation for n <= 64."""
+    No host synchronisation for any n (capturable in a CUDA graph)."""
     Wc, code = _validate(W, eps, scheme, allow_baseline=True)
     if X.shape != W.shape or X.dtype != W.dtype or not X.is_contiguous() or X.device != W.device:
         raise MatrixError("X must be a contiguous tensor shaped and typed like W, on W's device")

@@ -120,16 +120,15 @@ constexpr int kExpBias = 200;
 __device__ __forceinline__ unsigned long long exp_pack(float a) {
   return a > 0.f && a < INFINITY ? ((unsigned long long)(ilogbf(a) + kExpBias) << 20) | 1ull : 0ull;
 }
-__global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b) {
-  const int slot = blockIdx.z;
+__device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, int stage, const int* __restrict__ list,
+                                              const Bufs& b, int slot, int bx, int by) {
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
   __shared__ int cmax[32][33];
   __shared__ unsigned long long csum[32][33];
   const int n = g.n;  // a multiple of 16 on this path: groups of 4 columns are all in or all out
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int r0 = by * 32, c0 = bx * 32;
   const int i = threadIdx.x / 8, q = threadIdx.x % 8;  // row i of the tile, columns 4q..4q+3
   const int r = r0 + i, c = c0 + 4 * q;
   float lf[4] = {0.f, 0.f, 0.f, 0.f}, rf[4] = {0.f, 0.f, 0.f, 0.f};
@@ -173,6 +172,29 @@ __global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, c
     if (ss) atomicAdd(b.cc + (size_t)slot * n + c0 + cc, ss);
   }
 }
+// Units (slot, 32x32 tile) over the first *dcount slots, grid-strided.
+__global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b, const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
+  for (int64_t w = blockIdx.x; w < (int64_t)cnt * tiles; w += gridDim.x) {
+    const int slot = (int)(w / tiles), t = (int)(w - (int64_t)slot * tiles);
+    __syncthreads();  // shared tiles of the previous unit
+    i8_stats_tile(g, stage, list, b, slot, t % t32, t / t32);
+  }
+}
+
+// Zero the per-slot exponent / routing accumulators of the first *dcount slots.
+__global__ void __launch_bounds__(256) k_i8_zero(Bufs b, int n, const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  const size_t tot = (size_t)cnt * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    b.er[i] = 0;
+    b.ec[i] = 0;
+    b.rc[i] = 0ull;
+    b.cc[i] = 0ull;
+  }
+}
 
 // Route a product to this path only when every row of L and every column of
 // R is "flat": its largest entry's binary exponent exceeds the mean exponent
@@ -189,8 +211,9 @@ __device__ __forceinline__ bool flat_ok(int maxbits, unsigned long long pk) {
   return cnt > 0 && (long long)emax * cnt - esum <= (long long)kFlatBits * cnt;
 }
 __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b) {
-  const int slot = blockIdx.x;
+                                                   Bufs b, const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  for (int slot = blockIdx.x; slot < cnt; slot += gridDim.x) {
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   const bool part = make_epi(g, stage, z, e);
@@ -204,19 +227,19 @@ __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, c
   }
   flat = __syncthreads_and(flat);
   if (threadIdx.x == 0) b.ok[slot] = part && flat ? 1 : 0;
+  }
 }
 
 // One pass over 32x32 tiles: L slices row-major, R slices transposed (both K-major).
-__global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b) {
-  const int slot = blockIdx.z;
+__device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, int stage, const int* __restrict__ list,
+                                              const Bufs& b, int slot, int bx, int by) {
   if (!b.ok[slot]) return;
   const int z = list ? list[slot] : slot;
   Epi<float> e;
   if (!make_epi(g, stage, z, e)) return;
   __shared__ float tile[32][33];
   const int n = g.n;  // a multiple of 16 on this path
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int r0 = by * 32, c0 = bx * 32;
   const size_t plane = (size_t)n * b.np;
   int8_t* as = b.as + (size_t)slot * NSL * plane;
   int8_t* bs = b.bs + (size_t)slot * NSL * plane;
@@ -264,6 +287,16 @@ __global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, c
     }
   }
 }
+__global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                   Bufs b, const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
+  for (int64_t w = blockIdx.x; w < (int64_t)cnt * tiles; w += gridDim.x) {
+    const int slot = (int)(w / tiles), t = (int)(w - (int64_t)slot * tiles);
+    __syncthreads();  // the transpose tile of the previous unit
+    i8_slice_tile(g, stage, list, b, slot, t % t32, t / t32);
+  }
+}
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t accumulate) {
   asm volatile(
@@ -303,37 +336,51 @@ struct Maps {
   CUtensorMap a, b;
 };
 
-__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1)) k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g,
-                                                          int stage, const int* __restrict__ list, Bufs bf) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ double cs_sh[BN];  // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
-  __shared__ float dr_sh[BN];   // diagonal of R for this CTA's columns
-  const int slot = blockIdx.z;
-  if (!bf.ok[slot]) return;  // routed to the FFMA GEMM
-  const int z = list ? list[slot] : slot;
-  Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;  // uniform per CTA
+// Instruction descriptors for the concatenated-slice MMAs: slice i of L times
+// the R slices 0..3-i stacked along N (one operand of (4-i)*BN rows) lands in
+// the level accumulators i..3, which sit side by side in TMEM.
+__device__ __forceinline__ uint32_t idesc_n(int nrows) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nrows >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8_d(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate));
+}
 
+// Persistent, warp-specialised int8-slice GEMM stage.  The grid walks the work
+// units (slot, 128-row block, 64-column block) of the first *dcount slots;
+// warp 0 streams k-tiles through the TMA ring, warp 1 issues the MMAs into the
+// TMEM level accumulators, warps 2..5 run the fused epilogue.  The producer
+// runs ahead into the next unit while the epilogue drains the current one
+// (tmem_full / tmem_empty barriers hand the accumulators back and forth).
+__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
+k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs bf,
+           const int* __restrict__ dcount, int hcount) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ double cs_sh[BN];   // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
+  __shared__ float dr_sh[BN];    // diagonal of R for this unit's columns
+  __shared__ double red_sh[4][16];  // colnorm partials: one per epilogue warp and chunk column
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = g.n;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int KT = (n + BKB - 1) / BKB;
+  const int cnt = dcount ? *dcount : hcount;
+  const int tn = (n + BN - 1) / BN, tm = (n + BM - 1) / BM, tiles = tn * tm;
+  const int64_t total = (int64_t)cnt * tiles;
+  if ((int64_t)blockIdx.x >= total) return;  // uniform: no unit for this CTA
 
-  if (threadIdx.x < BN) {
-    const int c = n0 + threadIdx.x;
-    const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
-    cs_sh[threadIdx.x] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
-    dr_sh[threadIdx.x] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       tc::mbar_init(&full_bar[i], 1);
       tc::mbar_init(&empty_bar[i], 1);
     }
-    tc::mbar_init(&tmem_bar, 1);
+    tc::mbar_init(&tfull_bar, 1);
+    tc::mbar_init(&tempty_bar, 4);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -347,46 +394,69 @@ __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_sh;
 
+  // every role walks the same unit sequence and skips the same units
+  auto unit = [&](int64_t w, int& slot, int& z, int& bx, int& by, Epi<float>& e) -> bool {
+    slot = (int)(w / tiles);
+    const int t = (int)(w - (int64_t)slot * tiles);
+    bx = t % tn;
+    by = t / tn;
+    if (!bf.ok[slot]) return false;  // routed to the FFMA GEMM
+    z = list ? list[slot] : slot;
+    return make_epi(g, stage, z, e);
+  };
+
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: 4 L slices + 4 R slices per k-tile ----------------
-    for (int kt = 0; kt < KT; ++kt) {
-      const int st = kt % STAGES;
-      tc::mbar_wait(&empty_bar[st], ((kt / STAGES) & 1) ^ 1);
-      unsigned char* b = sm + st * STAGE_BYTES;
-      tc::mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+    uint32_t it = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+      int slot, z, bx, by;
+      Epi<float> e;
+      if (!unit(w, slot, z, bx, by, e)) continue;
+      const int m0 = by * BM, n0 = bx * BN;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int st = it % STAGES;
+        tc::mbar_wait(&empty_bar[st], ((it / STAGES) & 1) ^ 1);
+        unsigned char* b = sm + st * STAGE_BYTES;
+        tc::mbar_expect_tx(&full_bar[st], STAGE_BYTES);
 #pragma unroll
-      for (int i = 0; i < NSL; ++i) {
-        tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
-        tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
+        for (int i = 0; i < NSL; ++i) {
+          tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
+          tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer: ten slice pairs per 32-byte k-step ----------------
-    for (int kt = 0; kt < KT; ++kt) {
-      const int st = kt % STAGES;
-      tc::mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+    // ---------------- MMA issuer: 4 concatenated-slice MMAs per 32-byte k-step ----------------
+    uint32_t it = 0, u = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+      int slot, z, bx, by;
+      Epi<float> e;
+      if (!unit(w, slot, z, bx, by, e)) continue;
+      tc::mbar_wait(&tempty_bar, (u & 1) ^ 1);  // the epilogue has drained the accumulators
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t base = tc::smem_u32(sm + st * STAGE_BYTES);
-      // descriptors built once per stage; the slice / k-step offsets go into
-      // the 16-byte-unit address field (smem < 256 KB: no carry out of it)
-      const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
-      const uint32_t acc0 = (kt > 0) ? 1u : 0u;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int st = it % STAGES;
+        tc::mbar_wait(&full_bar[st], (it / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t base = tc::smem_u32(sm + st * STAGE_BYTES);
+        // descriptors built once per stage; slice / k-step offsets go into the
+        // 16-byte-unit address field (smem < 256 KB: no carry out of it)
+        const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
 #pragma unroll
-      for (int k = 0; k < BKB / 32; ++k) {
+        for (int k = 0; k < BKB / 32; ++k) {
 #pragma unroll
-        for (int lv = 0; lv < 4; ++lv) {
-#pragma unroll
-          for (int i = 0; i <= lv; ++i) {
-            const int j = lv - i;
+          for (int i = 0; i < NSL; ++i) {
             const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
-            const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + k * 32) >> 4);
-            mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (k > 0 || i > 0) ? 1u : acc0);
+            const uint64_t bd = bd0 + (uint64_t)((k * 32) >> 4);
+            // i = 0 covers every level: its first MMA of the unit initialises them all
+            mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
           }
         }
+        tc::mma_commit(&empty_bar[st]);
       }
-      tc::mma_commit(&empty_bar[st]);
+      tc::mma_commit(&tfull_bar);
+      ++u;
     }
-    tc::mma_commit(&tmem_bar);
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     // 16-column chunks keep the live arrays small enough for 2 CTAs/SM
@@ -394,14 +464,29 @@ __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 
     constexpr int CW = 16;
     const int q = warp & 3;
     const int rl = q * 32 + lane;
-    const int r = m0 + rl;
-    const bool rowok = r < n;
-    // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
-    // the int8 GEMM carries Yl Yr (each row / column scaled without its
-    // diagonal, which in the squaring phase dominates), the rest is exact
-    // elementwise work here, all summed in binary64 and rounded once.  The
-    // operand rows of the first chunk are fetched while the MMAs still run.
-    float lrow[CW], rrow[CW];
+    const int et = threadIdx.x - 64;  // 0..127
+    uint32_t u = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+      int slot, z, bx, by;
+      Epi<float> e;
+      if (!unit(w, slot, z, bx, by, e)) continue;
+      const int m0 = by * BM, n0 = bx * BN;
+      const int r = m0 + rl;
+      const bool rowok = r < n;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the previous unit's readers of cs_sh / dr_sh are done
+      if (et < BN) {
+        const int c = n0 + et;
+        const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
+        cs_sh[et] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
+        dr_sh[et] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
+      // the int8 GEMM carries Yl Yr (each row / column scaled without its
+      // diagonal, which in the squaring phase dominates), the rest is exact
+      // elementwise work here, all summed in binary64 and rounded once.  The
+      // operand rows of the first chunk are fetched while the MMAs still run.
+      float lrow[CW], rrow[CW];
 #define I8_LOAD_ROWS(C0)                                                                       \
   do {                                                                                         \
     const int c0_ = (C0);                                                                      \
@@ -422,124 +507,136 @@ __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 
       }                                                                                        \
     }                                                                                          \
   } while (0)
-    I8_LOAD_ROWS(n0);
-    const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
-    const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
-    const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
-    tc::mbar_wait(&tmem_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
+      I8_LOAD_ROWS(n0);
+      const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+      const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
+      const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
+      tc::mbar_wait(&tfull_bar, u & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-    for (int cb = 0; cb < BN / CW; ++cb) {
-      int a0[CW], a1[CW], a2[CW], a3[CW];
-      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
-      tmem_ld16i(ta, a0);
-      tmem_ld16i(ta + BN, a1);
-      tmem_ld16i(ta + 2 * BN, a2);
-      tmem_ld16i(ta + 3 * BN, a3);
-      const int c0 = n0 + cb * CW;
-      const bool full = rowok && c0 + CW <= n;
-      if (cb > 0) I8_LOAD_ROWS(c0);
-      float o0[CW];
-#pragma unroll
-      for (int j = 0; j < CW; ++j) {
-        const int c = c0 + j;
-        // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49) and a
-        // single int -> binary64 conversion (the conversion unit was the hot pipe)
-        const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
-                            (long long)a3[j];
-        double y = (double)T * rs21 * cs_sh[cb * CW + j];
-        const double dr = (double)dr_sh[cb * CW + j];
-        y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
-        o0[j] = e.alpha * (float)y;
-      }
-      for (int qq = 0; qq < e.nin; ++qq) {
-        const float cq = e.c[0][qq];
-        if (cq == 0.f || !rowok) continue;
-        const float* ip = e.in[qq] + (size_t)r * n + c0;
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < CW; j += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
-            o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
-            o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < CW; ++j)
-            if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
+      for (int cb = 0; cb < BN / CW; ++cb) {
+        int a0[CW], a1[CW], a2[CW], a3[CW];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
+        tmem_ld16i(ta, a0);
+        tmem_ld16i(ta + BN, a1);
+        tmem_ld16i(ta + 2 * BN, a2);
+        tmem_ld16i(ta + 3 * BN, a3);
+        if (cb == BN / CW - 1) {
+          // every accumulator word of this unit is in registers: hand TMEM back
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&tempty_bar)) : "memory");
         }
-      }
-      if (e.d[0] != 0.f && r >= c0 && r < c0 + CW) {
+        const int c0 = n0 + cb * CW;
+        const bool full = rowok && c0 + CW <= n;
+        if (cb > 0) I8_LOAD_ROWS(c0);
+        float o0[CW];
 #pragma unroll
-        for (int j = 0; j < CW; ++j)
-          if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
-      }
-      if (rowok) {
-        float* op = e.out[0] + (size_t)r * n + c0;
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < CW; j += 4)
-            *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < CW; ++j)
-            if (c0 + j < n) op[j] = o0[j];
+        for (int j = 0; j < CW; ++j) {
+          const int c = c0 + j;
+          // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49) and a
+          // single int -> binary64 conversion (the conversion unit was the hot pipe)
+          const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
+                              (long long)a3[j];
+          double y = (double)T * rs21 * cs_sh[cb * CW + j];
+          const double dr = (double)dr_sh[cb * CW + j];
+          y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
+          o0[j] = e.alpha * (float)y;
         }
-      }
-      for (int k = 1; k < e.nout; ++k) {
-        float ok[CW];
-#pragma unroll
-        for (int j = 0; j < CW; ++j) ok[j] = o0[j];
         for (int qq = 0; qq < e.nin; ++qq) {
-          const float cq = e.c[k][qq];
+          const float cq = e.c[0][qq];
           if (cq == 0.f || !rowok) continue;
           const float* ip = e.in[qq] + (size_t)r * n + c0;
           if (full) {
 #pragma unroll
             for (int j = 0; j < CW; j += 4) {
               const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
-              ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
-              ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
+              o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
+              o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
             }
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j)
-              if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+              if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
           }
         }
-        if (e.d[k] != 0.f && r >= c0 && r < c0 + CW) {
+        if (e.d[0] != 0.f && r >= c0 && r < c0 + CW) {
 #pragma unroll
           for (int j = 0; j < CW; ++j)
-            if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
+            if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
         }
         if (rowok) {
-          float* op = e.out[k] + (size_t)r * n + c0;
+          float* op = e.out[0] + (size_t)r * n + c0;
           if (full) {
 #pragma unroll
             for (int j = 0; j < CW; j += 4)
-              *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
+              *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j)
-              if (c0 + j < n) op[j] = ok[j];
+              if (c0 + j < n) op[j] = o0[j];
           }
         }
-      }
-      if (e.colnorm) {
-        // deterministic column abs-sums of this 128-row tile (select.py:193)
+        for (int k = 1; k < e.nout; ++k) {
+          float ok[CW];
 #pragma unroll
-        for (int j = 0; j < CW; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (rl < CW && c0 + rl < n) {
-          double a = 0.0;
-          for (int rr = 0; rr < BM; ++rr) a += red[rl * BM + rr];
-          g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + c0 + rl] = a;
+          for (int j = 0; j < CW; ++j) ok[j] = o0[j];
+          for (int qq = 0; qq < e.nin; ++qq) {
+            const float cq = e.c[k][qq];
+            if (cq == 0.f || !rowok) continue;
+            const float* ip = e.in[qq] + (size_t)r * n + c0;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < CW; j += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
+                ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
+                ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < CW; ++j)
+                if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+            }
+          }
+          if (e.d[k] != 0.f && r >= c0 && r < c0 + CW) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j)
+              if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
+          }
+          if (rowok) {
+            float* op = e.out[k] + (size_t)r * n + c0;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < CW; j += 4)
+                *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < CW; ++j)
+                if (c0 + j < n) op[j] = ok[j];
+            }
+          }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (e.colnorm) {
+          // deterministic column abs-sums of this 128-row tile (select.py:193):
+          // a fixed shuffle tree over each warp's 32 rows, then the 4 warps in order
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            double v = rowok ? fabs((double)o0[j]) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red_sh[q][j] = v;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et < CW && c0 + et < n) {
+            const double a = ((red_sh[0][et] + red_sh[1][et]) + red_sh[2][et]) + red_sh[3][et];
+            g.part[((size_t)z * g.tiles_m + by) * n + c0 + et] = a;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
       }
-    }
 #undef I8_LOAD_ROWS
+      ++u;
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

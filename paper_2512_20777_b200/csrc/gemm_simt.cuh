@@ -18,6 +18,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "fused_small.cuh"
 #include "select.cuh"
 
@@ -201,9 +203,9 @@ __device__ __forceinline__ int simt_col(int tx, int j) {
 // tensor cores) instead of DFMAs: warp (wr, wc) of the 2 x 4 warp grid owns a
 // 64 x 32 sub-tile = 8 x 4 DMMA tiles, and thread "row slot" i / column pair
 // j0 of the epilogue map onto the accumulator fragments.
-template <typename T, bool TWO = (sizeof(T) == 4), bool MMA = false>
-__global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
-gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
+template <typename T, bool TWO, bool MMA>
+__device__ __forceinline__ void gemm_tile(const GemmCtx<T>& g, int stage, const int* __restrict__ list, int slot,
+                                          int bx, int by, unsigned char* smem_raw) {
   using C = SimtCfg<T>;
   constexpr int BK = C::BK, ST = C::STAGES, KV = C::KV, VW = C::VW;
   // padded rows: fp64 strides of 20 / 132 doubles (= 8 banks mod 32) make the
@@ -214,16 +216,15 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
   // fragments (4 k-rows x 8 columns per warp load) hit the 2-wavefront minimum
   constexpr int LDB = kGemmBN + 4;
   constexpr int A_ELEMS = kGemmBM * LDA, B_ELEMS = BK * LDB;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
   T* Bs = As + ST * A_ELEMS;
 
-  const int z = list ? list[blockIdx.z] : (int)blockIdx.z;
-  if (g.route && g.route[blockIdx.z]) return;
+  const int z = list ? list[slot] : slot;
+  if (g.route && g.route[slot]) return;
   Epi<T> e;
   if (!make_epi(g, stage, z, e)) return;
   const int n = g.n;
-  const int m0 = blockIdx.y * kGemmBM, n0 = blockIdx.x * kGemmBN;
+  const int m0 = by * kGemmBM, n0 = bx * kGemmBN;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int lane = tid % 32, warp = tid / 32, lg = lane >> 2, lt = lane & 3, wr = warp >> 2, wc = warp & 3;
   // epilogue coordinates of accumulator slot (i, j) within the CTA tile
@@ -465,7 +466,40 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list) {
     if (tid < kGemmBN && n0 + tid < n) {
       double a = 0.0;
       for (int r = 0; r < 16; ++r) a += red[r * kGemmBN + tid];
-      g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + n0 + tid] = a;
+      g.part[((size_t)z * g.tiles_m + by) * n + n0 + tid] = a;
+    }
+  }
+}
+
+// One launch = one stage over the first *dcount slots of `list` (or `hcount`
+// when dcount is null): a persistent grid walks the work units (slot, tile
+// row, tile column) with the tile column fastest, so co-resident CTAs share
+// operand panels in L2.  The slot count lives in device memory (written by
+// the device bucket scheduler, k_bucket), so the host never waits for it.
+template <typename T, bool TWO>
+constexpr bool kZStride = sizeof(T) == 4 && !TWO;
+
+template <typename T, bool TWO = (sizeof(T) == 4), bool MMA = false>
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
+gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list, const int* __restrict__ dcount, int hcount) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int cnt = dcount ? *dcount : hcount;
+  if constexpr (kZStride<T, TWO>) {
+    // 2 CTAs/SM at the 128-register cap: the tile stays (blockIdx.x, blockIdx.y)
+    // and only the slot is walked (blockIdx.z stride), so the loop costs no
+    // mainloop registers; n <= 512 keeps the tile count far below the resident
+    // CTAs, so the z-stride grid is balanced
+    for (int slot = blockIdx.z; slot < cnt; slot += gridDim.z) {
+      __syncthreads();  // the previous unit's epilogue may still read shared memory
+      gemm_tile<T, TWO, MMA>(g, stage, list, slot, blockIdx.x, blockIdx.y, smem_raw);
+    }
+  } else {
+    const int total = cnt * (((g.n + kGemmBN - 1) / kGemmBN) * g.tiles_m);
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const int tn = (g.n + kGemmBN - 1) / kGemmBN, tiles = tn * g.tiles_m;
+      const int slot = w / tiles, t = w - slot * tiles;
+      __syncthreads();  // the previous unit's epilogue may still read shared memory
+      gemm_tile<T, TWO, MMA>(g, stage, list, slot, t % tn, t / tn, smem_raw);
     }
   }
 }
@@ -476,31 +510,63 @@ constexpr int simt_smem_bytes() {
   return (int)(C::STAGES * (kGemmBM * (C::BK + (sizeof(T) == 4 ? C::KV : 4)) + C::BK * (kGemmBN + 4)) * sizeof(T));
 }
 
+static inline int sm_count_dev() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+// Persistent grid size for a kernel: resident CTAs per SM x SMs, capped by the work.
+template <typename K>
+static int persistent_grid(K kern, int threads, size_t smem, int64_t units, int* occ_cache) {
+  if (*occ_cache <= 0) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess || o < 1) o = 1;
+    *occ_cache = o;
+  }
+  const int64_t cap = (int64_t)sm_count_dev() * *occ_cache;
+  return (int)(units < cap ? (units < 1 ? 1 : units) : cap);
+}
+
+// One product stage over `list` (null = slots 0..), the first *dcount slots
+// (dcount null: `count`); `count` bounds the work on the host side.
 template <typename T>
-static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st) {
+static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st,
+                       const int* dcount = nullptr) {
   if (count <= 0) return 0;
   static bool attr = false;
   constexpr int smem = simt_smem_bytes<T>();
+  auto k_two = gemm_stage_kernel<T, true>;
+  auto k_one = gemm_stage_kernel<T, false>;
+  auto k_mma = gemm_stage_kernel<T, false, sizeof(T) == 8>;
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm_stage_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(gemm_stage_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess ||
-        (sizeof(T) == 8 &&
-         cudaFuncSetAttribute(gemm_stage_kernel<T, false, sizeof(T) == 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem) != cudaSuccess))
+    if (cudaFuncSetAttribute(k_two, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_one, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        (sizeof(T) == 8 && cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess))
       return 1;
     attr = true;
   }
+  static int occ[3] = {0, 0, 0};
   const int tn = (g.n + kGemmBN - 1) / kGemmBN, tm = (g.n + kGemmBM - 1) / kGemmBM;
-  dim3 grid(tn, tm, count);
+  const int64_t units = (int64_t)count * tn * tm;
   static const bool dmma = !(getenv("EXPMB_NO_DMMA") && getenv("EXPMB_NO_DMMA")[0] == '1');
   if (sizeof(T) == 4 && g.n > 512)
-    gemm_stage_kernel<T, true><<<grid, 256, smem, st>>>(g, stage, list);
+    k_two<<<persistent_grid(k_two, 256, smem, units, &occ[0]), 256, smem, st>>>(g, stage, list, dcount, count);
   else if (sizeof(T) == 8 && dmma)
-    gemm_stage_kernel<T, false, sizeof(T) == 8><<<grid, 256, smem, st>>>(g, stage, list);
-  else
-    gemm_stage_kernel<T, false><<<grid, 256, smem, st>>>(g, stage, list);
+    k_mma<<<persistent_grid(k_mma, 256, smem, units, &occ[2]), 256, smem, st>>>(g, stage, list, dcount, count);
+  else {
+    // z-stride grid (kZStride): tiles x enough slots to fill every resident CTA once
+    const int t2 = tn * tm;
+    const int zc = std::max(1, persistent_grid(k_one, 256, smem, units, &occ[1]) / t2);
+    k_one<<<dim3(tn, tm, std::min(count, zc)), 256, smem, st>>>(g, stage, list, dcount, count);
+  }
   return cudaGetLastError() != cudaSuccess;
 }
 
@@ -508,8 +574,11 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
 // elementwise stage (before the first evaluation product)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __restrict__ list) {
-  const int z = list[blockIdx.y];
+__global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __restrict__ list,
+                                                   const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  for (int slot = blockIdx.y; slot < cnt; slot += gridDim.y) {
+  const int z = list[slot];
   const int m = g.m[z], s = g.s[z];
   const int n = g.n;
   const size_t nn = (size_t)n * n;
@@ -544,16 +613,20 @@ __global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __re
       g.Ra[o + i] = (T)(cc[0] * sg2) * A2[i] + (T)(cc[1] * sg) * Wz[i];
     }
   }
+  }
 }
 
 template <typename T>
-static int elem_launch(const GemmCtx<T>& g, const int* list, int count, cudaStream_t st) {
+static int elem_launch(const GemmCtx<T>& g, const int* list, int count, cudaStream_t st,
+                       const int* dcount = nullptr) {
   if (count <= 0) return 0;
   const size_t nn = (size_t)g.n * g.n;
   int bx = (int)((nn + 255) / 256);
   if (bx > 64) bx = 64;
-  dim3 grid(bx, count);
-  elem_kernel<T><<<grid, 256, 0, st>>>(g, list);
+  // slots grid-strided: enough CTAs for ~8 per SM
+  int by = (int)std::min<int64_t>(count, std::max<int64_t>(1, (int64_t)sm_count_dev() * 8 / bx));
+  dim3 grid(bx, by);
+  elem_kernel<T><<<grid, 256, 0, st>>>(g, list, dcount, count);
   return cudaGetLastError() != cudaSuccess;
 }
 

@@ -8,13 +8,16 @@
 //             abs-sum partials (select.py:192-193).  PS: W^3, W^4 likewise.
 //   K_select  ||W^2||_1 (fixed-order reduction of the partials) and the
 //             ladder (select.py:164-220) -> m, s, e1, e2, mults.
-//   -- one device->host copy of (m, s): the host buckets the batch --
+//   K_bucket  the device (m, s) bucket scheduler: stage lists and their sizes
+//             in device memory (no host round trip; every later launch reads
+//             its slot count on the device)
 //   K_elem    T0/T1/T2 results, T4's inner factor, R1 = c1 A^2 + c2 A
 //   G stage1..3  the products of poly.py:189-230, each epilogue emitting the
 //             next linear combinations (y02/L2/R2, y12/L3/R3, X) so no
 //             separate elementwise pass runs between products
 //   G square  s squarings (engine.py:80-87), bucket = prefix of the batch
-//             sorted by s descending.
+//             sorted by s descending; one launch per level up to MAX_SCALING,
+//             levels beyond the batch's largest s find a zero count and exit.
 // The 2^-s, 2^-2s scalings (engine.py:139-140) are folded into epilogue
 // coefficients; they are powers of two so the folding is exact.
 #pragma once
@@ -26,7 +29,6 @@
 #include <stdlib.h>
 
 #include <algorithm>
-#include <vector>
 
 #include "fused_small.cuh"
 #include "gemm_simt.cuh"
@@ -41,17 +43,6 @@ namespace expmb {
 // ---------------------------------------------------------------------------
 constexpr int kLargeBufsSastre = 7;  // W2 Y0 Y1 La Ra Lb Rb   (Tmp aliases Lb)
 constexpr int kLargeBufsPS = 6;      // W2 W3 W4 Q0 Q1 Tmp
-constexpr int kLargeBufsTC = 16;     // tensor-core path: see tc::Ctx
-
-// The tcgen05 split-TF32 path (gemm_tc.cuh) is opt-in (EXPMB_TC=1): the
-// tensor cores' fp32 accumulation truncates (measured: -1.4e-5 mean relative
-// bias on 256-step accumulation chains, profiles/tc_probe_r01.txt), a
-// systematic error the squaring phase amplifies by ~2^s, so it misses the
-// 1e-5 fp32 parity bar (C3: 1.09e-5).  The default fp32 path is the FFMA GEMM.
-static inline bool use_tc_path(int n, int esize, int scheme) {
-  const char* e = getenv("EXPMB_TC");
-  return esize == 4 && scheme == 0 && (n % 4) == 0 && e != nullptr && e[0] == '1';
-}
 // Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh):
 // opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
 // Default: on for fp32 n >= 512 (measured crossover, tools/i8_crossover.py:
@@ -73,7 +64,8 @@ struct LargeLayout {
   size_t mat_bytes;
   int nbufs;
   int tiles_m;
-  size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_flags, off_m, off_s, off_e1, off_e2, off_list, total;
+  size_t off_bufs, off_part, off_norm1, off_norm2, off_need, off_flags, off_m, off_s, off_e1, off_e2, off_list, off_cnt,
+      total;
   size_t off_i8as, off_i8bs, off_i8er, off_i8ec, off_i8rc, off_i8cc, off_i8ok;  // int8-slice path
 };
 
@@ -82,8 +74,8 @@ static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static inline LargeLayout large_layout(int64_t batch, int n, int esize, int scheme) {
   LargeLayout L{};
   L.mat_bytes = align256((size_t)n * n * esize);
-  L.nbufs = use_tc_path(n, esize, scheme) ? kLargeBufsTC : (scheme == 1 ? kLargeBufsPS : kLargeBufsSastre);
-  const bool i8p = use_i8_path(n, esize) && !use_tc_path(n, esize, scheme);
+  L.nbufs = scheme == 1 ? kLargeBufsPS : kLargeBufsSastre;
+  const bool i8p = use_i8_path(n, esize);
   const size_t i8plane = (size_t)n * i8_np(n);
   const size_t per_bufs = L.mat_bytes * L.nbufs;
   // per-matrix bytes for sizing the chunk (the int8-slice regions sit after the lists)
@@ -106,6 +98,7 @@ static inline LargeLayout large_layout(int64_t batch, int n, int esize, int sche
   L.off_e1 = off; off += align256((size_t)chunk * sizeof(double));
   L.off_e2 = off; off += align256((size_t)chunk * sizeof(double));
   L.off_list = off; off += align256((size_t)chunk * 8 * sizeof(int));
+  L.off_cnt = off; off += 256;
   L.off_i8as = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
   L.off_i8bs = off; off += i8p ? align256((size_t)chunk * i8::NSL * i8plane) : 0;
   L.off_i8er = off; off += i8p ? align256((size_t)chunk * n * sizeof(int)) : 0;
@@ -215,6 +208,51 @@ __global__ void __launch_bounds__(256) k_finish(int cnt, int scheme, const doubl
   }
 }
 
+// Device (m, s) bucket scheduler (the keys are the reference's plan,
+// select.py:164-220; the reference batches by caller loops, bench.py:294-309).
+// One CTA per chunk.  Writes `lists` = five slot lists of `ic` entries:
+//   [0] every matrix (elementwise stage), [1..3] the matrices whose formula
+//   uses evaluation product 1..3, [4] every matrix sorted by s descending
+//   (counting sort), so squaring level q is the prefix of length #(s > q);
+// and `cnt` = [ic, |E1|, |E2|, |E3|, #(s > 0), ..., #(s > kMaxSq - 1)].
+// Order within a bucket is immaterial: every matrix's result depends only on
+// its own data, so the output is bit-identical whatever CTA handles it.
+constexpr int kMaxSq = 20;  // MAX_SCALING (select.py:56)
+constexpr int kCntSq = 4;   // cnt index of squaring level 0
+__global__ void __launch_bounds__(1024) k_bucket(const int8_t* __restrict__ pm, const int8_t* __restrict__ ps,
+                                                 int ic, int scheme, int* __restrict__ lists, int* __restrict__ cnt) {
+  __shared__ int hist[kMaxSq + 1], fill[kMaxSq + 1], base[kMaxSq + 1], ecnt[3];
+  if (threadIdx.x <= kMaxSq) hist[threadIdx.x] = fill[threadIdx.x] = 0;
+  if (threadIdx.x < 3) ecnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < ic; i += blockDim.x) {
+    const int s = min(max((int)ps[i], 0), kMaxSq);
+    atomicAdd(&hist[s], 1);
+    lists[i] = i;
+    const int m = pm[i];
+    int k = 0;  // evaluation products after the powers
+    if (scheme == 0) k = (m >= 4) + (m >= 8) + (m >= 15);
+    else if (m >= 1) k = min(ps_k_of(m) - 1, 3);
+    for (int e = 0; e < k; ++e) lists[(size_t)(1 + e) * ic + atomicAdd(&ecnt[e], 1)] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int q = kMaxSq; q >= 0; --q) {  // base[s] = #(s' > s)
+      base[q] = acc;
+      acc += hist[q];
+    }
+    cnt[0] = ic;
+    for (int e = 0; e < 3; ++e) cnt[1 + e] = ecnt[e];
+    for (int q = 0; q < kMaxSq; ++q) cnt[kCntSq + q] = base[q];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ic; i += blockDim.x) {
+    const int s = min(max((int)ps[i], 0), kMaxSq);
+    lists[(size_t)4 * ic + base[s] + atomicAdd(&fill[s], 1)] = i;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
@@ -277,9 +315,10 @@ static bool encode_map_i8(CUtensorMap* m, const int8_t* base, int n, int np, int
   return r == CUDA_SUCCESS;
 }
 
-// One product stage on the int8-slice path: exponents, slices, GEMM.
+// One product stage on the int8-slice path: exponents, slices, GEMM, over
+// the first *dcount slots of `list` (dcount null: `count`).
 static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, const int* list, int count,
-                     const i8::Bufs& b, cudaStream_t st) {
+                     const i8::Bufs& b, cudaStream_t st, const int* dcount = nullptr) {
   if (count <= 0) return 0;
   static bool attr = false;
   if (!attr) {
@@ -289,10 +328,6 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     attr = true;
   }
   const int n = g.n;
-  const size_t vb = (size_t)count * n * sizeof(int);
-  if (cudaMemsetAsync(b.er, 0, vb, st) != cudaSuccess || cudaMemsetAsync(b.ec, 0, vb, st) != cudaSuccess ||
-      cudaMemsetAsync(b.rc, 0, 2 * vb, st) != cudaSuccess || cudaMemsetAsync(b.cc, 0, 2 * vb, st) != cudaSuccess)
-    return 1;
   static const bool dbg = getenv("EXPMB_DEBUG_SYNC") != nullptr;
   auto chk = [&](const char* what) {
     if (!dbg) return 0;
@@ -300,15 +335,22 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     if (e != cudaSuccess) fprintf(stderr, "expmb i8 stage %d: %s failed: %s\n", stage, what, cudaGetErrorString(e));
     return e != cudaSuccess ? 1 : 0;
   };
-  const dim3 tiles((n + 31) / 32, (n + 31) / 32, count);
-  i8::k_i8_stats<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  static int occ_stats = 0, occ_slice = 0, occ_zero = 0, occ_stage = 0;
+  const int t32 = (n + 31) / 32;
+  const int64_t u32 = (int64_t)count * t32 * t32;
+  i8::k_i8_zero<<<persistent_grid(i8::k_i8_zero, 256, 0, ((int64_t)count * n + 255) / 256, &occ_zero), 256, 0, st>>>(
+      b, n, dcount, count);
+  i8::k_i8_stats<<<persistent_grid(i8::k_i8_stats, 256, 0, u32, &occ_stats), 256, 0, st>>>(g, stage, list, b,
+                                                                                            dcount, count);
   if (chk("stats")) return 1;
-  i8::k_i8_route<<<count, 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_route<<<std::min(count, sm_count_dev() * 8), 256, 0, st>>>(g, stage, list, b, dcount, count);
   if (chk("route")) return 1;
-  i8::k_i8_slice<<<tiles, 256, 0, st>>>(g, stage, list, b);
+  i8::k_i8_slice<<<persistent_grid(i8::k_i8_slice, 256, 0, u32, &occ_slice), 256, 0, st>>>(g, stage, list, b,
+                                                                                            dcount, count);
   if (chk("slice")) return 1;
-  i8::k_i8_stage<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS, i8::SMEM_BYTES,
-                   st>>>(maps, g, stage, list, b);
+  const int64_t units = (int64_t)count * ((n + i8::BN - 1) / i8::BN) * ((n + i8::BM - 1) / i8::BM);
+  i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS, i8::SMEM_BYTES, units, &occ_stage), i8::NTHREADS,
+                   i8::SMEM_BYTES, st>>>(maps, g, stage, list, b, dcount, count);
   {
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
@@ -317,10 +359,10 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     }
     if (chk("stage")) return 1;
   }
-  // the products routed away run on the FFMA GEMM (its CTAs for routed-here matrices exit at once)
+  // the products routed away run on the FFMA GEMM (its units for routed-here matrices exit at once)
   GemmCtx<float> gs = g;
   gs.route = b.ok;
-  return gemm_launch<float>(gs, stage, list, count, st);
+  return gemm_launch<float>(gs, stage, list, count, st, dcount);
 }
 
 template <typename T>
@@ -384,186 +426,31 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
       }
     }
   }
-  auto stage_launch = [&](int stage, const int* list, int count) -> int {
+  auto stage_launch = [&](int stage, const int* list, int count, const int* dcount) -> int {
     if constexpr (sizeof(T) == 4) {
-      if (i8p) return i8_launch(i8maps, g, stage, list, count, i8b, st);
+      if (i8p) return i8_launch(i8maps, g, stage, list, count, i8b, st, dcount);
     }
-    return gemm_launch<T>(g, stage, list, count, st);
+    return gemm_launch<T>(g, stage, list, count, st, dcount);
   };
 
   // powers + ladder, gated on device flags (no host round trip)
   const int maxp = scheme == 1 ? 4 : 2;
   for (int p = 2; p <= maxp; ++p) {
-    if (stage_launch(p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic)) return EXPMB_ERR_CUDA;
+    if (stage_launch(p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4), nullptr, ic, nullptr)) return EXPMB_ERR_CUDA;
     k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
   }
 
-  // one small device->host copy of the plans
-  std::vector<int8_t> hm(cnt), hs(cnt);
-  if (cudaMemcpyAsync(hm.data(), dm, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  if (cudaMemcpyAsync(hs.data(), ds, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return EXPMB_ERR_CUDA;
-
-  // bucket scheduler: stage lists; every list is sorted by s descending so
-  // the squaring buckets are prefixes of one list.
-  std::vector<int> order(cnt);
-  for (int i = 0; i < ic; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return hs[a] > hs[b]; });
-  std::vector<int> lists;
-  lists.reserve(cnt * 4);
-  std::vector<int> l_elem(order), l_s1, l_s2, l_s3, l_sq(order);
-  int maxs = 0;
-  for (int i : order) {
-    const int m = hm[i], s = hs[i];
-    if (s > maxs) maxs = s;
-    if (scheme == 0) {
-      if (m >= 4) l_s1.push_back(i);
-      if (m >= 8) l_s2.push_back(i);
-      if (m >= 15) l_s3.push_back(i);
-    } else if (m >= 1) {
-      const int k = ps_k_of(m);
-      if (k >= 2) l_s1.push_back(i);
-      if (k >= 3) l_s2.push_back(i);
-      if (k >= 4) l_s3.push_back(i);
-    }
-  }
-  // upload: [elem | s1 | s2 | s3 | sq]
-  std::vector<int> hl;
-  hl.insert(hl.end(), l_elem.begin(), l_elem.end());
-  const size_t o1 = hl.size(); hl.insert(hl.end(), l_s1.begin(), l_s1.end());
-  const size_t o2 = hl.size(); hl.insert(hl.end(), l_s2.begin(), l_s2.end());
-  const size_t o3 = hl.size(); hl.insert(hl.end(), l_s3.begin(), l_s3.end());
-  const size_t o4 = hl.size(); hl.insert(hl.end(), l_sq.begin(), l_sq.end());
-  if (cudaMemcpyAsync(dlist, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return EXPMB_ERR_CUDA;
-
-  if (elem_launch<T>(g, dlist, ic, st)) return EXPMB_ERR_CUDA;
-  if (!l_s1.empty() && stage_launch(STAGE_E1, dlist + o1, (int)l_s1.size())) return EXPMB_ERR_CUDA;
-  if (!l_s2.empty() && stage_launch(STAGE_E2, dlist + o2, (int)l_s2.size())) return EXPMB_ERR_CUDA;
-  if (!l_s3.empty() && stage_launch(STAGE_E3, dlist + o3, (int)l_s3.size())) return EXPMB_ERR_CUDA;
-  for (int q = 0; q < maxs; ++q) {
-    int c = 0;
-    while (c < ic && hs[l_sq[c]] > q) ++c;
+  // device bucket scheduler: stage lists + their sizes stay on the device
+  int* dcnt = reinterpret_cast<int*>(ws + L.off_cnt);
+  k_bucket<<<1, 1024, 0, st>>>(dm, ds, ic, scheme, dlist, dcnt);
+  if (elem_launch<T>(g, dlist, ic, st, dcnt)) return EXPMB_ERR_CUDA;
+  for (int e = 0; e < 3; ++e)
+    if (stage_launch(STAGE_E1 + e, dlist + (size_t)(1 + e) * ic, ic, dcnt + 1 + e)) return EXPMB_ERR_CUDA;
+  for (int q = 0; q < kMaxSq; ++q) {
     g.sq_step = q;
-    if (stage_launch(STAGE_SQ, dlist + o4, c)) return EXPMB_ERR_CUDA;
+    if (stage_launch(STAGE_SQ, dlist + (size_t)4 * ic, ic, dcnt + kCntSq + q)) return EXPMB_ERR_CUDA;
   }
   launch_finish<T>(X, n, ic, scheme, L, ws, nrm4, dm, ds, de1, de2, base, po, st);
-  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
-}
-
-// ---------------------------------------------------------------------------
-// tensor-core path (fp32, Sastre)
-// ---------------------------------------------------------------------------
-// [cnt][n][n] fp32 with `mstride_bytes` between matrices; box 32 (k) x 128 rows x 1, 128B swizzle
-static bool encode_map(CUtensorMap* m, const float* base, int n, int64_t cnt, size_t mstride_bytes) {
-  TensorMapEncodeFn enc = tensor_map_encoder();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)cnt};
-  cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)mstride_bytes};
-  cuuint32_t box[3] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-static int tc_launch(const tc::Maps& maps, const tc::Ctx& g, int stage, const int* list, int count, cudaStream_t st) {
-  if (count <= 0) return 0;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc::tc_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES) !=
-        cudaSuccess)
-      return 1;
-    attr = true;
-  }
-  const int t = (g.n + tc::BM - 1) / tc::BM;
-  dim3 grid(t, t, count);
-  tc::tc_stage_kernel<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(maps, g, stage, list);
-  return cudaGetLastError() != cudaSuccess;
-}
-
-static int large_run_chunk_tc(const float* W, float* X, int64_t cnt, int n, double eps, int64_t base, PlanOut po,
-                              unsigned char* ws, const LargeLayout& L, cudaStream_t st) {
-  const int ic = (int)cnt;
-  auto buf = [&](int b) { return reinterpret_cast<float*>(ws + L.off_bufs + (size_t)b * L.mat_bytes * L.chunk); };
-  double* part = reinterpret_cast<double*>(ws + L.off_part);
-  double* nrm4 = reinterpret_cast<double*>(ws + L.off_norm1);
-  int* need = reinterpret_cast<int*>(ws + L.off_need);
-  int8_t* dm = reinterpret_cast<int8_t*>(ws + L.off_m);
-  int8_t* ds = reinterpret_cast<int8_t*>(ws + L.off_s);
-  double* de1 = reinterpret_cast<double*>(ws + L.off_e1);
-  double* de2 = reinterpret_cast<double*>(ws + L.off_e2);
-  int* dlist = reinterpret_cast<int*>(ws + L.off_list);
-
-  tc::Ctx g{};
-  g.n = n;
-  g.tiles_m = L.tiles_m;
-  g.ms = (int64_t)(L.mat_bytes / 4);
-  g.ws = (int64_t)n * n;
-  g.W = W;
-  g.X = X;
-  float** slots[16] = {&g.Wlo, &g.Wt, &g.Wtlo, &g.W2, &g.W2lo, &g.W2t, &g.Y0, &g.Y1,
-                       &g.La, &g.Lalo, &g.Ra, &g.Ralo, &g.Lb, &g.Lblo, &g.Rb, &g.Rblo};
-  for (int b = 0; b < 16; ++b) *slots[b] = buf(b);
-  g.m = dm;
-  g.s = ds;
-  g.need = need;
-  g.part = part;
-
-  tc::Maps maps;
-  const size_t wsb = (size_t)n * n * 4, msb = L.mat_bytes;
-  const float* mp[tc::M_COUNT] = {W, g.Wlo, g.Wt, g.Wtlo, g.W2, g.W2lo, g.La, g.Lalo, g.Ra, g.Ralo, g.Lb, g.Lblo, g.Rb, g.Rblo};
-  for (int i = 0; i < tc::M_COUNT; ++i)
-    if (!encode_map(&maps.m[i], mp[i], n, cnt, i == tc::M_W ? wsb : msb)) return EXPMB_ERR_CUDA;
-
-  const double log_eps = log2(eps);
-  launch_norm1<float>(W, n, ic, L, part, log_eps, 0, nrm4, need, dm, ds, de1, de2, st);
-  {
-    dim3 grid((n + 31) / 32, (n + 31) / 32, ic);
-    tc::tc_prep_kernel<<<grid, 256, 0, st>>>(g, ic);
-  }
-  if (tc_launch(maps, g, STAGE_W2, nullptr, ic, st)) return EXPMB_ERR_CUDA;
-  k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, 2, log_eps, 0, nrm4, need, dm, ds, de1, de2);
-
-  std::vector<int8_t> hm(cnt), hs(cnt);
-  if (cudaMemcpyAsync(hm.data(), dm, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  if (cudaMemcpyAsync(hs.data(), ds, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return EXPMB_ERR_CUDA;
-
-  std::vector<int> order(cnt);
-  for (int i = 0; i < ic; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return hs[a] > hs[b]; });
-  std::vector<int> l_s1, l_s2, l_s3;
-  int maxs = 0;
-  for (int i : order) {
-    const int m = hm[i];
-    if (hs[i] > maxs) maxs = hs[i];
-    if (m >= 4) l_s1.push_back(i);
-    if (m >= 8) l_s2.push_back(i);
-    if (m >= 15) l_s3.push_back(i);
-  }
-  std::vector<int> hl(order);
-  const size_t o1 = hl.size(); hl.insert(hl.end(), l_s1.begin(), l_s1.end());
-  const size_t o2 = hl.size(); hl.insert(hl.end(), l_s2.begin(), l_s2.end());
-  const size_t o3 = hl.size(); hl.insert(hl.end(), l_s3.begin(), l_s3.end());
-  if (cudaMemcpyAsync(dlist, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return EXPMB_ERR_CUDA;
-  {
-    const size_t nn = (size_t)n * n;
-    int bx = (int)((nn + 255) / 256);
-    if (bx > 64) bx = 64;
-    tc::tc_elem_kernel<<<dim3(bx, ic), 256, 0, st>>>(g, dlist);
-  }
-  if (tc_launch(maps, g, STAGE_E1, dlist + o1, (int)l_s1.size(), st)) return EXPMB_ERR_CUDA;
-  if (tc_launch(maps, g, STAGE_E2, dlist + o2, (int)l_s2.size(), st)) return EXPMB_ERR_CUDA;
-  if (tc_launch(maps, g, STAGE_E3, dlist + o3, (int)l_s3.size(), st)) return EXPMB_ERR_CUDA;
-  for (int q = 0; q < maxs; ++q) {
-    int c = 0;
-    while (c < ic && hs[order[c]] > q) ++c;
-    g.sq_step = q;
-    if (tc_launch(maps, g, STAGE_SQ, dlist, c, st)) return EXPMB_ERR_CUDA;
-  }
-  launch_finish<float>(X, n, ic, 0, L, ws, nrm4, dm, ds, de1, de2, base, po, st);
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
@@ -576,10 +463,7 @@ static inline int large_expm(const void* W, void* X, int64_t batch, int n, int d
     const int64_t cnt = std::min<int64_t>(L.chunk, batch - b0);
     const size_t off = (size_t)b0 * n * n;
     int rc;
-    if (dtype == 0 && use_tc_path(n, 4, scheme))
-      rc = large_run_chunk_tc(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n, eps,
-                              b0, po, ws, L, st);
-    else if (dtype == 0)
+    if (dtype == 0)
       rc = large_run_chunk<float>(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n,
                                   eps, scheme, b0, po, ws, L, st);
     else

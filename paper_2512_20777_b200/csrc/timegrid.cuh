@@ -32,7 +32,6 @@
 #include <stdint.h>
 
 #include <algorithm>
-#include <vector>
 
 #include "gemm_simt.cuh"
 #include "large.cuh"
@@ -45,7 +44,8 @@ constexpr int kTgPowers = 16;
 struct TgLayout {
   int64_t chunk;
   size_t mat_bytes;  // one T matrix, 256-aligned
-  size_t off_pow, off_tmp, off_part, off_nrmA, off_nrm4, off_flags, off_m, off_s, off_e1, off_e2, off_list, total;
+  size_t off_pow, off_tmp, off_part, off_nrmA, off_nrm4, off_flags, off_m, off_s, off_e1, off_e2, off_list, off_cnt,
+      total;
 };
 
 static inline TgLayout tg_layout(int64_t K, int n, int esize) {
@@ -67,7 +67,8 @@ static inline TgLayout tg_layout(int64_t K, int n, int esize) {
   L.off_s = off; off += align256((size_t)chunk);
   L.off_e1 = off; off += align256((size_t)chunk * sizeof(double));
   L.off_e2 = off; off += align256((size_t)chunk * sizeof(double));
-  L.off_list = off; off += align256((size_t)chunk * sizeof(int));
+  L.off_list = off; off += align256((size_t)chunk * 5 * sizeof(int));  // k_bucket's five lists
+  L.off_cnt = off; off += 256;
   L.total = off;
   return L;
 }
@@ -255,18 +256,11 @@ static int tg_run(const T* A, const T* t, T* X, int64_t K, int n, double eps, in
     k_tg_select<T><<<(ic + 127) / 128, 128, 0, st>>>(t + base, cnt, nrmA, eps, scheme, nrm4, dm, ds, de1, de2);
     k_tg_combine<T><<<dim3((unsigned)((nn + 255) / 256), (unsigned)((cnt + kTgChunkK - 1) / kTgChunkK)), 256, 0, st>>>(
         P, n, t + base, cnt, dm, ds, scheme, Xc, Tmp, mstride);
-    // squarings: buckets are prefixes of the chunk sorted by s descending
-    std::vector<int8_t> hs(cnt);
-    if (cudaMemcpyAsync(hs.data(), ds, cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EXPMB_ERR_CUDA;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return EXPMB_ERR_CUDA;
-    std::vector<int> order(cnt);
-    for (int i = 0; i < ic; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return hs[a] > hs[b]; });
-    int maxs = 0;
-    for (int i = 0; i < ic; ++i) maxs = std::max<int>(maxs, hs[i]);
-    if (maxs > 0) {
-      if (cudaMemcpyAsync(dlist, order.data(), (size_t)ic * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return EXPMB_ERR_CUDA;
+    // squarings: the device bucket scheduler sorts the chunk by s descending;
+    // level q runs on the prefix #(s > q), a count that stays on the device
+    int* dcnt = reinterpret_cast<int*>(ws + L.off_cnt);
+    k_bucket<<<1, 1024, 0, st>>>(dm, ds, ic, scheme, dlist, dcnt);
+    {
       GemmCtx<T> g{};
       g.n = n;
       g.scheme = scheme;
@@ -279,11 +273,9 @@ static int tg_run(const T* A, const T* t, T* X, int64_t K, int n, double eps, in
       g.m = dm;
       g.s = ds;
       g.part = reinterpret_cast<double*>(ws + L.off_part);
-      for (int q = 0; q < maxs; ++q) {
-        int c = 0;
-        while (c < ic && hs[order[c]] > q) ++c;
+      for (int q = 0; q < kMaxSq; ++q) {
         g.sq_step = q;
-        if (gemm_launch<T>(g, STAGE_SQ, dlist, c, st)) return EXPMB_ERR_CUDA;
+        if (gemm_launch<T>(g, STAGE_SQ, dlist + (size_t)4 * ic, ic, st, dcnt + kCntSq + q)) return EXPMB_ERR_CUDA;
       }
     }
     // non-finite scan + per-time outputs (mults = the reference's ledger)

@@ -486,3 +486,62 @@ def test_expm_host_pageable_ragged(n, B, dtype):
     dev = X.expm(W.cuda(), 2.0 ** -24 if dtype == torch.float32 else 1e-12)
     assert torch.equal(host.value, dev.value.cpu())
     assert torch.equal(host.plan.s, dev.plan.s.cpu()) and torch.equal(host.mults, dev.mults.cpu())
+
+
+@pytest.mark.parametrize("n,B,dtype", [(256, 24, torch.float32), (200, 9, torch.float64), (2048, 6, torch.float32)])
+def test_cuda_graph_capture_large_n(n, B, dtype):
+    """The large-n pipeline (n > 64) is sync-free: the device bucket scheduler
+    (k_bucket) keeps every stage's slot count on the device, so the whole call
+    captures into a CUDA graph (a host synchronisation inside capture fails).
+    Replayed on inputs with a different (m, s) mix, the graph gives exactly the
+    eager result: n = 256 fp32 (FFMA GEMM), n = 200 fp64 (DMMA GEMM), n = 2048
+    fp32 (exact int8-slice tcgen05 GEMM)."""
+    eps = 2.0 ** -24 if dtype == torch.float32 else 2.0 ** -53
+
+    def batch(seed, lo, hi):
+        g = torch.Generator().manual_seed(seed)
+        W = torch.randn(B, n, n, generator=g, dtype=torch.float64)
+        tgt = 10.0 ** (torch.rand(B, generator=g, dtype=torch.float64) * (hi - lo) + lo)
+        return (W * (tgt / W.abs().sum(dim=-2).amax(dim=-1))[:, None, None]).to(dtype).cuda()
+
+    W = batch(1, -1.0, 0.5)          # mostly s = 0
+    Xg = torch.empty_like(W)
+    plan = {"m": torch.empty(B, dtype=torch.int8, device="cuda"), "s": torch.empty(B, dtype=torch.int8, device="cuda"),
+            "mults": torch.empty(B, dtype=torch.int32, device="cuda"),
+            "nonfinite": torch.empty(B, dtype=torch.uint8, device="cuda")}
+    X.expm_into(W, Xg, eps, "sastre", plan)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.expm_into(W, Xg, eps, "sastre", plan)
+    W.copy_(batch(2, 0.0, 2.7))      # s up to ~8: more squaring levels than at capture time
+    g.replay()
+    torch.cuda.synchronize()
+    ref = X.expm(W.clone(), eps)
+    assert int(ref.plan.s.max()) >= 3
+    assert torch.equal(Xg, ref.value)
+    assert torch.equal(plan["s"], ref.plan.s) and torch.equal(plan["mults"], ref.mults)
+
+
+def test_cuda_graph_capture_timegrid():
+    """expm_timegrid for n > 64 is sync-free too (shared powers, device bucketing of the squarings)."""
+    A, t = WL.c3_factors()
+    Ad = torch.as_tensor(A, device="cuda")
+    td = torch.as_tensor(t[:64], device="cuda")
+    K, n = 64, 256
+    out = torch.empty(K, n, n, device="cuda")
+    plan = {k: torch.empty(K, dtype=dt, device="cuda") for k, dt in (("m", torch.int8), ("s", torch.int8),
+                                                                     ("mults", torch.int32),
+                                                                     ("nonfinite", torch.uint8))}
+    wsb = int(X._lib.lib().expmb_timegrid_workspace_bytes(K, n, 0))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    X.expm_timegrid(Ad, td, 2.0 ** -24, check_finite=False, out=out, plan=plan, workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.expm_timegrid(Ad, td, 2.0 ** -24, check_finite=False, out=out, plan=plan, workspace=ws)
+    td.copy_(torch.as_tensor(t[64:128]))
+    g.replay()
+    torch.cuda.synchronize()
+    ref = X.expm_timegrid(Ad, td.clone(), 2.0 ** -24)
+    assert torch.equal(out, ref.value) and torch.equal(plan["s"], ref.plan.s)

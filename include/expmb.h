@@ -41,7 +41,7 @@ extern "C" {
 #define EXPMB_SASTRE 0
 #define EXPMB_PS 1
 /* Alg. 1 term accumulation, the paper's comparator: engine.py:90-116
- * (expm_baseline); n <= 64 only.  m = terms added, s may exceed int8 (the
+ * (expm_baseline); any n.  m = terms added, s may exceed int8 (the
  * m/s outputs saturate at 127; mults = m + s is exact). */
 #define EXPMB_BASELINE 2
 
@@ -92,6 +92,18 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype,
                int8_t* m, int8_t* s, double* e1, double* e2, double* norms,
                int32_t* mults, uint8_t* nonfinite,
                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Plan only: select_sastre / select_ps (select.py:223-234), batched.  Forms
+ * exactly the powers the ladder needs (W^2; W^3, W^4 on the PS ladder) and
+ * writes the plan -- no exponential, no X.  Arguments as expmb_expm (scheme
+ * EXPMB_SASTRE or EXPMB_PS; workspace expmb_workspace_bytes(batch, n, dtype,
+ * scheme)).  nonfinite[] flags an input or formed power that is not finite
+ * (the reference raises NonFiniteError there, matrix.py:56-57, 95-102).
+ */
+int expmb_select(const void* W, int64_t batch, int32_t n, int dtype, double eps, int scheme,
+                 int8_t* m, int8_t* s, double* e1, double* e2, double* norms,
+                 int32_t* mults, uint8_t* nonfinite, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Host-side evaluation of the SAME selector the kernels run (one

@@ -32,6 +32,7 @@ EXPORTS = (
     "expmb_unit_roundoff",
     "expmb_workspace_bytes",
     "expmb_expm",
+    "expmb_select",
     "expmb_select_host",
     "expmb_expm_lowrank",
     "expmb_select_lowrank_host",
@@ -67,6 +68,16 @@ def lib() -> ctypes.CDLL:
     L.expmb_expm.restype = c.c_int
     L.expmb_expm.argtypes = [
         c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+        c.c_void_p, c.c_size_t, c.c_void_p,
+    ]
+    if not hasattr(L, "expmb_select"):  # an older A/B build (EXPMB_LIB)
+        L.expmb_select = None
+    else:
+        L.expmb_select.restype = c.c_int
+    if L.expmb_select is not None:
+        L.expmb_select.argtypes = [
+        c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
         c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
         c.c_void_p, c.c_size_t, c.c_void_p,
     ]

@@ -193,7 +193,10 @@ def expm_baseline(W: torch.Tensor, eps: float, check_finite: bool = True) -> Exp
     """Alg. 1, the paper's comparator (engine.py:90-116): scale until the
     1-norm is below 1/2, add Taylor terms B^k/k! until the next term's 1-norm
     is at most eps, square back.  plan.m = terms added, plan.e1 = the norm of
-    the first term not added, mults = m + s (test_engine.py:83-97).  n <= 64."""
+    the first term not added, mults = m + s (test_engine.py:83-97).  Any n:
+    fused per-matrix kernels for n <= 64, the GEMM pipeline above (term stages
+    over device-resident active lists, every squaring level in one
+    cooperative launch; no host synchronisation)."""
     t0 = time.perf_counter()
     Wc, code = _validate(W, eps, SCHEME_BASELINE, allow_baseline=True)
     lead, n = W.shape[:-2], W.shape[-1]
@@ -328,14 +331,62 @@ def expm_host(W: torch.Tensor, eps: float, scheme: str = SCHEME_SASTRE, chunks: 
     return pipe.run(W, eps, scheme, check_finite)
 
 
-def select_sastre(W: torch.Tensor, eps: float) -> EvalPlan:
-    """select.py:228-234, batched (runs the full op; the plan is its by-product)."""
-    return expm(W, eps, SCHEME_SASTRE, check_finite=False).plan
+@torch.library.custom_op("expmkit_b200::select", mutates_args=())
+def _select_op(W: torch.Tensor, eps: float, scheme: int) -> tuple[
+        torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    B, n = W.shape[0], W.shape[-1]
+    dev = W.device
+    m = torch.empty(B, dtype=torch.int8, device=dev)
+    s = torch.empty(B, dtype=torch.int8, device=dev)
+    e1 = torch.empty(B, dtype=torch.float64, device=dev)
+    e2 = torch.empty(B, dtype=torch.float64, device=dev)
+    norms = torch.empty(B, 2, dtype=torch.float64, device=dev)
+    mults = torch.empty(B, dtype=torch.int32, device=dev)
+    nonfinite = torch.empty(B, dtype=torch.uint8, device=dev)
+    L = _lib.lib()
+    dt = _lib.EXPMB_F32 if W.dtype == torch.float32 else _lib.EXPMB_F64
+    wsb = int(L.expmb_workspace_bytes(B, n, dt, scheme))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        rc = L.expmb_select(W.data_ptr(), B, n, dt, float(eps), scheme, m.data_ptr(), s.data_ptr(), e1.data_ptr(),
+                            e2.data_ptr(), norms.data_ptr(), mults.data_ptr(), nonfinite.data_ptr(), ws.data_ptr(),
+                            wsb, torch.cuda.current_stream(dev).cuda_stream)
+    if rc != 0:
+        _raise_rc(rc)
+    return m, s, e1, e2, norms, mults, nonfinite
 
 
-def select_ps(W: torch.Tensor, eps: float) -> EvalPlan:
-    """select.py:223-225, batched."""
-    return expm(W, eps, SCHEME_PS, check_finite=False).plan
+@_select_op.register_fake
+def _(W, eps, scheme):
+    B = W.shape[0]
+    return (W.new_empty(B, dtype=torch.int8), W.new_empty(B, dtype=torch.int8), W.new_empty(B, dtype=torch.float64),
+            W.new_empty(B, dtype=torch.float64), W.new_empty(B, 2, dtype=torch.float64),
+            W.new_empty(B, dtype=torch.int32), W.new_empty(B, dtype=torch.uint8))
+
+
+def _select(W: torch.Tensor, eps: float, scheme: str, check_finite: bool) -> EvalPlan:
+    Wc, code = _validate(W, eps, scheme)
+    lead = W.shape[:-2]
+    m, s, e1, e2, norms, _, nonfinite = torch.ops.expmkit_b200.select(Wc, float(eps), code)
+    if check_finite and Wc.shape[0] > 0 and bool(nonfinite.any()):
+        idx = torch.nonzero(nonfinite).flatten()[:8].tolist()
+        raise NonFiniteError(f"operation produced non-finite entries (batch indices {idx}...)")
+    return EvalPlan(m.reshape(lead), s.reshape(lead), scheme, e1.reshape(lead), e2.reshape(lead),
+                    norms.reshape(*lead, 2))
+
+
+def select_sastre(W: torch.Tensor, eps: float, check_finite: bool = True) -> EvalPlan:
+    """select.py:228-234, batched: ||W||_1, W^2 and ||W^2||_1 only where the
+    ladder needs them, then the (m, s) choice -- no exponential is formed
+    (expmb_select).  Raises NonFiniteError like the reference when the input
+    or W^2 is not finite (matrix.py:56-57, 95-102)."""
+    return _select(W, eps, SCHEME_SASTRE, check_finite)
+
+
+def select_ps(W: torch.Tensor, eps: float, check_finite: bool = True) -> EvalPlan:
+    """select.py:223-225, batched: the Paterson-Stockmeyer ladder (W^2, W^3,
+    W^4 as needed), plan only."""
+    return _select(W, eps, SCHEME_PS, check_finite)
 
 
 # ---------------------------------------------------------------------------

@@ -300,7 +300,6 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
                size_t workspace_bytes, void* stream) {
   if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
   if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS && scheme != EXPMB_BASELINE) return EXPMB_ERR_SCHEME;
-  if (scheme == EXPMB_BASELINE && n > 64) return EXPMB_ERR_UNSUPPORTED;
   if (n < 1 || batch < 0) return EXPMB_ERR_SHAPE;
   if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
   if (((uintptr_t)W | (uintptr_t)X) & 15u) return EXPMB_ERR_ALIGN;
@@ -326,6 +325,42 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
   return large_expm(W, X, batch, n, dtype, eps, scheme, po, workspace, st);
+}
+
+int expmb_select(const void* W, int64_t batch, int32_t n, int dtype, double eps, int scheme, int8_t* m, int8_t* s,
+                 double* e1, double* e2, double* norms, int32_t* mults, uint8_t* nonfinite, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
+  if (scheme != EXPMB_SASTRE && scheme != EXPMB_PS) return EXPMB_ERR_SCHEME;
+  if (n < 1 || batch < 0) return EXPMB_ERR_SHAPE;
+  if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
+  if (((uintptr_t)W) & 15u) return EXPMB_ERR_ALIGN;
+  if (batch == 0) return EXPMB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  PlanOut po{m, s, e1, e2, norms, mults, nonfinite, 1};
+  if (n <= 64) {
+    // the generic fused kernels (step machine) stop after the ladder
+    int* ctr = (workspace != nullptr && workspace_bytes >= sizeof(int)) ? (int*)workspace : nullptr;
+    if (dtype == EXPMB_F32) {
+      const float* w = (const float*)W;
+      if (n <= 16) return scheme == 0 ? launch_fused<float, 16, 2, 8, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                                      : launch_fused<float, 16, 2, 8, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+      if (n <= 32) return scheme == 0 ? launch_fused<float, 32, 4, 4, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                                      : launch_fused<float, 32, 4, 4, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+      return scheme == 0 ? launch_fused<float, 64, 4, 1, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                         : launch_fused<float, 64, 4, 1, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+    }
+    const double* w = (const double*)W;
+    if (n <= 16) return scheme == 0 ? launch_fused<double, 16, 2, 8, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                                    : launch_fused<double, 16, 2, 8, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+    if (n <= 32) return scheme == 0 ? launch_fused<double, 32, 4, 4, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                                    : launch_fused<double, 32, 4, 4, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+    return scheme == 0 ? launch_fused<double, 64, 4, 1, 0>(w, nullptr, batch, n, eps, po, ctr, st)
+                       : launch_fused<double, 64, 4, 1, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+  }
+  const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
+  if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
+  return large_expm(W, nullptr, batch, n, dtype, eps, scheme, po, workspace, st);
 }
 
 int expmb_expm_pipelined(const void* W_host, void* X_host, void* W_dev, void* X_dev, int64_t batch, int32_t n,

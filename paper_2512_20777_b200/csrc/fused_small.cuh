@@ -30,6 +30,15 @@
 #ifndef EXPMB_HM_RL
 #define EXPMB_HM_RL 1  // HM products take the left operand from registers
 #endif
+#ifndef EXPMB_HM_ASCALAR
+#define EXPMB_HM_ASCALAR 1  // A-fragment tf32 splits scalar (no pair moves; measured 80.5 -> 79.7 us on C2 with the two below)
+#endif
+#ifndef EXPMB_HM_NV
+#define EXPMB_HM_NV 1  // HMMA asm not volatile
+#endif
+#ifndef EXPMB_HM_ILV
+#define EXPMB_HM_ILV 1  // interleave the two column tiles' HMMA chains
+#endif
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -65,6 +74,7 @@ struct PlanOut {
   double* norms;
   int32_t* mults;
   uint8_t* nonfinite;
+  int plan_only;  // 1: select only (select.py:223-234) -- form the ladder's powers, write the plan, no e^W
 };
 
 template <typename T>
@@ -353,7 +363,11 @@ struct Fused {
     l1 = __float_as_uint(lo.y);
   }
   __device__ __forceinline__ static void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+#if EXPMB_HM_NV
+    asm(  // pure function of its operands: the compiler may schedule it
+#else
     asm volatile(
+#endif
         "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -408,7 +422,15 @@ struct Fused {
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       uint32_t ah[4], al[4];
-#if EXPMB_HM_SPLIT2
+#if EXPMB_HM_ASCALAR
+      // scalar splits: the A fragment needs four consecutive registers in the
+      // order (row g, row g+8) x (k, k+4); packed (FADD2) residuals come out
+      // paired along columns and cost a register move each
+      split_tf32(Lt[0][2 * ks], ah[0], al[0]);
+      split_tf32(Lt[1][2 * ks], ah[1], al[1]);
+      split_tf32(Lt[0][2 * ks + 1], ah[2], al[2]);
+      split_tf32(Lt[1][2 * ks + 1], ah[3], al[3]);
+#elif EXPMB_HM_SPLIT2
       split_tf32_2(Lt[0][2 * ks], Lt[0][2 * ks + 1], ah[0], al[0], ah[2], al[2]);
       split_tf32_2(Lt[1][2 * ks], Lt[1][2 * ks + 1], ah[1], al[1], ah[3], al[3]);
 #else
@@ -417,20 +439,34 @@ struct Fused {
       split_tf32(Lt[0][2 * ks + 1], ah[2], al[2]);
       split_tf32(Lt[1][2 * ks + 1], ah[3], al[3]);
 #endif
+      uint32_t bh[2][2], bl[2][2];
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
-        uint32_t bh0, bl0, bh1, bl1;
 #if EXPMB_HM_SPLIT2
-        split_tf32_2(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh0,
-                     bl0, bh1, bl1);
+        split_tf32_2(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8],
+                     bh[nt][0], bl[nt][0], bh[nt][1], bl[nt][1]);
 #else
-        split_tf32(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], bh0, bl0);
-        split_tf32(R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh1, bl1);
+        split_tf32(R[(8 * ks + 2 * t4) * LDR2 + 8 * nt + g8], bh[nt][0], bl[nt][0]);
+        split_tf32(R[(8 * ks + 2 * t4 + 1) * LDR2 + 8 * nt + g8], bh[nt][1], bl[nt][1]);
 #endif
-        hmma(acc[nt], al, bh0, bh1);  // small terms first
-        hmma(acc[nt], ah, bl0, bl1);
-        hmma(acc[nt], ah, bh0, bh1);
       }
+#if EXPMB_HM_ILV
+      // the two column tiles' chains interleaved: consecutive HMMAs are
+      // independent (the 'wait' stall on the accumulator dependency)
+      hmma(acc[0], al, bh[0][0], bh[0][1]);  // small terms first
+      hmma(acc[1], al, bh[1][0], bh[1][1]);
+      hmma(acc[0], ah, bl[0][0], bl[0][1]);
+      hmma(acc[1], ah, bl[1][0], bl[1][1]);
+      hmma(acc[0], ah, bh[0][0], bh[0][1]);
+      hmma(acc[1], ah, bh[1][0], bh[1][1]);
+#else
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        hmma(acc[nt], al, bh[nt][0], bh[nt][1]);  // small terms first
+        hmma(acc[nt], ah, bl[nt][0], bl[nt][1]);
+        hmma(acc[nt], ah, bh[nt][0], bh[nt][1]);
+      }
+#endif
     }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -929,6 +965,10 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
           step = need == 3 ? ST_W3 : ST_W4;
           continue;
         }
+        if (po.plan_only) {  // select_sastre / select_ps: the plan is all the caller wants
+          step = ST_DONE;
+          break;
+        }
         decided();
         if constexpr (SCHEME == 1) {
           const T sc3 = pow2_neg<T>(3 * p.s), sc4 = pow2_neg<T>(4 * p.s);
@@ -1001,13 +1041,13 @@ expm_fused_kernel(const T* __restrict__ W, T* __restrict__ X, int64_t batch, int
     mults = budget(p.m, SCHEME) + p.s;
     }  // SCHEME != 2
 
-    {  // x * 0 is NaN exactly when x is Inf/NaN: one check per lane instead of eight
+    if (!po.plan_only) {  // x * 0 is NaN exactly when x is Inf/NaN: one check per lane instead of eight
       Pr<T> z{T(0), T(0)};
       EW2(z = pfma(GP(P), T(0), z));
       bad |= !(z.x == T(0) && z.y == T(0));
     }
     bad = f.any_group(bad);
-    f.save(X + idx * nn, n, vec, P);
+    if (!po.plan_only) f.save(X + idx * nn, n, vec, P);
     if (f.t == 0) {
       if (po.m) po.m[idx] = (int8_t)(p.m < 127 ? p.m : 127);  // Alg. 1 may exceed int8: saturate
       if (po.s) po.s[idx] = (int8_t)(p.s < 127 ? p.s : 127);

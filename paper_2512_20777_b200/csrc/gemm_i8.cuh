@@ -52,6 +52,11 @@ namespace i8 {
 #ifndef EXPMB_I8_STAGES
 #define EXPMB_I8_STAGES (EXPMB_I8_BK64 ? 2 : 1)
 #endif
+// EXPMB_I8_CAT: slice i of L against the R slices 0..3-i stacked along N in
+// one MMA (4 MMAs per 32-byte k-step); 0: the ten slice-pair MMAs
+#ifndef EXPMB_I8_CAT
+#define EXPMB_I8_CAT 1
+#endif
 constexpr int BM = 128, BN = 64, BKB = EXPMB_I8_BK64 ? 64 : 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
 constexpr bool kSw64 = BKB == 64;
 // UMMA shared-memory descriptor, K-major: 64B swizzle (8-row atoms of 512 B) or 128B (1024 B)
@@ -173,12 +178,14 @@ __device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, int stage
   }
 }
 // Units (slot, 32x32 tile) over the first *dcount slots, grid-strided.
-__global__ void __launch_bounds__(256) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b, const int* __restrict__ dcount, int hcount) {
+// (8 CTAs/SM: the per-unit work is a short latency chain, occupancy hides it)
+__global__ void __launch_bounds__(256, 8) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                      Bufs b, const int* __restrict__ dcount, int hcount) {
   const int cnt = dcount ? *dcount : hcount;
   const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
-  for (int64_t w = blockIdx.x; w < (int64_t)cnt * tiles; w += gridDim.x) {
-    const int slot = (int)(w / tiles), t = (int)(w - (int64_t)slot * tiles);
+  const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int slot = w / tiles, t = w - slot * tiles;
     __syncthreads();  // shared tiles of the previous unit
     i8_stats_tile(g, stage, list, b, slot, t % t32, t / t32);
   }
@@ -287,12 +294,13 @@ __device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, int stage
     }
   }
 }
-__global__ void __launch_bounds__(256) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                   Bufs b, const int* __restrict__ dcount, int hcount) {
+__global__ void __launch_bounds__(256, 8) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
+                                                      Bufs b, const int* __restrict__ dcount, int hcount) {
   const int cnt = dcount ? *dcount : hcount;
   const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
-  for (int64_t w = blockIdx.x; w < (int64_t)cnt * tiles; w += gridDim.x) {
-    const int slot = (int)(w / tiles), t = (int)(w - (int64_t)slot * tiles);
+  const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int slot = w / tiles, t = w - slot * tiles;
     __syncthreads();  // the transpose tile of the previous unit
     i8_slice_tile(g, stage, list, b, slot, t % t32, t / t32);
   }
@@ -371,8 +379,8 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   const int KT = (n + BKB - 1) / BKB;
   const int cnt = dcount ? *dcount : hcount;
   const int tn = (n + BN - 1) / BN, tm = (n + BM - 1) / BM, tiles = tn * tm;
-  const int64_t total = (int64_t)cnt * tiles;
-  if ((int64_t)blockIdx.x >= total) return;  // uniform: no unit for this CTA
+  const int total = cnt * tiles;  // < 2^31: slots x (128 x 64) tiles of a chunk
+  if ((int)blockIdx.x >= total) return;  // uniform: no unit for this CTA
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -394,10 +402,22 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_sh;
 
-  // every role walks the same unit sequence and skips the same units
-  auto unit = [&](int64_t w, int& slot, int& z, int& bx, int& by, Epi<float>& e) -> bool {
-    slot = (int)(w / tiles);
-    const int t = (int)(w - (int64_t)slot * tiles);
+  // every role walks the same unit sequence and skips the same units: the
+  // producer and the MMA issuer use the light test (a slot of a stage list
+  // always needs its stage; the power stages run on every matrix that asked
+  // for that power), the epilogue builds the full stage program (make_epi)
+  const int pw = stage == STAGE_W2 ? 2 : stage == STAGE_W3 ? 3 : stage == STAGE_W4 ? 4 : 0;
+  auto unit_light = [&](int w, int& slot, int& bx, int& by) -> bool {
+    slot = w / tiles;
+    const int t = w - slot * tiles;
+    bx = t % tn;
+    by = t / tn;
+    if (!bf.ok[slot]) return false;  // routed to the FFMA GEMM
+    return pw == 0 || g.need[list ? list[slot] : slot] == pw;
+  };
+  auto unit = [&](int w, int& slot, int& z, int& bx, int& by, Epi<float>& e) -> bool {
+    slot = w / tiles;
+    const int t = w - slot * tiles;
     bx = t % tn;
     by = t / tn;
     if (!bf.ok[slot]) return false;  // routed to the FFMA GEMM
@@ -408,10 +428,9 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: 4 L slices + 4 R slices per k-tile ----------------
     uint32_t it = 0;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-      int slot, z, bx, by;
-      Epi<float> e;
-      if (!unit(w, slot, z, bx, by, e)) continue;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int slot, bx, by;
+      if (!unit_light(w, slot, bx, by)) continue;
       const int m0 = by * BM, n0 = bx * BN;
       for (int kt = 0; kt < KT; ++kt, ++it) {
         const int st = it % STAGES;
@@ -428,10 +447,9 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: 4 concatenated-slice MMAs per 32-byte k-step ----------------
     uint32_t it = 0, u = 0;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-      int slot, z, bx, by;
-      Epi<float> e;
-      if (!unit(w, slot, z, bx, by, e)) continue;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int slot, bx, by;
+      if (!unit_light(w, slot, bx, by)) continue;
       tc::mbar_wait(&tempty_bar, (u & 1) ^ 1);  // the epilogue has drained the accumulators
       asm volatile("tcgen05.fence::after_thread_sync;");
       for (int kt = 0; kt < KT; ++kt, ++it) {
@@ -444,6 +462,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
         const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
 #pragma unroll
         for (int k = 0; k < BKB / 32; ++k) {
+#if EXPMB_I8_CAT
 #pragma unroll
           for (int i = 0; i < NSL; ++i) {
             const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
@@ -451,6 +470,18 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
             // i = 0 covers every level: its first MMA of the unit initialises them all
             mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
           }
+#else
+#pragma unroll
+          for (int lv = 0; lv < 4; ++lv) {
+#pragma unroll
+            for (int i = 0; i <= lv; ++i) {
+              const int j = lv - i;
+              const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
+              const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + k * 32) >> 4);
+              mma_i8(tmem + (uint32_t)(lv * BN), a, bd, (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
+            }
+          }
+#endif
         }
         tc::mma_commit(&empty_bar[st]);
       }
@@ -466,7 +497,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
     const int rl = q * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
     uint32_t u = 0;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int slot, z, bx, by;
       Epi<float> e;
       if (!unit(w, slot, z, bx, by, e)) continue;
@@ -642,6 +673,250 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
+
+// One-unit-per-CTA form of the stage (grid: column blocks x row blocks x
+// slots, slots beyond the device count exit at once); A/B against the
+// persistent k_i8_stage (EXPMB_I8_PERSIST).
+__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
+k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs bf,
+              const int* __restrict__ dcount) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ double cs_sh[BN];  // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
+  __shared__ float dr_sh[BN];   // diagonal of R for this CTA's columns
+  const int slot = blockIdx.z;
+  if (dcount != nullptr && slot >= *dcount) return;  // beyond the device-resident bucket size
+  if (!bf.ok[slot]) return;  // routed to the FFMA GEMM
+  const int z = list ? list[slot] : slot;
+  Epi<float> e;
+  if (!make_epi(g, stage, z, e)) return;  // uniform per CTA
+
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = g.n;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int KT = (n + BKB - 1) / BKB;
+
+  if (threadIdx.x < BN) {
+    const int c = n0 + threadIdx.x;
+    const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
+    cs_sh[threadIdx.x] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
+    dr_sh[threadIdx.x] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(&full_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], 1);
+    }
+    tc::mbar_init(&tmem_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: 4 L slices + 4 R slices per k-tile ----------------
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      tc::mbar_wait(&empty_bar[st], ((kt / STAGES) & 1) ^ 1);
+      unsigned char* b = sm + st * STAGE_BYTES;
+      tc::mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+#pragma unroll
+      for (int i = 0; i < NSL; ++i) {
+        tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
+        tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: ten slice pairs per 32-byte k-step ----------------
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      tc::mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = tc::smem_u32(sm + st * STAGE_BYTES);
+      // descriptors built once per stage; the slice / k-step offsets go into
+      // the 16-byte-unit address field (smem < 256 KB: no carry out of it)
+      const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
+#pragma unroll
+      for (int k = 0; k < BKB / 32; ++k) {
+#pragma unroll
+        for (int i = 0; i < NSL; ++i) {
+          const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((k * 32) >> 4);
+          mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
+        }
+      }
+      tc::mma_commit(&empty_bar[st]);
+    }
+    tc::mma_commit(&tmem_bar);
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    // 16-column chunks keep the live arrays small enough for 2 CTAs/SM
+    // without spills.
+    constexpr int CW = 16;
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    const int r = m0 + rl;
+    const bool rowok = r < n;
+    // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
+    // the int8 GEMM carries Yl Yr (each row / column scaled without its
+    // diagonal, which in the squaring phase dominates), the rest is exact
+    // elementwise work here, all summed in binary64 and rounded once.  The
+    // operand rows of the first chunk are fetched while the MMAs still run.
+    float lrow[CW], rrow[CW];
+#define I8_LOAD_ROWS(C0)                                                                       \
+  do {                                                                                         \
+    const int c0_ = (C0);                                                                      \
+    if (rowok && c0_ + CW <= n) {                                                              \
+      const float4* lp = reinterpret_cast<const float4*>(e.L + (size_t)r * n + c0_);           \
+      const float4* rp = reinterpret_cast<const float4*>(e.R + (size_t)r * n + c0_);           \
+      _Pragma("unroll") for (int j = 0; j < CW / 4; ++j) {                                     \
+        const float4 a = __ldg(lp + j);                                                        \
+        lrow[4 * j] = a.x; lrow[4 * j + 1] = a.y; lrow[4 * j + 2] = a.z; lrow[4 * j + 3] = a.w; \
+        const float4 bb = (e.R == e.L) ? a : __ldg(rp + j);                                    \
+        rrow[4 * j] = bb.x; rrow[4 * j + 1] = bb.y; rrow[4 * j + 2] = bb.z; rrow[4 * j + 3] = bb.w; \
+      }                                                                                        \
+    } else {                                                                                   \
+      _Pragma("unroll") for (int j = 0; j < CW; ++j) {                                         \
+        const bool ok_ = rowok && c0_ + j < n;                                                 \
+        lrow[j] = ok_ ? e.L[(size_t)r * n + c0_ + j] : 0.f;                                     \
+        rrow[j] = ok_ ? e.R[(size_t)r * n + c0_ + j] : 0.f;                                     \
+      }                                                                                        \
+    }                                                                                          \
+  } while (0)
+    I8_LOAD_ROWS(n0);
+    const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+    const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
+    const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
+    tc::mbar_wait(&tmem_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
+#pragma unroll 1
+    for (int cb = 0; cb < BN / CW; ++cb) {
+      int a0[CW], a1[CW], a2[CW], a3[CW];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
+      tmem_ld16i(ta, a0);
+      tmem_ld16i(ta + BN, a1);
+      tmem_ld16i(ta + 2 * BN, a2);
+      tmem_ld16i(ta + 3 * BN, a3);
+      const int c0 = n0 + cb * CW;
+      const bool full = rowok && c0 + CW <= n;
+      if (cb > 0) I8_LOAD_ROWS(c0);
+      float o0[CW];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int c = c0 + j;
+        // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49) and a
+        // single int -> binary64 conversion (the conversion unit was the hot pipe)
+        const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
+                            (long long)a3[j];
+        double y = (double)T * rs21 * cs_sh[cb * CW + j];
+        const double dr = (double)dr_sh[cb * CW + j];
+        y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
+        o0[j] = e.alpha * (float)y;
+      }
+      for (int qq = 0; qq < e.nin; ++qq) {
+        const float cq = e.c[0][qq];
+        if (cq == 0.f || !rowok) continue;
+        const float* ip = e.in[qq] + (size_t)r * n + c0;
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
+            o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
+            o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW; ++j)
+            if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
+        }
+      }
+      if (e.d[0] != 0.f && r >= c0 && r < c0 + CW) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j)
+          if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
+      }
+      if (rowok) {
+        float* op = e.out[0] + (size_t)r * n + c0;
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < CW; j += 4)
+            *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW; ++j)
+            if (c0 + j < n) op[j] = o0[j];
+        }
+      }
+      for (int k = 1; k < e.nout; ++k) {
+        float ok[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) ok[j] = o0[j];
+        for (int qq = 0; qq < e.nin; ++qq) {
+          const float cq = e.c[k][qq];
+          if (cq == 0.f || !rowok) continue;
+          const float* ip = e.in[qq] + (size_t)r * n + c0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < CW; j += 4) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
+              ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
+              ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j)
+              if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
+          }
+        }
+        if (e.d[k] != 0.f && r >= c0 && r < c0 + CW) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j)
+            if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
+        }
+        if (rowok) {
+          float* op = e.out[k] + (size_t)r * n + c0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < CW; j += 4)
+              *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j)
+              if (c0 + j < n) op[j] = ok[j];
+          }
+        }
+      }
+      if (e.colnorm) {
+        // deterministic column abs-sums of this 128-row tile (select.py:193)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (rl < CW && c0 + rl < n) {
+          double a = 0.0;
+          for (int rr = 0; rr < BM; ++rr) a += red[rl * BM + rr];
+          g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + c0 + rl] = a;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+#undef I8_LOAD_ROWS
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 
 }  // namespace i8
 }  // namespace expmb

@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -29,7 +30,9 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 128;
 constexpr int kGemmBK = 8;
 
-enum Stage { STAGE_W2 = 0, STAGE_W3, STAGE_W4, STAGE_E1, STAGE_E2, STAGE_E3, STAGE_SQ };
+enum Stage { STAGE_W2 = 0, STAGE_W3, STAGE_W4, STAGE_E1, STAGE_E2, STAGE_E3, STAGE_SQ,
+             STAGE_A1,      // Alg. 1 term (engine.py:109-112): X += Y; Y <- B Y / k, k = sq_step + 2
+             STAGE_A1SQ };  // Alg. 1 squaring (engine.py:113): s from the int32 array s32
 
 template <typename T>
 struct GemmCtx {
@@ -47,6 +50,7 @@ struct GemmCtx {
   const int* need;
   double* part;
   const int* route;  // per list slot: 1 = another backend (the int8-slice GEMM) handles it; may be null
+  const int* s32;    // Alg. 1: per-matrix scaling (may exceed int8)
 };
 
 template <typename T>
@@ -60,6 +64,8 @@ struct Epi {
   T c[3][4];
   T d[3];
   T* out[3];
+  const T* acc_src;  // Alg. 1: acc_dst += acc_src elementwise (X += Y, engine.py:110)
+  T* acc_dst;
 };
 
 // pre-squaring target for a matrix squared s times: the buffer that, after s
@@ -74,6 +80,7 @@ __device__ __forceinline__ bool make_epi(const GemmCtx<T>& g, int stage, int z, 
   const int64_t o = (int64_t)z * g.mstride;
   const T* Wz = g.W + (int64_t)z * g.wstride;
   e.nin = 0; e.nout = 1; e.colnorm = false; e.alpha = T(1);
+  e.acc_src = nullptr; e.acc_dst = nullptr;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     e.d[k] = T(0);
@@ -87,6 +94,27 @@ __device__ __forceinline__ bool make_epi(const GemmCtx<T>& g, int stage, int z, 
     e.R = Wz;
     e.out[0] = p == 2 ? g.W2 + o : (p == 3 ? g.W3 + o : g.W4 + o);
     e.colnorm = true;
+    return true;
+  }
+  if (stage == STAGE_A1) {
+    // term j = sq_step (k = j + 2): the product B Y_j / k with B = 2^-s W
+    // stored in W2, Y ping-ponging between Y0 / Y1; X += Y_j fused into the
+    // same pass; column sums of Y_{j+1} for the termination test
+    const int j = g.sq_step;
+    e.L = g.W2 + o;
+    e.R = ((j & 1) ? g.Y1 : g.Y0) + o;
+    e.out[0] = ((j & 1) ? g.Y0 : g.Y1) + o;
+    e.alpha = T(1) / T(j + 2);  // Y / k taken as Y * fl(1/k), as the fused kernel
+    e.colnorm = true;
+    e.acc_src = e.R;
+    e.acc_dst = sq_target(g, z, g.s32[z], 0);
+    return true;
+  }
+  if (stage == STAGE_A1SQ) {
+    const int s = g.s32[z];
+    if (s <= g.sq_step) return false;
+    e.L = e.R = sq_target(g, z, s, g.sq_step);
+    e.out[0] = sq_target(g, z, s, g.sq_step + 1);
     return true;
   }
   const int m = g.m[z], s = g.s[z];
@@ -434,6 +462,12 @@ __device__ __forceinline__ void gemm_tile(const GemmCtx<T>& g, int stage, const 
         }
       };
       put(e.out[0], o0);
+      if (e.acc_dst != nullptr) {  // X += Y (Alg. 1): the same positions, one read-modify-write
+        T xv[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) xv[v] = (col0 + v < n) ? e.acc_dst[pos + v] + e.acc_src[pos + v] : T(0);
+        put(e.acc_dst, xv);
+      }
       if (e.nout > 1) {
 #pragma unroll
         for (int k = 1; k < 3; ++k) {
@@ -523,13 +557,22 @@ static inline int sm_count_dev() {
   return cached[dev];
 }
 
-// Persistent grid size for a kernel: resident CTAs per SM x SMs, capped by the work.
+// Persistent grid size for a kernel: resident CTAs per SM x SMs, capped by
+// the work.  `resident` is the residency the kernel's __launch_bounds__
+// guarantees (its minBlocksPerMultiprocessor, which register and shared
+// memory use are built to meet); 0 asks the occupancy API instead.  (On this
+// driver the API reported 1 CTA/SM for kernels the hardware runs two per SM
+// -- the int8 and 2-CTA FFMA stages -- so the launch bounds are the source of
+// truth where they exist.)
 template <typename K>
-static int persistent_grid(K kern, int threads, size_t smem, int64_t units, int* occ_cache) {
+static int persistent_grid(K kern, int threads, size_t smem, int64_t units, int* occ_cache, int resident = 0) {
   if (*occ_cache <= 0) {
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess || o < 1) o = 1;
+    int o = resident;
+    if (o <= 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess || o < 1))
+      o = 1;
     *occ_cache = o;
+    if (getenv("EXPMB_DEBUG_OCC"))
+      fprintf(stderr, "expmb occupancy: %d CTAs/SM (%d threads, %zu B dynamic smem)\n", o, threads, smem);
   }
   const int64_t cap = (int64_t)sm_count_dev() * *occ_cache;
   return (int)(units < cap ? (units < 1 ? 1 : units) : cap);
@@ -558,13 +601,13 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
   const int64_t units = (int64_t)count * tn * tm;
   static const bool dmma = !(getenv("EXPMB_NO_DMMA") && getenv("EXPMB_NO_DMMA")[0] == '1');
   if (sizeof(T) == 4 && g.n > 512)
-    k_two<<<persistent_grid(k_two, 256, smem, units, &occ[0]), 256, smem, st>>>(g, stage, list, dcount, count);
+    k_two<<<persistent_grid(k_two, 256, smem, units, &occ[0], 1), 256, smem, st>>>(g, stage, list, dcount, count);
   else if (sizeof(T) == 8 && dmma)
-    k_mma<<<persistent_grid(k_mma, 256, smem, units, &occ[2]), 256, smem, st>>>(g, stage, list, dcount, count);
+    k_mma<<<persistent_grid(k_mma, 256, smem, units, &occ[2], 1), 256, smem, st>>>(g, stage, list, dcount, count);
   else {
     // z-stride grid (kZStride): tiles x enough slots to fill every resident CTA once
     const int t2 = tn * tm;
-    const int zc = std::max(1, persistent_grid(k_one, 256, smem, units, &occ[1]) / t2);
+    const int zc = std::max(1, persistent_grid(k_one, 256, smem, units, &occ[1], sizeof(T) == 4 ? 2 : 1) / t2);
     k_one<<<dim3(tn, tm, std::min(count, zc)), 256, smem, st>>>(g, stage, list, dcount, count);
   }
   return cudaGetLastError() != cudaSuccess;

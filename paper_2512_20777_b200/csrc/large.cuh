@@ -22,6 +22,7 @@
 // coefficients; they are powers of two so the folding is exact.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
   }
   if (threadIdx.x == 0) {
     nrm4[4 * z + have - 1] = red[0];
-    if (have == 1) nrm4[4 * z + 1] = NAN;
+    if (have == 1) nrm4[4 * z + 1] = nrm4[4 * z + 2] = nrm4[4 * z + 3] = NAN;
     double nr[4];
     for (int q = 0; q < 4; ++q) nr[q] = nrm4[4 * z + q];
     Plan p{0, 0, 0.0, 0.0};
@@ -204,7 +205,9 @@ __global__ void __launch_bounds__(256) k_finish(int cnt, int scheme, const doubl
     if (po.e2) po.e2[g] = pe2[z];
     if (po.norms) { po.norms[2 * g] = n1; po.norms[2 * g + 1] = n2; }
     if (po.mults) po.mults[g] = budget(m, scheme) + s;
-    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || !(n1 < INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
+    const double n3 = nrm4[4 * z + 2], n4 = nrm4[4 * z + 3];
+    const bool pw_bad = scheme == 1 && ((n3 == n3 && !(n3 < INFINITY)) || (n4 == n4 && !(n4 < INFINITY)));
+    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || pw_bad || !(n1 < INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
   }
 }
 
@@ -340,16 +343,29 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
   const int64_t u32 = (int64_t)count * t32 * t32;
   i8::k_i8_zero<<<persistent_grid(i8::k_i8_zero, 256, 0, ((int64_t)count * n + 255) / 256, &occ_zero), 256, 0, st>>>(
       b, n, dcount, count);
-  i8::k_i8_stats<<<persistent_grid(i8::k_i8_stats, 256, 0, u32, &occ_stats), 256, 0, st>>>(g, stage, list, b,
+  i8::k_i8_stats<<<persistent_grid(i8::k_i8_stats, 256, 0, u32, &occ_stats, 8), 256, 0, st>>>(g, stage, list, b,
                                                                                             dcount, count);
   if (chk("stats")) return 1;
   i8::k_i8_route<<<std::min(count, sm_count_dev() * 8), 256, 0, st>>>(g, stage, list, b, dcount, count);
   if (chk("route")) return 1;
-  i8::k_i8_slice<<<persistent_grid(i8::k_i8_slice, 256, 0, u32, &occ_slice), 256, 0, st>>>(g, stage, list, b,
+  i8::k_i8_slice<<<persistent_grid(i8::k_i8_slice, 256, 0, u32, &occ_slice, 8), 256, 0, st>>>(g, stage, list, b,
                                                                                             dcount, count);
   if (chk("slice")) return 1;
+  static const bool persist = getenv("EXPMB_I8_PERSIST") && getenv("EXPMB_I8_PERSIST")[0] == '1';
+  static bool attr_np = false;
+  if (!persist) {
+    if (!attr_np) {
+      if (cudaFuncSetAttribute(i8::k_i8_stage_np, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::SMEM_BYTES) !=
+          cudaSuccess)
+        return 1;
+      attr_np = true;
+    }
+    i8::k_i8_stage_np<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS,
+                        i8::SMEM_BYTES, st>>>(maps, g, stage, list, b, dcount);
+  }
   const int64_t units = (int64_t)count * ((n + i8::BN - 1) / i8::BN) * ((n + i8::BM - 1) / i8::BM);
-  i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS, i8::SMEM_BYTES, units, &occ_stage), i8::NTHREADS,
+  if (persist) i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS, i8::SMEM_BYTES, units, &occ_stage,
+                                   i8::STAGE_BYTES * i8::STAGES <= 100 * 1024 ? 2 : 1), i8::NTHREADS,
                    i8::SMEM_BYTES, st>>>(maps, g, stage, list, b, dcount, count);
   {
     const cudaError_t le = cudaGetLastError();
@@ -440,6 +456,13 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
     k_select<<<ic, 256, 0, st>>>(part, L.tiles_m, n, p, log_eps, scheme, nrm4, need, dm, ds, de1, de2);
   }
 
+  if (po.plan_only) {  // select_sastre / select_ps (select.py:223-234): the plan only
+    int* flags = reinterpret_cast<int*>(ws + L.off_flags);
+    if (cudaMemsetAsync(flags, 0, (size_t)ic * sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
+    k_finish<<<(ic + 255) / 256, 256, 0, st>>>(ic, scheme, nrm4, dm, ds, de1, de2, flags, base, po);
+    return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+  }
+
   // device bucket scheduler: stage lists + their sizes stay on the device
   int* dcnt = reinterpret_cast<int*>(ws + L.off_cnt);
   k_bucket<<<1, 1024, 0, st>>>(dm, ds, ic, scheme, dlist, dcnt);
@@ -454,6 +477,225 @@ static int large_run_chunk(const T* W, T* X, int64_t cnt, int n, double eps, int
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
+// ---------------------------------------------------------------------------
+// Alg. 1 for n > 64 (engine.py:90-116, the paper's comparator), sync-free:
+// the term loop and the squaring loop are data dependent per matrix, so the
+// host launches a bounded number of term stages over device-resident active
+// lists, and one cooperative kernel runs every squaring level (grid-wide
+// barrier between levels, as many levels as the largest s of the batch).
+// ---------------------------------------------------------------------------
+constexpr int kA1MaxTerms = 40;  // ||B||_1 < 1/2: ||B^k / k!||_1 < 2^-53 by k = 16 (the fused kernel caps at 398)
+constexpr int kA1MaxS = 1100;    // ||W||_1 <= 2^1024 (the fused kernel's cap)
+
+// ||W||_1 from the slab partials, s = min{s >= 0 : ||W||_1 2^-s < 1/2}
+// (engine.py:102-104), the first termination test ||B||_1 > eps, and the
+// initial active list of the term loop.
+__global__ void __launch_bounds__(256) k_a1_init(const double* __restrict__ part, int tiles_m, int n, double eps,
+                                                 double* __restrict__ nrm4, int* __restrict__ s32,
+                                                 int* __restrict__ m32, double* __restrict__ pe1,
+                                                 int* __restrict__ list0, int* __restrict__ cnt) {
+  const int z = blockIdx.x;
+  __shared__ double red[256];
+  const double* pz = part + (size_t)z * tiles_m * n;
+  double mx = -INFINITY;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double a = 0.0;
+    for (int t = 0; t < tiles_m; ++t) a += pz[(size_t)t * n + c];
+    mx = nanmax(mx, a);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] = nanmax(red[threadIdx.x], red[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double n1 = red[0];
+    int s = 0;
+    if (n1 >= 0.5) {  // while ldexp(n1, -s) >= 1/2: s += 1
+      int e;
+      frexp(n1, &e);  // n1 = f 2^e, f in [1/2, 1)
+      s = (n1 <= 1e300) ? e + 1 : kA1MaxS;
+    }
+    if (!(n1 < INFINITY)) s = 0;  // NaN / Inf input: flagged (NonFiniteError), no work spent on it
+    nrm4[4 * z] = n1;
+    nrm4[4 * z + 1] = nrm4[4 * z + 2] = nrm4[4 * z + 3] = NAN;
+    s32[z] = s;
+    m32[z] = 0;
+    const double nb = ldexp(n1, -s);  // ||B||_1 exactly (power-of-two scaling)
+    pe1[z] = nb;
+    if (nb > eps) list0[atomicAdd(&cnt[0], 1)] = z;
+    atomicMax(&cnt[kA1MaxTerms + 1], s);
+  }
+}
+
+// B = 2^-s W (W2 buffer), Y_0 = B, X_0 = I (the buffer the squarings end in X from).
+template <typename T>
+__global__ void __launch_bounds__(256) k_a1_setup(GemmCtx<T> g, int ic) {
+  const size_t nn = (size_t)g.n * g.n;
+  for (int z = blockIdx.y; z < ic; z += gridDim.y) {
+    const int s = g.s32[z];
+    const int64_t o = (int64_t)z * g.mstride;
+    const T* Wz = g.W + (int64_t)z * g.wstride;
+    T* Xz = sq_target(g, z, s, 0);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x) {
+      const T b = (T)ldexp((double)Wz[i], -s);  // exact unless the result is subnormal (scale_pow2, matrix.py:159-167)
+      g.W2[o + i] = b;
+      g.Y0[o + i] = b;
+      Xz[i] = (i / g.n == i % g.n) ? T(1) : T(0);
+    }
+  }
+}
+
+// After term j: ||Y_{j+1}||_1 from the GEMM's column partials; the matrices
+// still above eps go on to term j + 1.
+__global__ void __launch_bounds__(256) k_a1_check(const double* __restrict__ part, int tiles_m, int n, double eps,
+                                                  int term, const int* __restrict__ list, const int* __restrict__ cnt,
+                                                  int* __restrict__ next, int* __restrict__ next_cnt,
+                                                  int* __restrict__ m32, double* __restrict__ pe1) {
+  __shared__ double red[256];
+  for (int slot = blockIdx.x; slot < *cnt; slot += gridDim.x) {
+    const int z = list[slot];
+    const double* pz = part + (size_t)z * tiles_m * n;
+    double mx = -INFINITY;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      double a = 0.0;
+      for (int t = 0; t < tiles_m; ++t) a += pz[(size_t)t * n + c];
+      mx = nanmax(mx, a);
+    }
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+      if (threadIdx.x < off) red[threadIdx.x] = nanmax(red[threadIdx.x], red[threadIdx.x + off]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double ny = red[0];
+      m32[z] = term + 1;  // products charged so far (one per term formed, engine.py:111)
+      pe1[z] = ny;
+      if (ny > eps) next[atomicAdd(next_cnt, 1)] = z;  // NaN stops, as the reference's comparison
+    }
+    __syncthreads();
+  }
+}
+
+// Every squaring level of the batch in one cooperative launch (engine.py:113):
+// level q squares the matrices with s > q; a grid-wide barrier separates the
+// levels, whose count is the batch's largest s (read on the device).
+template <typename T, bool TWO, bool MMA>
+__global__ void __launch_bounds__(256, 1) k_a1_square(GemmCtx<T> g, int ic, const int* __restrict__ maxs_ptr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int maxs = *maxs_ptr;
+  const int tn = (g.n + kGemmBN - 1) / kGemmBN, tiles = tn * g.tiles_m;
+  const int total = ic * tiles;
+  for (int q = 0; q < maxs; ++q) {
+    GemmCtx<T> gq = g;
+    gq.sq_step = q;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const int z = w / tiles, t = w - z * tiles;
+      if (g.s32[z] <= q) continue;  // done squaring (uniform per CTA)
+      __syncthreads();
+      gemm_tile<T, TWO, MMA>(gq, STAGE_A1SQ, nullptr, z, t % tn, t / tn, smem_raw);
+    }
+    __threadfence();
+    grid.sync();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_a1_finish(int ic, const double* __restrict__ nrm4, const int* __restrict__ s32,
+                                                   const int* __restrict__ m32, const double* __restrict__ pe1,
+                                                   const int* __restrict__ flags, int64_t base, PlanOut po) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  if (z < ic) {
+    const int64_t gi = base + z;
+    const int m = m32[z], s = s32[z];
+    const double n1 = nrm4[4 * z];
+    if (po.m) po.m[gi] = (int8_t)(m < 127 ? m : 127);  // int8 outputs saturate; mults is exact
+    if (po.s) po.s[gi] = (int8_t)(s < 127 ? s : 127);
+    if (po.e1) po.e1[gi] = pe1[z];
+    if (po.e2) po.e2[gi] = 0.0;
+    if (po.norms) { po.norms[2 * gi] = n1; po.norms[2 * gi + 1] = NAN; }
+    if (po.mults) po.mults[gi] = m + s;
+    if (po.nonfinite) po.nonfinite[gi] = (uint8_t)(flags[z] || !(n1 < INFINITY));
+  }
+}
+
+template <typename T>
+static int large_run_chunk_alg1(const T* W, T* X, int64_t cnt, int n, double eps, int64_t base, PlanOut po,
+                                unsigned char* ws, const LargeLayout& L, cudaStream_t st) {
+  const int ic = (int)cnt;
+  const size_t nn = (size_t)n * n;
+  auto buf = [&](int b) { return reinterpret_cast<T*>(ws + L.off_bufs + (size_t)b * L.mat_bytes * L.chunk); };
+  double* part = reinterpret_cast<double*>(ws + L.off_part);
+  double* nrm4 = reinterpret_cast<double*>(ws + L.off_norm1);
+  double* de1 = reinterpret_cast<double*>(ws + L.off_e1);
+  int* lists = reinterpret_cast<int*>(ws + L.off_list);  // [2][chunk] ping-pong, s32 [chunk], m32 [chunk]
+  int* la = lists;
+  int* lb = lists + L.chunk;
+  int* s32 = lists + 2 * L.chunk;
+  int* m32 = lists + 3 * L.chunk;
+  int* dcnt = reinterpret_cast<int*>(ws + L.off_cnt);  // [0..kA1MaxTerms] list sizes, [kA1MaxTerms+1] max s
+  if (cudaMemsetAsync(dcnt, 0, 256, st) != cudaSuccess) return EXPMB_ERR_CUDA;
+
+  GemmCtx<T> g{};
+  g.n = n;
+  g.W = W;
+  g.X = X;
+  g.mstride = (int64_t)(L.mat_bytes / sizeof(T));
+  g.wstride = (int64_t)nn;
+  g.tiles_m = L.tiles_m;
+  g.part = part;
+  g.s32 = s32;
+  g.W2 = buf(0); g.Y0 = buf(1); g.Y1 = buf(2); g.Tmp = buf(5);
+
+  dim3 cgrid((n + 255) / 256, L.tiles_m, ic);
+  k_colsum_partial<T><<<cgrid, 256, 0, st>>>(W, n, (int64_t)nn, part, L.tiles_m);
+  k_a1_init<<<ic, 256, 0, st>>>(part, L.tiles_m, n, eps, nrm4, s32, m32, de1, la, dcnt);
+  {
+    int bx = (int)std::min<size_t>((nn + 255) / 256, 64);
+    int by = std::min(ic, std::max(1, sm_count_dev() * 8 / bx));
+    k_a1_setup<T><<<dim3(bx, by), 256, 0, st>>>(g, ic);
+  }
+  // term loop (engine.py:109-112): stage j runs on the matrices still active
+  for (int j = 0; j < kA1MaxTerms; ++j) {
+    int* cur = (j & 1) ? lb : la;
+    int* nxt = (j & 1) ? la : lb;
+    g.sq_step = j;
+    if (gemm_launch<T>(g, STAGE_A1, cur, ic, st, dcnt + j)) return EXPMB_ERR_CUDA;
+    k_a1_check<<<std::min(ic, sm_count_dev() * 4), 256, 0, st>>>(part, L.tiles_m, n, eps, j, cur, dcnt + j, nxt,
+                                                                  dcnt + j + 1, m32, de1);
+  }
+  // squarings: one cooperative launch for every level
+  {
+    constexpr bool kMMA = sizeof(T) == 8;
+    constexpr bool kTwo = sizeof(T) == 4;  // the 1-CTA/SM fp32 variant (two-level accumulation)
+    auto kern = k_a1_square<T, kTwo, kMMA>;
+    constexpr int smem = simt_smem_bytes<T>();
+    static int occ = 0;
+    if (occ == 0) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return EXPMB_ERR_CUDA;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem) != cudaSuccess || occ < 1) occ = 1;
+    }
+    const int tiles = ((n + kGemmBN - 1) / kGemmBN) * L.tiles_m;
+    const int grid = (int)std::min<int64_t>((int64_t)sm_count_dev() * occ, (int64_t)ic * tiles);
+    int icv = ic;
+    const int* mp = dcnt + kA1MaxTerms + 1;
+    void* args[] = {(void*)&g, (void*)&icv, (void*)&mp};
+    if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+  }
+  // non-finite scan of X + per-matrix outputs (m = terms, s, e1 = ||last Y||_1, mults = m + s)
+  int* flags = reinterpret_cast<int*>(ws + L.off_flags);
+  if (cudaMemsetAsync(flags, 0, (size_t)ic * sizeof(int), st) != cudaSuccess) return EXPMB_ERR_CUDA;
+  int bx = (int)((nn + 256 * 8 - 1) / (256 * 8));
+  if (bx > 1024) bx = 1024;
+  k_nonfinite<T><<<dim3(bx, ic), 256, 0, st>>>(X, n, (int64_t)nn, flags);
+  k_a1_finish<<<(ic + 255) / 256, 256, 0, st>>>(ic, nrm4, s32, m32, de1, flags, base, po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
 static inline int large_expm(const void* W, void* X, int64_t batch, int n, int dtype, double eps, int scheme,
                              PlanOut po, void* workspace, cudaStream_t st) {
   const int es = dtype == 0 ? 4 : 8;
@@ -463,7 +705,13 @@ static inline int large_expm(const void* W, void* X, int64_t batch, int n, int d
     const int64_t cnt = std::min<int64_t>(L.chunk, batch - b0);
     const size_t off = (size_t)b0 * n * n;
     int rc;
-    if (dtype == 0)
+    if (scheme == 2 && dtype == 0)
+      rc = large_run_chunk_alg1<float>(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt,
+                                       n, eps, b0, po, ws, L, st);
+    else if (scheme == 2)
+      rc = large_run_chunk_alg1<double>(reinterpret_cast<const double*>(W) + off, reinterpret_cast<double*>(X) + off,
+                                        cnt, n, eps, b0, po, ws, L, st);
+    else if (dtype == 0)
       rc = large_run_chunk<float>(reinterpret_cast<const float*>(W) + off, reinterpret_cast<float*>(X) + off, cnt, n,
                                   eps, scheme, b0, po, ws, L, st);
     else

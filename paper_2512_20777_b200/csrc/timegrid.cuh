@@ -60,7 +60,7 @@ static inline TgLayout tg_layout(int64_t K, int n, int esize) {
   L.off_pow = off; off += align256((size_t)kTgPowers * n * n * sizeof(double));
   L.off_tmp = off; off += L.mat_bytes * (size_t)chunk;
   L.off_part = off; off += align256((size_t)chunk * ((n + kGemmBM - 1) / kGemmBM) * n * sizeof(double));
-  L.off_nrmA = off; off += align256(4 * sizeof(double));
+  L.off_nrmA = off; off += align256(5 * sizeof(double));  // ||P_p||_1, p = 1..4, and sigma
   L.off_nrm4 = off; off += align256((size_t)chunk * 4 * sizeof(double));
   L.off_flags = off; off += align256((size_t)chunk * sizeof(int));
   L.off_m = off; off += align256((size_t)chunk);
@@ -77,6 +77,20 @@ template <typename T>
 __global__ void k_tg_upcast(const T* __restrict__ A, double* __restrict__ P1, size_t nn) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x)
     P1[i] = (double)A[i];
+}
+
+// P1 <- A / sigma with sigma = 2^e the power of two that brings ||A||_1 into
+// [1/2, 1) (exact): the shared powers are then those of A / sigma, bounded by
+// 1 in norm, so A^16 neither overflows for large ||A|| nor underflows for
+// small; sigma^p goes into the per-time coefficients.  nrm[4] = sigma.
+__global__ void k_tg_normalize(double* __restrict__ P1, size_t nn, double* __restrict__ nrm) {
+  const double n0 = nrm[0];
+  int e = 0;
+  if (n0 > 0.0 && n0 < INFINITY) frexp(n0, &e);
+  const double inv = ldexp(1.0, -e);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x)
+    P1[i] *= inv;
+  if (blockIdx.x == 0 && threadIdx.x == 0) nrm[4] = ldexp(1.0, e);
 }
 
 // Up to 8 independent products P[c] = P[a] P[b] per launch (blockIdx.z):
@@ -155,7 +169,7 @@ __global__ void k_tg_select(const T* __restrict__ t, int64_t cnt, const double* 
                             double* __restrict__ pe1, double* __restrict__ pe2) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= cnt) return;
-  const double at = fabs((double)t[k]);
+  const double at = fabs((double)t[k]) * nrmA[4];  // |t_k| sigma: the powers are of A / sigma
   double nr[4];
   double tp = 1.0;
   for (int p = 0; p < 4; ++p) {
@@ -178,7 +192,8 @@ __global__ void k_tg_select(const T* __restrict__ t, int64_t cnt, const double* 
 constexpr int kTgChunkK = 64;
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_tg_combine(const double* __restrict__ P, int n, const T* __restrict__ t,
+__global__ void __launch_bounds__(256) k_tg_combine(const double* __restrict__ P, const double* __restrict__ nrmA,
+                                                    int n, const T* __restrict__ t,
                                                     int64_t cnt, const int8_t* __restrict__ pm,
                                                     const int8_t* __restrict__ ps, int scheme, T* X, T* Tmp,
                                                     int64_t mstride) {
@@ -189,7 +204,7 @@ __global__ void __launch_bounds__(256) k_tg_combine(const double* __restrict__ P
   for (int i = threadIdx.x; i < kc; i += blockDim.x) {
     const int64_t k = k0 + i;
     const int m = pm[k], s = ps[k];
-    const double tau = (double)t[k] * pow2_neg<double>(s);
+    const double tau = (double)t[k] * pow2_neg<double>(s) * nrmA[4];  // t 2^-s sigma (powers of A / sigma)
     const int deg = (scheme == 0 && m == 15) ? 16 : m;
     double tp = 1.0;
     gam[i][0] = 1.0;
@@ -228,6 +243,8 @@ static int tg_run(const T* A, const T* t, T* X, int64_t K, int n, double eps, in
   double* nrmA = reinterpret_cast<double*>(ws + L.off_nrmA);
   // shared powers A^1..A^16 in binary64 and their norms
   k_tg_upcast<T><<<256, 256, 0, st>>>(A, P, nn);
+  k_tg_norms<<<1, 256, 0, st>>>(P, n, nrmA);          // ||A||_1
+  k_tg_normalize<<<256, 256, 0, st>>>(P, nn, nrmA);   // P1 = A / sigma, nrmA[4] = sigma
   // level L forms A^(h+1) .. A^(2h) as A^h A^(i) (h = 1, 2, 4, 8); index = power - 1
   for (int h = 1; h < kTgPowers; h *= 2) {
     TgProducts pr{};
@@ -255,7 +272,7 @@ static int tg_run(const T* A, const T* t, T* X, int64_t K, int n, double eps, in
     const int64_t mstride = (int64_t)(L.mat_bytes / sizeof(T));
     k_tg_select<T><<<(ic + 127) / 128, 128, 0, st>>>(t + base, cnt, nrmA, eps, scheme, nrm4, dm, ds, de1, de2);
     k_tg_combine<T><<<dim3((unsigned)((nn + 255) / 256), (unsigned)((cnt + kTgChunkK - 1) / kTgChunkK)), 256, 0, st>>>(
-        P, n, t + base, cnt, dm, ds, scheme, Xc, Tmp, mstride);
+        P, nrmA, n, t + base, cnt, dm, ds, scheme, Xc, Tmp, mstride);
     // squarings: the device bucket scheduler sorts the chunk by s descending;
     // level q runs on the prefix #(s > q), a count that stays on the device
     int* dcnt = reinterpret_cast<int*>(ws + L.off_cnt);

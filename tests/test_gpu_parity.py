@@ -348,6 +348,46 @@ def test_baseline_alg1_vs_oracle(dtype):
             _check_batch(W, eps, "baseline", dtype, f"baseline n={n}")
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_baseline_alg1_large_n_vs_oracle(dtype):
+    """Alg. 1 for n > 64 on the GEMM pipeline (term stages over device active
+    lists, cooperative squaring): same (m, s, mults) as the oracle (pinned to
+    engine.py:90-116), values within the bar, including s well above 8."""
+    rng = np.random.default_rng(91)
+    for n in (65, 100, 256):
+        B = 4 if n < 256 else 3
+        W = rng.uniform(-1, 1, (B, n, n))
+        # fp32: norms up to ~16 (s <= 6), as the n <= 64 test -- every squaring doubles the fp32 error
+        top = 2.7 if dtype == torch.float64 else 1.2
+        W *= (10.0 ** rng.uniform(-3, top, B) / np.abs(W).sum(axis=1).max(axis=1))[:, None, None]
+        if dtype == torch.float32:
+            W = W.astype(np.float32)
+        for eps in ((1e-12, 2.0 ** -53) if dtype == torch.float64 else (2.0 ** -24,)):
+            _check_batch(W, eps, "baseline", dtype, f"baseline n={n}")
+    # a batch mixing the fused-kernel size limit's neighbour orders
+    Wz = np.zeros((2, 96, 96))
+    Wz[1] = np.diag(np.full(96, -30.0))  # s = 7, e^W = e^-30 I
+    if dtype == torch.float32:
+        Wz = Wz.astype(np.float32)
+    _check_batch(Wz, 1e-12 if dtype == torch.float64 else 2.0 ** -24, "baseline", dtype, "baseline diag")
+
+
+def test_baseline_alg1_large_n_graph_capture():
+    """The n > 64 Alg. 1 path is sync-free too: it captures into a CUDA graph."""
+    W = (torch.randn(3, 128, 128, device="cuda", dtype=torch.float64) / 12)
+    X0 = torch.empty_like(W)
+    X.expm_into(W, X0, 1e-12, "baseline")
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.expm_into(W, X0, 1e-12, "baseline")
+    W.mul_(7.0)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = X.expm_baseline(W.clone(), 1e-12)
+    assert torch.equal(X0, ref.value)
+
+
 def test_baseline_cost_ratio_vs_sastre():
     """The paper's claim on the reference's own bands: Alg. 1 needs
     1.6-2.4x the products of the Sastre route on flow-norm matrices."""

@@ -92,3 +92,15 @@ def test_timegrid_negative_times_ps_fp32():
     A = (rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32)
     t = np.array([-3.0, -1.25, -0.01, 0.5, 2.75], np.float32)
     _check(A, t, 2.0 ** -24, "ps", torch.float32, 1e-5)
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 80, 2.0 ** -70])
+def test_timegrid_extreme_norm_of_A(scale):
+    """The shared powers are formed from A / sigma (sigma a power of two near
+    ||A||_1), so ||A|| far from 1 neither overflows A^16 nor underflows it:
+    e^(t_k A) for t_k ||A|| of order one matches the oracle on fl(t_k A)."""
+    rng = np.random.default_rng(23)
+    n = 80
+    A = rng.standard_normal((n, n)) / np.sqrt(n) * scale
+    t = np.array([0.3, 1.0, 2.5, -1.7]) / scale
+    _check(A, t, 1e-12, "sastre", torch.float64, 1e-12)

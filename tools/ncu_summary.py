@@ -49,7 +49,7 @@ def raw(rep):
 def main():
     rep, ksub, outp = sys.argv[1:4]
     note = sys.argv[4] if len(sys.argv) > 4 else ""
-    units = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
+    n_units = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
     hdr, units, vals = raw(rep)
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
@@ -57,8 +57,8 @@ def main():
     for k in KEYS:
         if k in d:
             lines.append(f"{k:70s} {d[k]:>16s} {u.get(k, '')}")
-    if units > 0 and "smsp__inst_executed.sum" in d:
-        lines.append(f"{'warp instructions per unit':70s} {float(d['smsp__inst_executed.sum'].replace(',', '')) / units:16.1f}")
+    if n_units > 0 and "smsp__inst_executed.sum" in d:
+        lines.append(f"{'warp instructions per unit':70s} {float(d['smsp__inst_executed.sum'].replace(',', '')) / n_units:16.1f}")
     stalls = [(k, d[k]) for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
     stalls = sorted(stalls, key=lambda kv: -float(kv[1].replace(",", "") or 0))
     tot = sum(float(v.replace(",", "") or 0) for _, v in stalls) or 1

@@ -140,19 +140,23 @@ int expmb_expm_pipelined(const void* W_host, void* X_host, void* W_dev, void* X_
  *   A1         [batch,n,t] device, row-major     (LowRankPair.a1)
  *   A2         [batch,t,n] device, row-major     (LowRankPair.a2)
  *   X          [batch,n,n] output e^(A1 A2)
- *   1 <= t <= n (MatrixError otherwise); t <= 32 (EXPMB_ERR_UNSUPPORTED)
+ *   1 <= t <= n (MatrixError otherwise)
  *   m, e1, e2  [batch] plan (EvalPlan.m/.e1/.e2; s is always 0)
  *   norms      [batch,2] ||V||_1, ||V^2||_1 (NaN if V^2 never formed)
  *   mults      [batch] t x t products (ExpmResult.mults; rect_mults is 3)
  *   flags      [batch] EXPMB_LR_* bits; a flagged matrix's X is NaN
- * Any of m..flags may be NULL.  No workspace, no host synchronisation.
+ *   workspace  expmb_lowrank_workspace_bytes(batch, n, t, dtype) bytes: 0
+ *              (NULL allowed) for t <= 32, where every t x t operand lives
+ *              in shared memory; for t > 32 the t x t operands live here
+ * Any of m..flags may be NULL.  No host synchronisation.
  */
 #define EXPMB_LR_BAD_INPUT 1 /* non-finite factor entry: MatrixError (engine.py:179-180)  */
 #define EXPMB_LR_NONFINITE 2 /* V, a power, psi or e^W not finite: NonFiniteError        */
 #define EXPMB_LR_NO_ORDER 4  /* no admissible order: LowRankOrderError (engine.py:236-240) */
+size_t expmb_lowrank_workspace_bytes(int64_t batch, int32_t n, int32_t t, int dtype);
 int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, int32_t n, int32_t t,
                        int dtype, double eps, int8_t* m, double* e1, double* e2, double* norms,
-                       int32_t* mults, uint8_t* flags, void* stream);
+                       int32_t* mults, uint8_t* flags, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Host evaluation of the low-rank ladder the kernel runs (engine.py:224-244):

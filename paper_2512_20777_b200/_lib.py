@@ -34,6 +34,7 @@ EXPORTS = (
     "expmb_expm",
     "expmb_select",
     "expmb_select_host",
+    "expmb_lowrank_workspace_bytes",
     "expmb_expm_lowrank",
     "expmb_select_lowrank_host",
     "expmb_timegrid_workspace_bytes",
@@ -86,10 +87,12 @@ def lib() -> ctypes.CDLL:
         c.POINTER(c.c_double), c.c_double, c.c_int,
         c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
     ]
+    L.expmb_lowrank_workspace_bytes.restype = c.c_size_t
+    L.expmb_lowrank_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32, c.c_int]
     L.expmb_expm_lowrank.restype = c.c_int
     L.expmb_expm_lowrank.argtypes = [
         c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_int, c.c_double,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p,
     ]
     L.expmb_select_lowrank_host.restype = c.c_int
     L.expmb_select_lowrank_host.argtypes = [

@@ -442,10 +442,13 @@ def _expm_lowrank_op(A1: torch.Tensor, A2: torch.Tensor, eps: float) -> tuple[
     flags = torch.empty(B, dtype=torch.uint8, device=dev)
     L = _lib.lib()
     dt = _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64
+    wsb = int(L.expmb_lowrank_workspace_bytes(B, n, t, dt))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     with torch.cuda.device(dev):
         rc = L.expmb_expm_lowrank(A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t, dt, float(eps),
                                   m.data_ptr(), e1.data_ptr(), e2.data_ptr(), norms.data_ptr(), mults.data_ptr(),
-                                  flags.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+                                  flags.data_ptr(), None if ws is None else ws.data_ptr(), wsb,
+                                  torch.cuda.current_stream(dev).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
     return X, m, e1, e2, norms, mults, flags
@@ -468,7 +471,9 @@ def expm_lowrank(pair: LowRankPair, eps: float) -> ExpmResult:
     Raises, after the batch completes: MatrixError when a factor holds
     NaN/Inf (engine.py:179-180), LowRankOrderError when no order qualifies
     (engine.py:236-240), NonFiniteError when V, psi or the result is not
-    finite (matrix.py:95-102).  t <= 32."""
+    finite (matrix.py:95-102).  Any 1 <= t <= n: t <= 32 runs one CTA per
+    matrix with every t x t operand in shared memory; larger inner ranks keep
+    the t x t operands in a device workspace (lowrank_large.cuh)."""
     t0 = time.perf_counter()
     if not isinstance(pair, LowRankPair):
         pair = LowRankPair(*pair)
@@ -498,11 +503,13 @@ def expm_lowrank(pair: LowRankPair, eps: float) -> ExpmResult:
 
 
 def expm_lowrank_into(A1: torch.Tensor, A2: torch.Tensor, X: torch.Tensor, eps: float,
-                      plan: dict | None = None) -> None:
+                      plan: dict | None = None, workspace: torch.Tensor | None = None) -> None:
     """Allocation-free, synchronisation-free ``expm_lowrank`` for steady-state
     loops and CUDA graphs: A1 [B,n,t], A2 [B,t,n], X [B,n,n] contiguous CUDA
     tensors; plan tensors (keys m, e1, e2, norms, mults, flags) are optional.
-    Errors are left in plan["flags"] (EXPMB_LR_* bits) instead of raised."""
+    Errors are left in plan["flags"] (EXPMB_LR_* bits) instead of raised.  For
+    t > 32 a preallocated ``workspace`` (expmb_lowrank_workspace_bytes) keeps the
+    call allocation-free."""
     LowRankPair(A1, A2)
     B, n, t = A1.shape
     if X.shape != (B, n, n) or X.dtype != A1.dtype or not (A1.is_contiguous() and A2.is_contiguous()
@@ -516,12 +523,19 @@ def expm_lowrank_into(A1: torch.Tensor, A2: torch.Tensor, X: torch.Tensor, eps: 
     def p(k):
         v = plan.get(k)
         return None if v is None else v.data_ptr()
+    L = _lib.lib()
+    dt = _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64
+    wsb = int(L.expmb_lowrank_workspace_bytes(B, n, t, dt))
+    if wsb and (workspace is None or not isinstance(workspace, torch.Tensor) or workspace.dtype != torch.uint8
+                or workspace.device != A1.device or workspace.numel() < wsb or not workspace.is_contiguous()):
+        if workspace is not None:
+            raise MatrixError(f"workspace must be a contiguous uint8 tensor of >= {wsb} bytes on {A1.device}")
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=A1.device)
     with torch.cuda.device(A1.device):
-        rc = _lib.lib().expmb_expm_lowrank(
-            A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t,
-            _lib.EXPMB_F32 if A1.dtype == torch.float32 else _lib.EXPMB_F64, float(eps),
+        rc = L.expmb_expm_lowrank(
+            A1.data_ptr(), A2.data_ptr(), X.data_ptr(), B, n, t, dt, float(eps),
             p("m"), p("e1"), p("e2"), p("norms"), p("mults"), p("flags"),
-            torch.cuda.current_stream(A1.device).cuda_stream)
+            workspace.data_ptr() if wsb else None, wsb, torch.cuda.current_stream(A1.device).cuda_stream)
     if rc != 0:
         _raise_rc(rc)
 

@@ -14,7 +14,9 @@
 #include "fused_small.cuh"
 #include "fused_dmma.cuh"
 #include "large.cuh"
+#include "fused_tile.cuh"
 #include "lowrank.cuh"
+#include "lowrank_large.cuh"
 #include "timegrid.cuh"
 
 namespace expmb {
@@ -253,17 +255,27 @@ const char* expmb_strerror(int code) {
     case EXPMB_ERR_CUDA: return "CUDA launch or copy failed";
     case EXPMB_ERR_ALIGN: return "W and X must be 16-byte aligned";
     case EXPMB_ERR_UNSUPPORTED:
-      return "combination not supported (baseline scheme needs n <= 64; low-rank path needs t <= 32)";
+      return "combination not supported";
     default: return "unknown error";
   }
 }
 
 double expmb_unit_roundoff(int dtype) { return dtype == EXPMB_F32 ? 0x1p-24 : 0x1p-53; }
 
+// 64 < n <= EXPMB_FUSED_TILE_MAX (default 128): one CTA per matrix
+// (fused_tile.cuh); EXPMB_FUSED_TILE=0 sends those orders to the pipeline
+static bool use_fused_tile(int n, int scheme) {
+  static const bool off = getenv("EXPMB_FUSED_TILE") && getenv("EXPMB_FUSED_TILE")[0] == '0';
+  static const int nmax = getenv("EXPMB_FUSED_TILE_MAX") ? atoi(getenv("EXPMB_FUSED_TILE_MAX")) : 128;
+  return !off && n > 64 && n <= nmax && (scheme == EXPMB_SASTRE || scheme == EXPMB_PS);
+}
+
 size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme) {
   if (batch <= 0) return 0;
   if (n <= 64) return 256;  // work counter of the persistent fused kernel
-  return large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
+  const int es = dtype == EXPMB_F32 ? 4 : 8;
+  if (use_fused_tile(n, scheme)) return ft_workspace_bytes(batch, n, es, scheme, ft_ctas(es));
+  return large_workspace_bytes(batch, n, es, scheme);
 }
 
 int expmb_select_host(const double* norms, double eps, int scheme, int* m, int* s, double* e1, double* e2) {
@@ -322,6 +334,13 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
            : scheme == EXPMB_PS   ? dispatch_small<double, 1>(w, x, batch, n, eps, po, ctr, st)
                                   : dispatch_small<double, 2>(w, x, batch, n, eps, po, ctr, st);
   }
+  if (use_fused_tile(n, scheme)) {
+    if (workspace == nullptr || workspace_bytes < expmb_workspace_bytes(batch, n, dtype, scheme))
+      return EXPMB_ERR_WORKSPACE;
+    unsigned char* ws = (unsigned char*)workspace;
+    return dtype == EXPMB_F32 ? ft_run<float>((const float*)W, (float*)X, batch, n, eps, scheme, po, ws, st)
+                              : ft_run<double>((const double*)W, (double*)X, batch, n, eps, scheme, po, ws, st);
+  }
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
   return large_expm(W, X, batch, n, dtype, eps, scheme, po, workspace, st);
@@ -357,6 +376,13 @@ int expmb_select(const void* W, int64_t batch, int32_t n, int dtype, double eps,
                                     : launch_fused<double, 32, 4, 4, 1>(w, nullptr, batch, n, eps, po, ctr, st);
     return scheme == 0 ? launch_fused<double, 64, 4, 1, 0>(w, nullptr, batch, n, eps, po, ctr, st)
                        : launch_fused<double, 64, 4, 1, 1>(w, nullptr, batch, n, eps, po, ctr, st);
+  }
+  if (use_fused_tile(n, scheme)) {
+    if (workspace == nullptr || workspace_bytes < expmb_workspace_bytes(batch, n, dtype, scheme))
+      return EXPMB_ERR_WORKSPACE;
+    unsigned char* ws = (unsigned char*)workspace;
+    return dtype == EXPMB_F32 ? ft_run<float>((const float*)W, nullptr, batch, n, eps, scheme, po, ws, st)
+                              : ft_run<double>((const double*)W, nullptr, batch, n, eps, scheme, po, ws, st);
   }
   const size_t need = large_workspace_bytes(batch, n, dtype == EXPMB_F32 ? 4 : 8, scheme);
   if (workspace == nullptr || workspace_bytes < need) return EXPMB_ERR_WORKSPACE;
@@ -433,16 +459,29 @@ int expmb_select_lowrank_host(const double* norms, int have_v2, double eps, int*
   return rc;
 }
 
+size_t expmb_lowrank_workspace_bytes(int64_t batch, int32_t n, int32_t t, int dtype) {
+  (void)dtype;
+  if (batch <= 0 || n < 1 || t <= 32 || t > n) return 0;  // t <= 32: shared memory only
+  return lrl_layout(batch, n, t).total;
+}
+
 int expmb_expm_lowrank(const void* A1, const void* A2, void* X, int64_t batch, int32_t n, int32_t t, int dtype,
                        double eps, int8_t* m, double* e1, double* e2, double* norms, int32_t* mults, uint8_t* flags,
-                       void* stream) {
+                       void* workspace, size_t workspace_bytes, void* stream) {
   if (dtype != EXPMB_F32 && dtype != EXPMB_F64) return EXPMB_ERR_DTYPE;
   if (n < 1 || t < 1 || t > n || batch < 0) return EXPMB_ERR_SHAPE;
   if (isnan(eps) || eps < expmb_unit_roundoff(dtype)) return EXPMB_ERR_TOLERANCE;
-  if (t > 32) return EXPMB_ERR_UNSUPPORTED;
   if (batch == 0) return EXPMB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   LrOut po{m, e1, e2, norms, mults, flags};
+  if (t > 32) {  // t x t operands in the global workspace (lowrank_large.cuh)
+    const LrlLayout L = lrl_layout(batch, n, t);
+    if (workspace == nullptr || workspace_bytes < L.total) return EXPMB_ERR_WORKSPACE;
+    unsigned char* ws = (unsigned char*)workspace;
+    if (dtype == EXPMB_F32)
+      return lrl_run<float>((const float*)A1, (const float*)A2, (float*)X, batch, n, t, eps, po, ws, L, st);
+    return lrl_run<double>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, ws, L, st);
+  }
   if (dtype == EXPMB_F32)
     return dispatch_lowrank<float>((const float*)A1, (const float*)A2, (float*)X, batch, n, t, eps, po, st);
   return dispatch_lowrank<double>((const double*)A1, (const double*)A2, (double*)X, batch, n, t, eps, po, st);

@@ -125,11 +125,22 @@ constexpr int kExpBias = 200;
 __device__ __forceinline__ unsigned long long exp_pack(float a) {
   return a > 0.f && a < INFINITY ? ((unsigned long long)(ilogbf(a) + kExpBias) << 20) | 1ull : 0ull;
 }
-__device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, int stage, const int* __restrict__ list,
-                                              const Bufs& b, int slot, int bx, int by) {
-  const int z = list ? list[slot] : slot;
+// The operands of a slot's product (make_epi once per slot, not per tile).
+struct I8Ops {
+  const float* L;
+  const float* R;
+};
+__device__ __forceinline__ bool i8_slot_ops(const GemmCtx<float>& g, int stage, const int* __restrict__ list,
+                                            int slot, I8Ops& ops) {
   Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;
+  if (!make_epi(g, stage, list ? list[slot] : slot, e)) return false;
+  ops.L = e.L;
+  ops.R = e.R;
+  return true;
+}
+
+__device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, const I8Ops& e, const Bufs& b, int slot, int bx,
+                                              int by) {
   __shared__ int cmax[32][33];
   __shared__ unsigned long long csum[32][33];
   const int n = g.n;  // a multiple of 16 on this path: groups of 4 columns are all in or all out
@@ -184,10 +195,22 @@ __global__ void __launch_bounds__(256, 8) k_i8_stats(GemmCtx<float> g, int stage
   const int cnt = dcount ? *dcount : hcount;
   const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
   const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+  // a contiguous run of units per CTA: the slot's operands are looked up once
+  // per slot, not per 32x32 tile
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int w1 = min(total, (int)blockIdx.x * per + per);
+  int cur = -1;
+  bool valid = false;
+  I8Ops ops{};
+  for (int w = blockIdx.x * per; w < w1; ++w) {
     const int slot = w / tiles, t = w - slot * tiles;
+    if (slot != cur) {
+      cur = slot;
+      valid = i8_slot_ops(g, stage, list, slot, ops);
+    }
+    if (!valid) continue;
     __syncthreads();  // shared tiles of the previous unit
-    i8_stats_tile(g, stage, list, b, slot, t % t32, t / t32);
+    i8_stats_tile(g, ops, b, slot, t % t32, t / t32);
   }
 }
 
@@ -238,12 +261,8 @@ __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, c
 }
 
 // One pass over 32x32 tiles: L slices row-major, R slices transposed (both K-major).
-__device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, int stage, const int* __restrict__ list,
-                                              const Bufs& b, int slot, int bx, int by) {
-  if (!b.ok[slot]) return;
-  const int z = list ? list[slot] : slot;
-  Epi<float> e;
-  if (!make_epi(g, stage, z, e)) return;
+__device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, const I8Ops& e, const Bufs& b, int slot, int bx,
+                                              int by) {
   __shared__ float tile[32][33];
   const int n = g.n;  // a multiple of 16 on this path
   const int r0 = by * 32, c0 = bx * 32;
@@ -299,10 +318,20 @@ __global__ void __launch_bounds__(256, 8) k_i8_slice(GemmCtx<float> g, int stage
   const int cnt = dcount ? *dcount : hcount;
   const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
   const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+  const int per = (total + gridDim.x - 1) / gridDim.x;  // contiguous units per CTA (see k_i8_stats)
+  const int w1 = min(total, (int)blockIdx.x * per + per);
+  int cur = -1;
+  bool valid = false;
+  I8Ops ops{};
+  for (int w = blockIdx.x * per; w < w1; ++w) {
     const int slot = w / tiles, t = w - slot * tiles;
+    if (slot != cur) {
+      cur = slot;
+      valid = b.ok[slot] && i8_slot_ops(g, stage, list, slot, ops);
+    }
+    if (!valid) continue;
     __syncthreads();  // the transpose tile of the previous unit
-    i8_slice_tile(g, stage, list, b, slot, t % t32, t / t32);
+    i8_slice_tile(g, ops, b, slot, t % t32, t / t32);
   }
 }
 

@@ -616,12 +616,9 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
 // ---------------------------------------------------------------------------
 // elementwise stage (before the first evaluation product)
 // ---------------------------------------------------------------------------
+// The elementwise first step for matrix z, elements i0, i0 + stride, ...
 template <typename T>
-__global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __restrict__ list,
-                                                   const int* __restrict__ dcount, int hcount) {
-  const int cnt = dcount ? *dcount : hcount;
-  for (int slot = blockIdx.y; slot < cnt; slot += gridDim.y) {
-  const int z = list[slot];
+__device__ __forceinline__ void elem_one(const GemmCtx<T>& g, int z, size_t i0, size_t stride) {
   const int m = g.m[z], s = g.s[z];
   const int n = g.n;
   const size_t nn = (size_t)n * n;
@@ -629,7 +626,7 @@ __global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __re
   const T* Wz = g.W + (int64_t)z * g.wstride;
   const T* A2 = g.W2 + o;
   const double sg = pow2_neg<double>(s), sg2 = pow2_neg<double>(2 * s);
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x) {
+  for (size_t i = i0; i < nn; i += stride) {
     const int r = (int)(i / n), c = (int)(i % n);
     const T dg = (r == c) ? T(1) : T(0);
     if (g.scheme == 1) {
@@ -656,7 +653,13 @@ __global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __re
       g.Ra[o + i] = (T)(cc[0] * sg2) * A2[i] + (T)(cc[1] * sg) * Wz[i];
     }
   }
-  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) elem_kernel(GemmCtx<T> g, const int* __restrict__ list,
+                                                   const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  for (int slot = blockIdx.y; slot < cnt; slot += gridDim.y)
+    elem_one(g, list[slot], (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
 }
 
 template <typename T>

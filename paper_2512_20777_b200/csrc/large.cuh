@@ -119,13 +119,12 @@ static inline size_t large_workspace_bytes(int64_t batch, int n, int esize, int 
 // small kernels
 // ---------------------------------------------------------------------------
 
-// Reduce the per-tile column partials of W^p and walk the ladder again.
-__global__ void __launch_bounds__(256) k_select(const double* __restrict__ part, int tiles_m, int n, int have,
-                                                double eps, int scheme, double* __restrict__ nrm4,
-                                                int* __restrict__ need, int8_t* __restrict__ pm,
-                                                int8_t* __restrict__ ps, double* __restrict__ pe1,
-                                                double* __restrict__ pe2) {
-  const int z = blockIdx.x;
+// Reduce the per-tile column partials of W^p and walk the ladder again
+// (select.py:164-220) for matrix z; the whole CTA takes part.
+__device__ __forceinline__ void select_block(const double* __restrict__ part, int tiles_m, int n, int have,
+                                             double eps, int scheme, double* __restrict__ nrm4, int* __restrict__ need,
+                                             int8_t* __restrict__ pm, int8_t* __restrict__ ps,
+                                             double* __restrict__ pe1, double* __restrict__ pe2, int z) {
   if (have > 1 && need[z] != have) return;  // this matrix did not form W^have
   __shared__ double red[256];
   const double* pz = part + (size_t)z * tiles_m * n;
@@ -157,6 +156,13 @@ __global__ void __launch_bounds__(256) k_select(const double* __restrict__ part,
     }
   }
 }
+__global__ void __launch_bounds__(256) k_select(const double* __restrict__ part, int tiles_m, int n, int have,
+                                                double eps, int scheme, double* __restrict__ nrm4,
+                                                int* __restrict__ need, int8_t* __restrict__ pm,
+                                                int8_t* __restrict__ ps, double* __restrict__ pe1,
+                                                double* __restrict__ pe2) {
+  select_block(part, tiles_m, n, have, eps, scheme, nrm4, need, pm, ps, pe1, pe2, blockIdx.x);
+}
 
 // Column abs-sum partials of W over 128-row slabs: grid (col blocks, slabs,
 // matrices), one thread per column, coalesced row reads (select.py:169).
@@ -186,29 +192,30 @@ __global__ void __launch_bounds__(256) k_nonfinite(const T* __restrict__ X, int 
   if (bad && threadIdx.x == 0) atomicOr(flags + z, 1);
 }
 
-// Per-matrix outputs + non-finite scan of the final X (and of W).
 // Per-matrix outputs.  A non-finite input shows in ||W||_1 (NaN / Inf
 // propagate through the abs-sums); non-finite outputs come from k_nonfinite.
+__device__ __forceinline__ void finish_one(int z, int scheme, const double* __restrict__ nrm4,
+                                           const int8_t* __restrict__ pm, const int8_t* __restrict__ ps,
+                                           const double* __restrict__ pe1, const double* __restrict__ pe2, int bad,
+                                           int64_t g, PlanOut po) {
+  const int m = pm[z], s = ps[z];
+  const double n1 = nrm4[4 * z], n2 = nrm4[4 * z + 1];
+  if (po.m) po.m[g] = (int8_t)m;
+  if (po.s) po.s[g] = (int8_t)s;
+  if (po.e1) po.e1[g] = pe1[z];
+  if (po.e2) po.e2[g] = pe2[z];
+  if (po.norms) { po.norms[2 * g] = n1; po.norms[2 * g + 1] = n2; }
+  if (po.mults) po.mults[g] = budget(m, scheme) + s;
+  const double n3 = nrm4[4 * z + 2], n4 = nrm4[4 * z + 3];
+  const bool pw_bad = scheme == 1 && ((n3 == n3 && !(n3 < INFINITY)) || (n4 == n4 && !(n4 < INFINITY)));
+  if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || pw_bad || !(n1 < INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
+}
 __global__ void __launch_bounds__(256) k_finish(int cnt, int scheme, const double* __restrict__ nrm4,
                                                 const int8_t* __restrict__ pm, const int8_t* __restrict__ ps,
                                                 const double* __restrict__ pe1, const double* __restrict__ pe2,
                                                 const int* __restrict__ flags, int64_t base, PlanOut po) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
-  if (z < cnt) {
-    const int bad = flags[z];
-    const int64_t g = base + z;
-    const int m = pm[z], s = ps[z];
-    const double n1 = nrm4[4 * z], n2 = nrm4[4 * z + 1];
-    if (po.m) po.m[g] = (int8_t)m;
-    if (po.s) po.s[g] = (int8_t)s;
-    if (po.e1) po.e1[g] = pe1[z];
-    if (po.e2) po.e2[g] = pe2[z];
-    if (po.norms) { po.norms[2 * g] = n1; po.norms[2 * g + 1] = n2; }
-    if (po.mults) po.mults[g] = budget(m, scheme) + s;
-    const double n3 = nrm4[4 * z + 2], n4 = nrm4[4 * z + 3];
-    const bool pw_bad = scheme == 1 && ((n3 == n3 && !(n3 < INFINITY)) || (n4 == n4 && !(n4 < INFINITY)));
-    if (po.nonfinite) po.nonfinite[g] = (uint8_t)(bad || pw_bad || !(n1 < INFINITY) || (n2 == n2 && !(n2 < INFINITY)));
-  }
+  if (z < cnt) finish_one(z, scheme, nrm4, pm, ps, pe1, pe2, flags[z], base + z, po);
 }
 
 // Device (m, s) bucket scheduler (the keys are the reference's plan,

@@ -168,8 +168,11 @@ def test_lowrank_errors():
     bad = np.ones((4, 2)); bad[1, 1] = np.nan
     with pytest.raises(X.MatrixError):
         _run(bad, np.ones((2, 4)), 1e-8)                          # engine.py:179-180
+    with pytest.raises(X.LowRankOrderError):
+        _run(np.ones((40, 33)), np.ones((33, 40)), 1e-8)          # t > 32 path: ||V||_1 = 1320 has no order
+    bad = np.ones((40, 33)) * 0.01; bad[3, 7] = np.inf
     with pytest.raises(X.MatrixError):
-        _run(np.ones((40, 33)), np.ones((33, 40)), 1e-8)          # t > 32: unsupported here
+        _run(bad, np.ones((33, 40)) * 0.01, 1e-8)                 # t > 32 path: non-finite factor
     with pytest.raises(X.ToleranceError):
         _run(np.ones((4, 2)), np.ones((2, 4)), 2.0 ** -54)
     # one bad matrix in a batch raises for the batch; the good ones are computed
@@ -254,3 +257,50 @@ def test_lowrank_leading_batch_dims():
     assert r.value.shape == (2, 3, 40, 40) and r.plan.m.shape == (2, 3)
     flat = X.expm_lowrank(X.LowRankPair(a1.reshape(6, 40, 5), a2.reshape(6, 5, 40)), 1e-10)
     assert torch.equal(r.value.reshape(6, 40, 40), flat.value)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_lowrank_large_inner_rank(dtype):
+    """t > 32 (t x t operands in the device workspace, lowrank_large.cuh):
+    identical order, mults and e1 to the oracle, values within the bar, over
+    ragged (n, t) up to the reference generator's t = n/8 at n = 1024
+    (bench.py:134-142) and every ladder order."""
+    rng = np.random.default_rng(33 + (dtype == torch.float32))
+    for (n, t, B, lo, hi) in ((33, 33, 3, 1e-3, 3.0), (64, 40, 4, 1e-6, 4.0), (100, 64, 3, 1e-2, 5.0),
+                              (200, 128, 2, 0.3, 5.0), (1024, 128, 2, 0.5, 3.0)):
+        A1, A2 = _gen(rng, B, n, t, lo, hi)
+        if dtype == torch.float32:
+            A1, A2 = A1.astype(np.float32), A2.astype(np.float32)
+        eps = 1e-12 if dtype == torch.float64 else 2.0 ** -24
+        r = _run(A1, A2, eps, dtype)
+        got = r.value.double().cpu().numpy()
+        for b in range(B):
+            want = O.expm_lowrank(np.asarray(A1[b], np.float64), np.asarray(A2[b], np.float64), eps,
+                                  tol_floor=2.0 ** -24 if dtype == torch.float32 else 2.0 ** -53)
+            if int(r.plan.m[b]) != want.m:
+                assert O.lowrank_near_threshold(want.norm1, want.norm2, eps), (n, t, b)
+                continue
+            assert int(r.mults[b]) == want.mults, (n, t, b)
+            err = float(_rel1(got[b], want.value))
+            assert err <= _tol(A1[b], A2[b], want.m, want.value, dtype), (n, t, b, err, want.m)
+
+
+def test_lowrank_large_inner_rank_graph_capture():
+    """The t > 32 path is sync-free: expm_lowrank_into with a workspace captures into a CUDA graph."""
+    rng = np.random.default_rng(5)
+    A1, A2 = _gen(rng, 3, 96, 48, 0.5, 2.0)
+    a1 = torch.as_tensor(A1, device="cuda")
+    a2 = torch.as_tensor(A2, device="cuda")
+    xo = torch.empty(3, 96, 96, dtype=torch.float64, device="cuda")
+    wsb = int(X._lib.lib().expmb_lowrank_workspace_bytes(3, 96, 48, 1))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    X.expm_lowrank_into(a1, a2, xo, 1e-12, workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.expm_lowrank_into(a1, a2, xo, 1e-12, workspace=ws)
+    a2.mul_(1.7)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = X.expm_lowrank(X.LowRankPair(a1.clone(), a2.clone()), 1e-12)
+    assert torch.equal(xo, ref.value)

@@ -17,7 +17,7 @@ def test_lowrank_argument_errors_are_synchronous():
     L = _lib.lib()
 
     def call(b=1, n=8, t=2, dt=1, eps=1e-8):
-        return L.expmb_expm_lowrank(None, None, None, b, n, t, dt, eps, *([None] * 6), None)
+        return L.expmb_expm_lowrank(None, None, None, b, n, t, dt, eps, *([None] * 6), None, 0, None)
     assert call(eps=2.0 ** -54) == _lib.ERR_TOLERANCE
     assert call(dt=0, eps=2.0 ** -25) == _lib.ERR_TOLERANCE
     assert call(eps=float("nan")) == _lib.ERR_TOLERANCE
@@ -25,7 +25,9 @@ def test_lowrank_argument_errors_are_synchronous():
     assert call(t=9) == _lib.ERR_SHAPE          # t > n
     assert call(t=0) == _lib.ERR_SHAPE
     assert call(n=0, t=0) == _lib.ERR_SHAPE
-    assert call(n=64, t=33) == _lib.ERR_UNSUPPORTED
+    assert call(n=64, t=33) == _lib.ERR_WORKSPACE   # t > 32 keeps its t x t operands in a workspace
+    assert L.expmb_lowrank_workspace_bytes(4, 64, 32, 1) == 0
+    assert L.expmb_lowrank_workspace_bytes(4, 64, 33, 1) > 4 * 9 * 33 * 33 * 8
     assert call(b=0) == 0
 
 

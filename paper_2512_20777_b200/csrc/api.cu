@@ -262,19 +262,22 @@ const char* expmb_strerror(int code) {
 
 double expmb_unit_roundoff(int dtype) { return dtype == EXPMB_F32 ? 0x1p-24 : 0x1p-53; }
 
-// 64 < n <= EXPMB_FUSED_TILE_MAX (default 128): one CTA per matrix
-// (fused_tile.cuh); EXPMB_FUSED_TILE=0 sends those orders to the pipeline
-static bool use_fused_tile(int n, int scheme) {
-  static const bool off = getenv("EXPMB_FUSED_TILE") && getenv("EXPMB_FUSED_TILE")[0] == '0';
+// fp64, 64 < n <= EXPMB_FUSED_TILE_MAX (default 128): one CTA per matrix
+// (fused_tile.cuh; measured 1.14-1.26x the pipeline).  EXPMB_FUSED_TILE=0
+// sends those orders to the pipeline, =1 also routes fp32 there (0.85x: A/B only).
+static bool use_fused_tile(int n, int scheme, int dtype) {
+  const char* e = getenv("EXPMB_FUSED_TILE");
+  static const int mode = e ? (e[0] == '0' ? 0 : 2) : 1;
   static const int nmax = getenv("EXPMB_FUSED_TILE_MAX") ? atoi(getenv("EXPMB_FUSED_TILE_MAX")) : 128;
-  return !off && n > 64 && n <= nmax && (scheme == EXPMB_SASTRE || scheme == EXPMB_PS);
+  if (mode == 0 || (mode == 1 && dtype != EXPMB_F64)) return false;
+  return n > 64 && n <= nmax && (scheme == EXPMB_SASTRE || scheme == EXPMB_PS);
 }
 
 size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme) {
   if (batch <= 0) return 0;
   if (n <= 64) return 256;  // work counter of the persistent fused kernel
   const int es = dtype == EXPMB_F32 ? 4 : 8;
-  if (use_fused_tile(n, scheme)) return ft_workspace_bytes(batch, n, es, scheme, ft_ctas(es));
+  if (use_fused_tile(n, scheme, dtype)) return ft_workspace_bytes(batch, n, es, scheme, ft_ctas(es));
   return large_workspace_bytes(batch, n, es, scheme);
 }
 
@@ -334,7 +337,7 @@ int expmb_expm(const void* W, void* X, int64_t batch, int32_t n, int dtype, doub
            : scheme == EXPMB_PS   ? dispatch_small<double, 1>(w, x, batch, n, eps, po, ctr, st)
                                   : dispatch_small<double, 2>(w, x, batch, n, eps, po, ctr, st);
   }
-  if (use_fused_tile(n, scheme)) {
+  if (use_fused_tile(n, scheme, dtype)) {
     if (workspace == nullptr || workspace_bytes < expmb_workspace_bytes(batch, n, dtype, scheme))
       return EXPMB_ERR_WORKSPACE;
     unsigned char* ws = (unsigned char*)workspace;
@@ -377,7 +380,7 @@ int expmb_select(const void* W, int64_t batch, int32_t n, int dtype, double eps,
     return scheme == 0 ? launch_fused<double, 64, 4, 1, 0>(w, nullptr, batch, n, eps, po, ctr, st)
                        : launch_fused<double, 64, 4, 1, 1>(w, nullptr, batch, n, eps, po, ctr, st);
   }
-  if (use_fused_tile(n, scheme)) {
+  if (use_fused_tile(n, scheme, dtype)) {
     if (workspace == nullptr || workspace_bytes < expmb_workspace_bytes(batch, n, dtype, scheme))
       return EXPMB_ERR_WORKSPACE;
     unsigned char* ws = (unsigned char*)workspace;

@@ -1,4 +1,4 @@
-// fused_tile.cuh -- one CTA per matrix for 64 < n <= 128: the whole program
+// fused_tile.cuh -- one CTA per matrix for 64 < n <= 128 (fp64; fp32 opt-in): the whole program
 // of engine.py:119-152 in one persistent kernel.
 //
 // For these orders a matrix is exactly one 128 x 128 GEMM tile, so the CTA
@@ -38,8 +38,18 @@ static inline FtLayout ft_layout(int n, int esize, int scheme) {
   return L;
 }
 
-// (one CTA per SM: the per-matrix program keeps more state live than a bare
-// GEMM stage, and at the 2-CTA register cap of 128 it spilled)
+// One product tile of the per-matrix program.
+template <typename T, bool TWO, bool MMA>
+__device__ __forceinline__ void ft_tile(const GemmCtx<T>& g, int stage, int bx, int by, unsigned char* smem_raw) {
+  gemm_tile<T, TWO, MMA>(g, stage, nullptr, 0, bx, by, smem_raw);
+}
+
+// One CTA per SM (fp64 runs its products on DMMA at one CTA per SM in the
+// pipeline too).  Measured on B200 against the pipeline (tools/fused_tile_bench.py,
+// profiles/fused_tile_r02.json): fp64 1.26x at n = 96, 1.14x at n = 128; fp32
+// 0.87x / 0.85x -- the fp32 stage kernel runs two CTAs per SM at 128 registers,
+// which the per-matrix program cannot fit without spilling (1.7 KB inlined,
+// 0.4 KB with an out-of-line tile), so fp32 stays on the pipeline by default.
 template <typename T, bool TWO, bool MMA>
 __global__ void __launch_bounds__(256, 1)
 expm_tile_fused_kernel(GemmCtx<T> g0, int64_t batch, double log_eps, int scheme, PlanOut po, unsigned char* ws,
@@ -94,7 +104,7 @@ expm_tile_fused_kernel(GemmCtx<T> g0, int64_t batch, double log_eps, int scheme,
       const int stage = p == 2 ? STAGE_W2 : (p == 3 ? STAGE_W3 : STAGE_W4);
       for (int t = 0; t < tn * tiles_m; ++t) {
         __syncthreads();
-        gemm_tile<T, TWO, MMA>(g, stage, nullptr, 0, t % tn, t / tn, smem_raw);
+        ft_tile<T, TWO, MMA>(g, stage, t % tn, t / tn, smem_raw);
       }
       __syncthreads();
       select_block(part, tiles_m, n, p, log_eps, scheme, nrm4, need, pm, ps, pe1, pe2, 0);
@@ -109,14 +119,14 @@ expm_tile_fused_kernel(GemmCtx<T> g0, int64_t batch, double log_eps, int scheme,
     for (int stage = STAGE_E1; stage <= STAGE_E3; ++stage)
       for (int t = 0; t < tn * tiles_m; ++t) {
         __syncthreads();
-        gemm_tile<T, TWO, MMA>(g, stage, nullptr, 0, t % tn, t / tn, smem_raw);
+        ft_tile<T, TWO, MMA>(g, stage, t % tn, t / tn, smem_raw);
       }
     const int s = ps[0];
     for (int q = 0; q < s; ++q) {
       g.sq_step = q;
       for (int t = 0; t < tn * tiles_m; ++t) {
         __syncthreads();
-        gemm_tile<T, TWO, MMA>(g, STAGE_SQ, nullptr, 0, t % tn, t / tn, smem_raw);
+        ft_tile<T, TWO, MMA>(g, STAGE_SQ, t % tn, t / tn, smem_raw);
       }
     }
     __syncthreads();

@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(256, (TP <= 16 ? LR_T16_MINB : LR_T32_MINB)) e
             __syncthreads();
           }
         }
-        if (__syncthreads_or(bo)) flags = kLrNonFinite;
+        if (__syncthreads_or(bo)) {  // overflow in the assembly: a flagged X is NaN (include/expmb.h)
+          flags = kLrNonFinite;
+          lr_fill_nan<TI, TP>(x, nn);
+        }
       }
     }
     if (tid == 0) {
@@ -891,8 +894,10 @@ __global__ void __launch_bounds__(128) expm_lowrank_warp_kernel(const T* __restr
         if (__any_sync(0xffffffffu, bo)) flags = kLrNonFinite;
       }
     }
-    if (flags && !wrote)
+    if (flags) {  // also after an overflowing write: a flagged X is NaN (include/expmb.h)
+      __syncwarp();
       for (size_t i = lane; i < (size_t)n * n; i += 32) x[i] = (T)NAN;
+    }
     if (lane == 0) {
       if (po.m) po.m[mat] = (int8_t)m;
       if (po.e1) po.e1[mat] = e1;
@@ -1210,8 +1215,10 @@ __global__ void __launch_bounds__(128, 3) expm_lowrank_dmma_kernel(const TI* __r
         if (__any_sync(0xffffffffu, bo)) flags = kLrNonFinite;
       }
     }
-    if (flags && !wrote)
+    if (flags) {  // also after an overflowing write: a flagged X is NaN (include/expmb.h)
+      __syncwarp();
       for (int i = lane; i < nn; i += 32) x[i] = (TI)NAN;
+    }
     if (lane == 0) {
       if (po.m) po.m[mat] = (int8_t)m;
       if (po.e1) po.e1[mat] = e1;

@@ -40,23 +40,24 @@ def test_fused_tile_bit_identical_to_pipeline(n, dtype, scheme):
     W *= (10.0 ** rng.uniform(-4, 2.3, B) / np.abs(W).sum(axis=1).max(axis=1))[:, None, None]
     W = W.astype(np.float32 if dtype == torch.float32 else np.float64)
     eps = 2.0 ** -24 if dtype == torch.float32 else 1e-12
-    fused = X.expm(torch.as_tensor(W).cuda(), eps, scheme, check_finite=False)
+    res = {}
     with tempfile.TemporaryDirectory() as td:
         np.savez(os.path.join(td, "in.npz"), W=W, eps=eps, scheme=scheme)
-        env = dict(os.environ, EXPMB_FUSED_TILE="0")
-        subprocess.run([sys.executable, "-c", _CHILD, ROOT, os.path.join(td, "in.npz"), os.path.join(td, "out.npz")],
-                       env=env, check=True, timeout=600)
-        pipe = np.load(os.path.join(td, "out.npz"))
-    assert np.array_equal(fused.plan.m.cpu().numpy(), pipe["m"])
-    assert np.array_equal(fused.plan.s.cpu().numpy(), pipe["s"])
-    assert np.array_equal(fused.value.cpu().numpy(), pipe["value"])
-    nm = np.nan_to_num(pipe["norms"], nan=-1.0)
-    assert np.array_equal(np.nan_to_num(fused.plan.norms.cpu().numpy(), nan=-1.0), nm)
+        for path, flag in (("fused", "1"), ("pipe", "0")):   # 1: the fused kernel for fp32 too
+            env = dict(os.environ, EXPMB_FUSED_TILE=flag)
+            out = os.path.join(td, f"{path}.npz")
+            subprocess.run([sys.executable, "-c", _CHILD, ROOT, os.path.join(td, "in.npz"), out],
+                           env=env, check=True, timeout=600)
+            res[path] = dict(np.load(out))
+    fused, pipe = res["fused"], res["pipe"]
+    assert np.array_equal(fused["m"], pipe["m"]) and np.array_equal(fused["s"], pipe["s"])
+    assert np.array_equal(fused["value"], pipe["value"])
+    assert np.array_equal(np.nan_to_num(fused["norms"], nan=-1.0), np.nan_to_num(pipe["norms"], nan=-1.0))
     # and within the bar of the oracle on a few of them
     for i in range(0, B, 13):
         want = O.expm(np.asarray(W[i], np.float64), eps, scheme,
                       tol_floor=2.0 ** -24 if dtype == torch.float32 else 2.0 ** -53)
-        got = fused.value[i].double().cpu().numpy()
+        got = np.asarray(fused["value"][i], np.float64)
         err = np.abs(got - want.value).sum(axis=0).max() / np.abs(want.value).sum(axis=0).max()
         assert err <= (1e-5 if dtype == torch.float32 else 1e-12), (i, err)
 

@@ -304,3 +304,23 @@ def test_lowrank_large_inner_rank_graph_capture():
     torch.cuda.synchronize()
     ref = X.expm_lowrank(X.LowRankPair(a1.clone(), a2.clone()), 1e-12)
     assert torch.equal(xo, ref.value)
+
+
+@pytest.mark.parametrize("n,t", [(2, 1), (64, 8), (40, 20), (80, 40)])
+def test_lowrank_overflow_in_assembly_gives_nan_x(n, t):
+    """V = A2 A1 = 0 (m = 0) but I + A1 A2 overflows fp32: the matrix is flagged
+    non-finite and its X is all NaN (include/expmb.h), on every kernel."""
+    A1 = np.zeros((1, n, t), np.float32)
+    A2 = np.zeros((1, t, n), np.float32)
+    A1[0, 0, 0] = 1e30
+    A2[0, 0, n - 1] = 1e30          # A2 A1 = 0 (disjoint supports), A1 A2 has one 1e60 entry
+    a1 = torch.as_tensor(A1, device="cuda")
+    a2 = torch.as_tensor(A2, device="cuda")
+    xo = torch.zeros(1, n, n, device="cuda")
+    flags = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    X.expm_lowrank_into(a1, a2, xo, 2.0 ** -24, {"flags": flags})
+    torch.cuda.synchronize()
+    assert int(flags[0]) & 2
+    assert torch.isnan(xo).all()
+    with pytest.raises(X.NonFiniteError):
+        _run(A1[0], A2[0], 2.0 ** -24, torch.float32)

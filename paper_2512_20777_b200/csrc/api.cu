@@ -12,6 +12,7 @@
 
 #include "../../include/expmb.h"
 #include "fused_small.cuh"
+#include "fused_w16.cuh"
 #include "fused_dmma.cuh"
 #include "large.cuh"
 #include "fused_tile.cuh"
@@ -80,6 +81,38 @@ static int launch_dmma(const double* W, double* X, int64_t batch, int n, double 
   return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
 }
 
+// fp32 Sastre, n == 16: the warp-batched kernel (fused_w16.cuh).
+template <int Q, int MINB>
+static int launch_w16_q(const float* W, float* X, int64_t batch, double eps, PlanOut po, cudaStream_t st) {
+  auto kern = w16::expm_w16_kernel<Q, MINB>;
+  constexpr size_t smem = w16::smem_bytes<Q>();
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return EXPMB_ERR_CUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, w16::NT, smem) != cudaSuccess || o < 1)
+      return EXPMB_ERR_CUDA;
+    occ = o;
+  }
+  const int64_t warps_needed = (batch + Q - 1) / Q;
+  const int64_t ctas_needed = (warps_needed + w16::WARPS - 1) / w16::WARPS;
+  const int64_t persistent = (int64_t)sm_count() * occ;
+  const int grid = (int)(ctas_needed < persistent ? ctas_needed : persistent);
+  if (grid <= 0) return EXPMB_OK;
+  kern<<<grid, w16::NT, smem, st>>>(W, X, batch, log2(eps), po);
+  return cudaGetLastError() == cudaSuccess ? EXPMB_OK : EXPMB_ERR_CUDA;
+}
+
+static int launch_w16(const float* W, float* X, int64_t batch, double eps, PlanOut po, int*, cudaStream_t st) {
+  // EXPMB_W16_Q: matrices per warp batch (A/B); 6 x 8 warps x 2 CTAs = 212 KB of shared memory per SM
+  static const int q = getenv("EXPMB_W16_Q") ? atoi(getenv("EXPMB_W16_Q")) : 4;
+  static const int minb = getenv("EXPMB_W16_MINB") ? atoi(getenv("EXPMB_W16_MINB")) : 2;
+  if (q == 2) return minb == 3 ? launch_w16_q<2, 3>(W, X, batch, eps, po, st) : launch_w16_q<2, 2>(W, X, batch, eps, po, st);
+  if (minb == 3) return launch_w16_q<4, 3>(W, X, batch, eps, po, st);
+  return launch_w16_q<4, 2>(W, X, batch, eps, po, st);
+}
+
 template <typename T, int SCHEME>
 static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, PlanOut po, int* ctr, cudaStream_t st) {
   // Sastre runs as straight-line code per order (VARIANT 1: 10% faster than
@@ -90,6 +123,10 @@ static int dispatch_small(const T* W, T* X, int64_t batch, int n, double eps, Pl
   // forces dynamic claiming (A/B experiments).
   static const bool claim16 = getenv("EXPMB_CLAIM") && getenv("EXPMB_CLAIM")[0] == '1';
   static const int minb = getenv("EXPMB_C2_MINB") ? atoi(getenv("EXPMB_C2_MINB")) : 2;
+  if constexpr (sizeof(T) == 4 && SCHEME == 0) {
+    static const bool w16 = !(getenv("EXPMB_W16") && getenv("EXPMB_W16")[0] == '0');
+    if (n == 16 && w16) return launch_w16(W, X, batch, eps, po, ctr, st);
+  }
   if (n <= 16) {
     int* c16 = claim16 ? ctr : nullptr;
     // fp32 Sastre default: variant 2 (3xTF32 mma.sync products); 1 = FFMA2 straight-line, 0 = step machine
@@ -288,7 +325,23 @@ int expmb_select_host(const double* norms, double eps, int scheme, int* m, int* 
     // the kernels' fast path first; it must agree with the exact walk below
     const double le = log2(eps);
     int nd = (norms[0] > rung0_threshold(le)) ? 2 : select_sastre_fast(norms[0], 0.0, 1, le, &p);
-    if (nd == 2) nd = select_sastre_fast2(norms[0], norms[1], le, &p), have = 2;
+    if (nd == 2) {
+      // both fast forms (select_sastre_fast2: fused kernels; select_sastre_bf:
+      // the warp-batched n = 16 kernel); a decided plan from either must be
+      // the exact walk's, which the loop below recomputes and checks
+      Plan pb{};
+      const int nb = select_sastre_bf(norms[0], norms[1], le, &pb);
+      nd = select_sastre_fast2(norms[0], norms[1], le, &p), have = 2;
+      if (nb == 0) {
+        Plan px{};
+        int hv = 1;
+        for (int need; (need = select_walk(norms, hv, eps, scheme, &px)) != 0;) hv = need;
+        if (px.m != pb.m || px.s != pb.s || pb.e1 != (nd == 0 ? p.e1 : pb.e1)) {
+          if (m) *m = -1;  // surfaces as a plan mismatch in the tests
+          return -1;
+        }
+      }
+    }
     if (nd == 0) {
       if (m) *m = p.m;
       if (s) *s = p.s;
@@ -365,6 +418,8 @@ int expmb_select(const void* W, int64_t batch, int32_t n, int dtype, double eps,
     int* ctr = (workspace != nullptr && workspace_bytes >= sizeof(int)) ? (int*)workspace : nullptr;
     if (dtype == EXPMB_F32) {
       const float* w = (const float*)W;
+      if (n == 16 && scheme == 0 && !(getenv("EXPMB_W16") && getenv("EXPMB_W16")[0] == '0'))
+        return launch_w16(w, nullptr, batch, eps, po, ctr, st);  // the same kernel (and norms) as expmb_expm
       if (n <= 16) return scheme == 0 ? launch_fused<float, 16, 2, 8, 0>(w, nullptr, batch, n, eps, po, ctr, st)
                                       : launch_fused<float, 16, 2, 8, 1>(w, nullptr, batch, n, eps, po, ctr, st);
       if (n <= 32) return scheme == 0 ? launch_fused<float, 32, 4, 4, 0>(w, nullptr, batch, n, eps, po, ctr, st)

@@ -462,6 +462,73 @@ done:
   return 0;
 }
 
+// Branch-free form of select_sastre_fast2 for the warp-batched kernel, whose
+// lanes 0..Q-1 each select for a different matrix: divergent early exits made
+// the SIMT walk cost the union of every lane's path.  All four rungs are
+// evaluated (two MUFU ops each) and the first one that does not certainly fail
+// is picked with selects.  A rung passes if max(l1, l2) + 1 or the fast
+// logaddexp2 clears log_eps - M, fails if max(l1, l2) or the fast logaddexp2
+// exceeds log_eps + M, else it is too close to call (-1: exact walk).  The
+// fast logaddexp2 is within 1e-6 of the exact one, which lies in
+// [max, max + 1], so no decided rung can disagree with the exact walk; the
+// e1/e2 products are select_sastre_fast2's.
+EXPMB_HD int select_sastre_bf(double n1, double n2, double log_eps_d, Plan* out) {
+  const double lo = 0x1p-100, hi = 0x1p100;
+  if (!(n1 >= lo && n1 <= hi && n2 >= lo && n2 <= hi)) return -1;
+  const float M = 2e-4f;
+  const float le = (float)log_eps_d;
+  const float lw1 = lg2_fast(n1), lw2 = lg2_fast(n2);
+  const float T[8] = {(float)-0x1.4ae00d1cfdeb4p+1, (float)-0x1.2570068e7ef5ap+2, (float)-0x1.ba0a7eda4c113p+2,
+                      (float)-0x1.2fbd42b465836p+3, (float)-0x1.278191a01a44ep+4, (float)-0x1.5ca82fb30d8bcp+4,
+                      (float)-0x1.6b1bc6161c270p+5, (float)-0x1.82b3695d62b2fp+5};
+  int ri = 4, v = 0;
+  float L1 = 0.f, L2 = 0.f;
+#pragma unroll
+  for (int i = 4; i >= 1; --i) {  // reverse: the first rung that does not fail wins
+    const float kf = (float)(1 << (i - 1));
+    float l1, l2;
+    if (i < 4) {  // m = 2, 4, 8: J K = m, both tails gain lw1 / lw2
+      l1 = T[2 * i - 2] + kf * lw2 + lw1;
+      l2 = T[2 * i - 1] + kf * lw2 + lw2;
+    } else {      // m = 15
+      l1 = T[6] + 8.0f * lw2;
+      l2 = T[7] + 8.0f * lw2 + lw1;
+    }
+    const float h = fmaxf(l1, l2);
+    const float lae = h + fast_l2p(fabsf(l1 - l2));
+    const bool pass = (h + 1.0f < le - M) || (lae < le - M);
+    const bool fail = (h > le + M) || (lae > le + M);
+    const int vi = pass ? 1 : (fail ? 0 : -1);
+    if (i == 4) { L1 = l1; L2 = l2; }
+    if (vi != 0) { ri = i; v = vi; L1 = l1; L2 = l2; }
+  }
+  if (v < 0) return -1;
+  int s = 0;
+  if (v == 0) {
+    const float va = fmaxf((L1 - le) * (1.0f / 16.0f), (L2 - le) * (1.0f / 17.0f));
+    float c_lo = ceilf(va - M), c_hi = ceilf(va + M);
+    c_lo = fminf(fmaxf(c_lo, 0.f), (float)kMaxScaling);
+    c_hi = fminf(fmaxf(c_hi, 0.f), (float)kMaxScaling);
+    if (c_lo != c_hi) return -1;
+    s = (int)c_lo;
+  }
+  double pk = n2;
+  if (ri >= 2) pk *= pk;
+  if (ri >= 3) pk *= pk;
+  if (ri >= 4) pk *= pk;
+  const double t1 = sastre_tail(2 * ri), t2 = sastre_tail(2 * ri + 1);
+  out->m = ri == 1 ? 2 : ri == 2 ? 4 : ri == 3 ? 8 : 15;
+  out->s = s;
+  if (ri < 4) {
+    out->e1 = t1 * pk * n1;
+    out->e2 = t2 * pk * n2;
+  } else {
+    out->e1 = t1 * pk;
+    out->e2 = t2 * pk * n1;
+  }
+  return 0;
+}
+
 // Same walk from the norms themselves (host tests, large-n select kernels).
 EXPMB_HD int select_walk(const double* nrm, int have, double eps, int scheme, Plan* out) {
   if (nrm[0] == 0.0) {  // select.py:172-173

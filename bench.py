@@ -472,9 +472,10 @@ def run_lowrank(args):
         traffic = json.load(open(tpath)).get("dram_bytes_per_launch") if os.path.exists(tpath) else None
         roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["hbm_src"],
-                "algorithmic_bytes_per_launch": hbm_bytes, "kernel": "expm_lowrank_kernel<double,8>",
-                "other": {"bound": "fp64_dfma", "achieved": flops / (ms_per_step * 1e-3) / 1e12,
-                          "peak": pk["dfma_fp64"], "unit": "TFLOP/s", "useful_flops_per_launch": flops}}
+                "algorithmic_bytes_per_launch": hbm_bytes, "kernel": "expm_lowrank_dmma_kernel (DMMA)",
+                "other": {"bound": "fp64", "achieved": flops / (ms_per_step * 1e-3) / 1e12,
+                          "peak": pk["fp64"], "peak_source": pk["fp64_src"], "unit": "TFLOP/s",
+                          "useful_flops_per_launch": flops}}
         cpu = None
         if not args.no_cpu_baseline and ws == 1:  # the CPU baseline is an N=1 measurement
             r, cores, sample = cpu_lowrank_rate()
@@ -705,7 +706,8 @@ def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool =
     hbm_binds = t_hbm >= t_cmp or tc_products
     roof = dict(hbm_roof if hbm_binds else cmp_roof)
     if cfg.n <= 16:
-        roof["kernel"] = "expm_fused_kernel<float,16,...> (3xTF32 mma.sync)" if tc_products else "expm_fused_kernel"
+        roof["kernel"] = ("w16::expm_w16_kernel (warp-batched, 3xTF32 mma.sync)" if tc_products and cfg.n == 16
+                          else "expm_fused_kernel<float,16,...> (3xTF32 mma.sync)" if tc_products else "expm_fused_kernel")
     elif cfg.n <= 64:
         roof["kernel"] = "expm_dmma_kernel (DMMA)" if cfg.dtype == "f64" else "expm_fused_kernel"
     else:

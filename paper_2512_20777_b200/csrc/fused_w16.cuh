@@ -25,8 +25,7 @@
 // reads (LDS.64) and the B-fragment reads of the W^2 product (LDS.32) are
 // bank-conflict free.  Slot j of the next batch is refilled as soon as phase 3
 // has read W_j, so the copy overlaps the rest of the batch; nothing is
-// prefetched into registers.  Batches are claimed dynamically one batch ahead
-// (one atomic per Q matrices).
+// prefetched into registers.  Each warp owns a contiguous range of matrices.
 //
 // Register layout of a 16x16 state matrix (the m16n8k8 accumulator layout,
 // lane = 4 g + t): v[4 nt + q] = X[g + 8 (q >> 1)][8 nt + 2 t + (q & 1)].
@@ -41,7 +40,10 @@
 namespace expmb {
 namespace w16 {
 
-constexpr int WARPS = 8;   // warps per CTA
+#ifndef EXPMB_W16_WARPS
+#define EXPMB_W16_WARPS 8
+#endif
+constexpr int WARPS = EXPMB_W16_WARPS;   // warps per CTA
 constexpr int NT = 32 * WARPS;
 constexpr int LDR = 20;    // product right-operand stride: B-fragment rows 2t, 2t+1 conflict-free
 
@@ -80,9 +82,9 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// stage matrix idx (if it exists) into a slot: lane copies chunks lane, lane + 32
-__device__ __forceinline__ void stage(float* slot, const float* __restrict__ W, int64_t idx, int64_t batch, int lane) {
-  if (idx < batch) {
+// stage matrix idx (if idx < end) into a slot: lane copies chunks lane, lane + 32
+__device__ __forceinline__ void stage(float* slot, const float* __restrict__ W, int64_t idx, int64_t end, int lane) {
+  if (idx < end) {
     const float* src = W + idx * 256;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -315,20 +317,24 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   WarpSmem<Q>& S = reinterpret_cast<WarpSmem<Q>*>(smem_raw)[warp];
-  const int64_t nbatch = (batch + Q - 1) / Q;
-  const int64_t stride = (int64_t)gridDim.x * WARPS;  // static round-robin over warp batches
-  int64_t b = (int64_t)blockIdx.x * WARPS + warp;
-  if (b >= nbatch) return;
+  // each warp owns a contiguous range of floor/ceil(batch / warps) matrices,
+  // taken Q at a time (round-robin whole batches left a tail of up to one
+  // batch per warp: 7 vs 6 batches at C2's 65536 / 2368 warps)
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t lo = batch * gw / nwarps, hi = batch * (gw + 1) / nwarps;
+  if (lo >= hi) return;
   const double rung0_thr = rung0_threshold(log_eps);
   const float2 dg = make_float2(g == 2 * t ? 1.f : 0.f, g == 2 * t + 1 ? 1.f : 0.f);
   float* lane_a2 = &S.a2[0][0] + 8 * lane;
+  int64_t base = lo;
 
 #pragma unroll
-  for (int j = 0; j < Q; ++j) stage(S.w[j], W, b * Q + j, batch, lane);
+  for (int j = 0; j < Q; ++j) stage(S.w[j], W, base + j, hi, lane);
 
   while (true) {
-    const int64_t nb = b + stride;
-    const int nq = (int)min((int64_t)Q, batch - b * Q);  // matrices in this batch (warp-uniform)
+    const int64_t nbase = base + Q;
+    const int nq = (int)min((int64_t)Q, hi - base);  // matrices in this batch (warp-uniform)
     // ---- phase 1: W^2 and both norms per matrix --------------------------------
     // (slot j's copy was issued while the previous batch's matrix j finished;
     // by now every one has landed, so one wait for all of them)
@@ -345,7 +351,22 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
       *reinterpret_cast<float4*>(lane_a2 + 256 * j) = make_float4(a[0], a[1], a[2], a[3]);
       *reinterpret_cast<float4*>(lane_a2 + 256 * j + 4) = make_float4(a[4], a[5], a[6], a[7]);
     };
-#if EXPMB_W16_P1X2
+#if EXPMB_W16_P1X2 == 4
+    if (nq == 4) {  // four independent W^2 chains
+      float w[4][8], a[4][8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) load_w(S.w[j], g, t, w[j]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float* sj = S.w[j];
+        product(w[j], [sj](int k, int n) { return sj[widx(k, n)]; }, g, t, a[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) finish1(j, w[j], a[j]);
+    }
+#pragma unroll 1
+    for (int j = (nq == 4 ? 4 : 0); j < nq; ++j) {
+#elif EXPMB_W16_P1X2
     // two matrices per iteration: independent HMMA / shuffle chains interleave
 #pragma unroll 1
     for (int j = 0; j + 1 < nq; j += 2) {
@@ -376,7 +397,7 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
     int packed = 0;  // m << 8 | s
     bool my_bad = false;
     if (lane < nq) {
-      const int64_t idx = b * Q + lane;
+      const int64_t idx = base + lane;
       const double n1 = (double)my_n1;
       double n2 = (double)my_n2;
       // the common case stays in registers (select_sastre_bf inlines); the
@@ -432,12 +453,12 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
     // ---- phase 3: evaluate and square ------------------------------------------
 #pragma unroll 1
     for (int j = 0; j < Q; ++j) {
-      const int64_t idx = b * Q + j;
+      const int64_t idx = base + j;
       const int pk = __shfl_sync(0xffffffffu, packed, j);
       float B[8];
       if (j < nq && !po.plan_only) load_w(S.w[j], g, t, B);
       __syncwarp();  // every lane has read slot j: refill it with the next batch's matrix j
-      stage(S.w[j], W, nb < nbatch ? nb * Q + j : batch, batch, lane);
+      stage(S.w[j], W, nbase + j, hi, lane);
       if (j >= nq || po.plan_only) continue;
       const int m = pk >> 8, s = pk & 0xff;
       float P[8];
@@ -487,9 +508,9 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
           __stcs(reinterpret_cast<float2*>(dst + (g + 8 * h) * 16 + 8 * nt + 2 * t),
                  make_float2(P[4 * nt + 2 * h], P[4 * nt + 2 * h + 1]));
     }
-    if (po.nonfinite && lane < nq) po.nonfinite[b * Q + lane] = (uint8_t)my_bad;
-    if (nb >= nbatch) break;
-    b = nb;
+    if (po.nonfinite && lane < nq) po.nonfinite[base + lane] = (uint8_t)my_bad;
+    if (nbase >= hi) break;
+    base = nbase;
   }
   cp_wait<0>();
 }

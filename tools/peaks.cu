@@ -84,6 +84,29 @@ __global__ void k_tf32(float* out) {
   for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
   if (s == 1.2345f) out[0] = s;
 }
+template <bool BF>
+__global__ void k_h16(float* out) {  // mma.sync m16n8k16, f16 / bf16 inputs, f32 accumulate
+  unsigned a0 = threadIdx.x * 0x00010001u, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, b0 = a0 * 3, b1 = a0 * 5;
+  float c[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i][0] = i; c[i][1] = i + threadIdx.x; c[i][2] = -i; c[i][3] = i * 0.5f; }
+  for (int it = 0; it < ITERS / 16; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if constexpr (BF)
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                     : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      else
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                     : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 1.2345f) out[0] = s;
+}
 
 // ---- tcgen05.mma throughput: operands stay in shared memory (128B-swizzled,
 // K-major), so the tensor pipe is the only thing measured ----
@@ -191,6 +214,10 @@ int main() {
   printf("{\"pipe\": \"dmma_m8n8k4_fp64\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 512 / (t * 1e-3) / 1e12, t);
   t = timeit([&] { k_tf32<<<blocks, threads>>>(fo); });
   printf("{\"pipe\": \"mma_sync_m16n8k8_tf32\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 2048 / (t * 1e-3) / 1e12, t);
+  t = timeit([&] { k_h16<false><<<blocks, threads>>>(fo); });
+  printf("{\"pipe\": \"mma_sync_m16n8k16_f16\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 4096 / (t * 1e-3) / 1e12, t);
+  t = timeit([&] { k_h16<true><<<blocks, threads>>>(fo); });
+  printf("{\"pipe\": \"mma_sync_m16n8k16_bf16\", \"tflops\": %.2f, \"ms\": %.3f}\n", warps * (ITERS / 16) * 8 * 4096 / (t * 1e-3) / 1e12, t);
   {
     int* io; cudaMalloc(&io, 64);
     cudaFuncSetAttribute(k_tcgen05<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);

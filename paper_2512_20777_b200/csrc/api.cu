@@ -108,6 +108,7 @@ static int launch_w16(const float* W, float* X, int64_t batch, double eps, PlanO
   // EXPMB_W16_Q: matrices per warp batch (A/B); 6 x 8 warps x 2 CTAs = 212 KB of shared memory per SM
   static const int q = getenv("EXPMB_W16_Q") ? atoi(getenv("EXPMB_W16_Q")) : 4;
   static const int minb = getenv("EXPMB_W16_MINB") ? atoi(getenv("EXPMB_W16_MINB")) : 2;
+  if (q == 8) return minb == 3 ? launch_w16_q<8, 3>(W, X, batch, eps, po, st) : launch_w16_q<8, 2>(W, X, batch, eps, po, st);
   if (q == 2) return minb == 3 ? launch_w16_q<2, 3>(W, X, batch, eps, po, st) : launch_w16_q<2, 2>(W, X, batch, eps, po, st);
   if (minb == 3) return launch_w16_q<4, 3>(W, X, batch, eps, po, st);
   return launch_w16_q<4, 2>(W, X, batch, eps, po, st);

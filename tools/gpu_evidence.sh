@@ -2,7 +2,7 @@
 # Full evidence run (round 2): GPU tests, smoke, default bench (C2 headline +
 # per_config C1/C3/C4/C5, CPU baseline), reference arm, Alg. 1 / time-grid /
 # low-rank lines, then the C2 launch list and one ncu --set full capture each
-# of the C2 (w16), C1 (DMMA) and C5 (int8 stage) kernels.
+# of the C2 (w16) kernel; tools/gpu_evidence_b.sh has the C1 / C5 captures.
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q -rf -p no:cacheprovider --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
@@ -18,10 +18,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-per-config > gpurun_out/ncu1.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:w16 -s 3 -c 1 \
     -o gpurun_out/prof_C2 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-per-config > gpurun_out/ncu2.log 2>&1
-python bench.py --config C1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:dmma -s 3 -c 1 \
-    -o gpurun_out/prof_C1 -f python bench.py --config C1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu3.log 2>&1
-python bench.py --config C5 --steps 1 --warmup 3 --no-cpu-baseline --batch 8 > gpurun_out/plain5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_i8_stage -s 30 -c 1 \
-    -o gpurun_out/prof_C5 -f python bench.py --config C5 --steps 1 --warmup 3 --no-cpu-baseline --batch 8 > gpurun_out/ncu5.log 2>&1
 echo done

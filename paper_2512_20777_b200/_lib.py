@@ -59,60 +59,33 @@ def lib() -> ctypes.CDLL:
         )
     L = ctypes.CDLL(LIB_PATH)
     c = ctypes
-    L.expmb_version.restype = c.c_int
-    L.expmb_strerror.restype = c.c_char_p
-    L.expmb_strerror.argtypes = [c.c_int]
-    L.expmb_unit_roundoff.restype = c.c_double
-    L.expmb_unit_roundoff.argtypes = [c.c_int]
-    L.expmb_workspace_bytes.restype = c.c_size_t
-    L.expmb_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int, c.c_int]
-    L.expmb_expm.restype = c.c_int
-    L.expmb_expm.argtypes = [
-        c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-        c.c_void_p, c.c_size_t, c.c_void_p,
-    ]
-    if not hasattr(L, "expmb_select"):  # an older A/B build (EXPMB_LIB)
-        L.expmb_select = None
-    else:
-        L.expmb_select.restype = c.c_int
-    if L.expmb_select is not None:
-        L.expmb_select.argtypes = [
-        c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-        c.c_void_p, c.c_size_t, c.c_void_p,
-    ]
-    L.expmb_select_host.restype = c.c_int
-    L.expmb_select_host.argtypes = [
-        c.POINTER(c.c_double), c.c_double, c.c_int,
-        c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
-    ]
-    L.expmb_lowrank_workspace_bytes.restype = c.c_size_t
-    L.expmb_lowrank_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32, c.c_int]
-    L.expmb_expm_lowrank.restype = c.c_int
-    L.expmb_expm_lowrank.argtypes = [
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_int, c.c_double,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p,
-    ]
-    L.expmb_select_lowrank_host.restype = c.c_int
-    L.expmb_select_lowrank_host.argtypes = [
-        c.POINTER(c.c_double), c.c_int, c.c_double,
-        c.POINTER(c.c_int), c.POINTER(c.c_double), c.POINTER(c.c_double),
-    ]
-    L.expmb_timegrid_workspace_bytes.restype = c.c_size_t
-    L.expmb_timegrid_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int]
-    L.expmb_expm_timegrid.restype = c.c_int
-    L.expmb_expm_timegrid.argtypes = [
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-        c.c_void_p, c.c_size_t, c.c_void_p,
-    ]
-    L.expmb_expm_pipelined.restype = c.c_int
-    L.expmb_expm_pipelined.argtypes = [
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int, c.c_double, c.c_int,
-        c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-        c.c_int, c.c_void_p, c.c_size_t, c.c_void_p, c.c_void_p, c.c_void_p,
-    ]
+    vp, sz, i32, i64, ci, cd = c.c_void_p, c.c_size_t, c.c_int32, c.c_int64, c.c_int, c.c_double
+    dp, ip = c.POINTER(c.c_double), c.POINTER(c.c_int)
+    sigs = {
+        "expmb_version": (ci, []),
+        "expmb_strerror": (c.c_char_p, [ci]),
+        "expmb_unit_roundoff": (cd, [ci]),
+        "expmb_workspace_bytes": (sz, [i64, i32, ci, ci]),
+        "expmb_expm": (ci, [vp, vp, i64, i32, ci, cd, ci] + [vp] * 7 + [vp, sz, vp]),
+        "expmb_select": (ci, [vp, i64, i32, ci, cd, ci] + [vp] * 7 + [vp, sz, vp]),
+        "expmb_select_host": (ci, [dp, cd, ci, ip, ip, dp, dp]),
+        "expmb_lowrank_workspace_bytes": (sz, [i64, i32, i32, ci]),
+        "expmb_expm_lowrank": (ci, [vp, vp, vp, i64, i32, i32, ci, cd] + [vp] * 7 + [sz, vp]),
+        "expmb_select_lowrank_host": (ci, [dp, ci, cd, ip, dp, dp]),
+        "expmb_timegrid_workspace_bytes": (sz, [i64, i32, ci]),
+        "expmb_expm_timegrid": (ci, [vp, vp, vp, i64, i32, ci, cd, ci] + [vp] * 7 + [vp, sz, vp]),
+        "expmb_expm_pipelined": (ci, [vp, vp, vp, vp, i64, i32, ci, cd, ci] + [vp] * 7 + [ci, vp, sz, vp, vp, vp]),
+    }
+    ab_build = "EXPMB_LIB" in os.environ  # an A/B build of another revision may lack newer entry points
+    for name, (res, args) in sigs.items():
+        if not hasattr(L, name):
+            if not ab_build:
+                raise OSError(f"{LIB_PATH} does not export {name} (stale build? run make)")
+            setattr(L, name, None)
+            continue
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
     _lib = L
     return L
 

@@ -231,7 +231,10 @@ __device__ __forceinline__ int simt_col(int tx, int j) {
 // tensor cores) instead of DFMAs: warp (wr, wc) of the 2 x 4 warp grid owns a
 // 64 x 32 sub-tile = 8 x 4 DMMA tiles, and thread "row slot" i / column pair
 // j0 of the epilogue map onto the accumulator fragments.
-template <typename T, bool TWO, bool MMA>
+// A1: the Alg. 1 term stage's extra X += Y epilogue (its own instantiation,
+// so the other stages' epilogues carry no extra live registers: with it
+// inline the fp32 kernel's spills grew from 48 to 84 bytes and C3 slowed 13%)
+template <typename T, bool TWO, bool MMA, bool A1 = false>
 __device__ __forceinline__ void gemm_tile(const GemmCtx<T>& g, int stage, const int* __restrict__ list, int slot,
                                           int bx, int by, unsigned char* smem_raw) {
   using C = SimtCfg<T>;
@@ -462,7 +465,7 @@ __device__ __forceinline__ void gemm_tile(const GemmCtx<T>& g, int stage, const 
         }
       };
       put(e.out[0], o0);
-      if (e.acc_dst != nullptr) {  // X += Y (Alg. 1): the same positions, one read-modify-write
+      if (A1 && e.acc_dst != nullptr) {  // X += Y (Alg. 1): the same positions, one read-modify-write
         T xv[VW];
 #pragma unroll
         for (int v = 0; v < VW; ++v) xv[v] = (col0 + v < n) ? e.acc_dst[pos + v] + e.acc_src[pos + v] : T(0);
@@ -513,7 +516,7 @@ __device__ __forceinline__ void gemm_tile(const GemmCtx<T>& g, int stage, const 
 template <typename T, bool TWO>
 constexpr bool kZStride = sizeof(T) == 4 && !TWO;
 
-template <typename T, bool TWO = (sizeof(T) == 4), bool MMA = false>
+template <typename T, bool TWO = (sizeof(T) == 4), bool MMA = false, bool A1 = false>
 __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !TWO) ? 2 : 1)
 gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list, const int* __restrict__ dcount, int hcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -525,7 +528,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list, const i
     // CTAs, so the z-stride grid is balanced
     for (int slot = blockIdx.z; slot < cnt; slot += gridDim.z) {
       __syncthreads();  // the previous unit's epilogue may still read shared memory
-      gemm_tile<T, TWO, MMA>(g, stage, list, slot, blockIdx.x, blockIdx.y, smem_raw);
+      gemm_tile<T, TWO, MMA, A1>(g, stage, list, slot, blockIdx.x, blockIdx.y, smem_raw);
     }
   } else {
     const int total = cnt * (((g.n + kGemmBN - 1) / kGemmBN) * g.tiles_m);
@@ -533,7 +536,7 @@ gemm_stage_kernel(GemmCtx<T> g, int stage, const int* __restrict__ list, const i
       const int tn = (g.n + kGemmBN - 1) / kGemmBN, tiles = tn * g.tiles_m;
       const int slot = w / tiles, t = w - slot * tiles;
       __syncthreads();  // the previous unit's epilogue may still read shared memory
-      gemm_tile<T, TWO, MMA>(g, stage, list, slot, t % tn, t / tn, smem_raw);
+      gemm_tile<T, TWO, MMA, A1>(g, stage, list, slot, t % tn, t / tn, smem_raw);
     }
   }
 }
@@ -580,15 +583,15 @@ static int persistent_grid(K kern, int threads, size_t smem, int64_t units, int*
 
 // One product stage over `list` (null = slots 0..), the first *dcount slots
 // (dcount null: `count`); `count` bounds the work on the host side.
-template <typename T>
-static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st,
-                       const int* dcount = nullptr) {
+template <typename T, bool A1>
+static int gemm_launch_t(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st,
+                         const int* dcount) {
   if (count <= 0) return 0;
   static bool attr = false;
   constexpr int smem = simt_smem_bytes<T>();
-  auto k_two = gemm_stage_kernel<T, true>;
-  auto k_one = gemm_stage_kernel<T, false>;
-  auto k_mma = gemm_stage_kernel<T, false, sizeof(T) == 8>;
+  auto k_two = gemm_stage_kernel<T, true, false, A1>;
+  auto k_one = gemm_stage_kernel<T, false, false, A1>;
+  auto k_mma = gemm_stage_kernel<T, false, sizeof(T) == 8, A1>;
   if (!attr) {
     if (cudaFuncSetAttribute(k_two, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
         cudaFuncSetAttribute(k_one, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
@@ -611,6 +614,12 @@ static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int coun
     k_one<<<dim3(tn, tm, std::min(count, zc)), 256, smem, st>>>(g, stage, list, dcount, count);
   }
   return cudaGetLastError() != cudaSuccess;
+}
+template <typename T>
+static int gemm_launch(const GemmCtx<T>& g, int stage, const int* list, int count, cudaStream_t st,
+                       const int* dcount = nullptr) {
+  return stage == STAGE_A1 ? gemm_launch_t<T, true>(g, stage, list, count, st, dcount)
+                           : gemm_launch_t<T, false>(g, stage, list, count, st, dcount);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,9 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out
 for rep in 1 2; do
-timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/s4_base_$rep.json 2>gpurun_out/s4_base_$rep.err
-EXPMB_LIB=libexpmb_w6.so EXPMB_W16_Q=8 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/s4_q8w6_$rep.json 2>gpurun_out/s4_q8w6_$rep.err
-EXPMB_LIB=libexpmb_w4.so EXPMB_W16_Q=8 EXPMB_W16_MINB=3 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/s4_q8w4m3_$rep.json 2>gpurun_out/s4_q8w4m3_$rep.err
-EXPMB_LIB=libexpmb_w6.so timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/s4_q4w6_$rep.json 2>gpurun_out/s4_q4w6_$rep.err
+for lib in libexpmb_old.so libexpmb_c686.so libexpmb.so; do
+for c in C3 C4; do
+EXPMB_LIB=$lib timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-per-config > gpurun_out/s7_${c}_${lib}_$rep.json 2>gpurun_out/s7_${c}_${lib}_$rep.err
+done
+done
 done
 echo done

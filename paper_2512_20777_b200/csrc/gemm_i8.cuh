@@ -703,9 +703,38 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// Multicast TMA / commit helpers for the 2-CTA cluster form below.
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(tc::smem_u32(dst)),
+      "l"(map), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          tc::smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // One-unit-per-CTA form of the stage (grid: column blocks x row blocks x
 // slots, slots beyond the device count exit at once); A/B against the
 // persistent k_i8_stage (EXPMB_I8_PERSIST).
+//
+// MC: launched as 2-CTA clusters along the column blocks.  The pair shares
+// its 128-row L block, so each CTA loads two of the four L slices with
+// .multicast::cluster into both CTAs' rings (and its own four R slices), and
+// each MMA warp releases a ring stage to both producers (multicast commit;
+// the empty barriers count two arrivals).  The stage was bound by the L2 ->
+// SM operand stream (768 MB per 2048^2 product at 128 x 64 tiles); sharing
+// the L panel cuts it to 512 MB.
+template <bool MC>
 __global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
 k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs bf,
               const int* __restrict__ dcount) {
@@ -733,10 +762,11 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
     cs_sh[threadIdx.x] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
     dr_sh[threadIdx.x] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
   }
+  const int rank = MC ? (int)(blockIdx.x & 1) : 0;  // cluster dims (2, 1, 1): the rank is blockIdx.x % 2
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       tc::mbar_init(&full_bar[i], 1);
-      tc::mbar_init(&empty_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], MC ? 2 : 1);  // MC: both CTAs' MMAs release the stage
     }
     tc::mbar_init(&tmem_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -748,7 +778,8 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // the peer's barriers are initialised before any multicast lands
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_sh;
 
@@ -758,11 +789,19 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
       const int st = kt % STAGES;
       tc::mbar_wait(&empty_bar[st], ((kt / STAGES) & 1) ^ 1);
       unsigned char* b = sm + st * STAGE_BYTES;
-      tc::mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+      // (MC, odd column-block count: the pad CTA of the last pair has no
+      // columns; it still takes its share of the L multicast, loads no R)
+      const bool rvalid = !MC || n0 < n;
+      tc::mbar_expect_tx(&full_bar[st], rvalid ? STAGE_BYTES : NSL * A_TILE);
 #pragma unroll
       for (int i = 0; i < NSL; ++i) {
-        tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
-        tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
+        if constexpr (MC) {
+          if ((i >> 1) == rank)  // L slices 2 rank, 2 rank + 1 into both CTAs of the pair
+            tma_load_3d_mc(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i, (uint16_t)3);
+        } else {
+          tc::tma_load_3d(b + i * A_TILE, &maps.a, &full_bar[st], kt * BKB, m0, slot * NSL + i);
+        }
+        if (rvalid) tc::tma_load_3d(b + NSL * A_TILE + i * B_TILE, &maps.b, &full_bar[st], kt * BKB, n0, slot * NSL + i);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -784,7 +823,8 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
           mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
         }
       }
-      tc::mma_commit(&empty_bar[st]);
+      if constexpr (MC) mma_commit_mc(&empty_bar[st], (uint16_t)3);
+      else tc::mma_commit(&empty_bar[st]);
     }
     tc::mma_commit(&tmem_bar);
   } else if (warp >= 2) {
@@ -942,7 +982,10 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
 #undef I8_LOAD_ROWS
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  // MC: the peer's last multicast commits target this CTA's barriers, so
+  // neither CTA leaves before both are done
+  if constexpr (MC) cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 

@@ -359,16 +359,37 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
                                                                                             dcount, count);
   if (chk("slice")) return 1;
   static const bool persist = getenv("EXPMB_I8_PERSIST") && getenv("EXPMB_I8_PERSIST")[0] == '1';
+  // 2-CTA clusters sharing the L panel by multicast (EXPMB_I8_MC=0: one CTA per tile)
+  static const bool mc = !(getenv("EXPMB_I8_MC") && getenv("EXPMB_I8_MC")[0] == '0');
   static bool attr_np = false;
   if (!persist) {
     if (!attr_np) {
-      if (cudaFuncSetAttribute(i8::k_i8_stage_np, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::SMEM_BYTES) !=
-          cudaSuccess)
+      if (cudaFuncSetAttribute(i8::k_i8_stage_np<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               i8::SMEM_BYTES) != cudaSuccess ||
+          cudaFuncSetAttribute(i8::k_i8_stage_np<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               i8::SMEM_BYTES) != cudaSuccess)
         return 1;
       attr_np = true;
     }
-    i8::k_i8_stage_np<<<dim3((n + i8::BN - 1) / i8::BN, (n + i8::BM - 1) / i8::BM, count), i8::NTHREADS,
-                        i8::SMEM_BYTES, st>>>(maps, g, stage, list, b, dcount);
+    const int tn = (n + i8::BN - 1) / i8::BN, tm = (n + i8::BM - 1) / i8::BM;
+    if (mc) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)((tn + 1) & ~1), (unsigned)tm, (unsigned)count);  // whole pairs
+      cfg.blockDim = dim3(i8::NTHREADS);
+      cfg.dynamicSmemBytes = i8::SMEM_BYTES;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, i8::k_i8_stage_np<true>, maps, g, stage, list, b, dcount) != cudaSuccess) return 1;
+    } else {
+      i8::k_i8_stage_np<false><<<dim3(tn, tm, count), i8::NTHREADS, i8::SMEM_BYTES, st>>>(maps, g, stage, list, b,
+                                                                                        dcount);
+    }
   }
   const int64_t units = (int64_t)count * ((n + i8::BN - 1) / i8::BN) * ((n + i8::BM - 1) / i8::BM);
   if (persist) i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS, i8::SMEM_BYTES, units, &occ_stage,

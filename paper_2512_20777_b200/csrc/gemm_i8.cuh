@@ -335,6 +335,166 @@ __global__ void __launch_bounds__(256, 8) k_i8_slice(GemmCtx<float> g, int stage
   }
 }
 
+// One pass per operand instead of stats (32 x 32 tiles, atomics) + slice:
+//  - an L unit is 8 rows, one warp per row: the warp reads its row once for
+//    the maximum |entry| and the exponent sums (no atomics: the row is whole
+//    in one warp) and once more, from L1/L2, to cut the four slices;
+//  - an R unit is a 32-column strip: 8 warps stream its rows for the column
+//    maxima (a shared-memory reduction), then re-read it in 32 x 32 tiles
+//    and write the transposed slices.
+// Same outputs (er / rc / ec / cc / as / bs) and bits as k_i8_stats +
+// k_i8_slice; the diagonal is left out exactly as there.
+#ifndef EXPMB_I8_PREP_MINB
+#define EXPMB_I8_PREP_MINB 4
+#endif
+__device__ __forceinline__ uint32_t pack_plane(const int8_t (&v)[4][4], int j) {
+  return (uint32_t)(uint8_t)v[0][j] | ((uint32_t)(uint8_t)v[1][j] << 8) | ((uint32_t)(uint8_t)v[2][j] << 16) |
+         ((uint32_t)(uint8_t)v[3][j] << 24);
+}
+__device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const float* __restrict__ L, const Bufs& b,
+                                             int slot, int r) {
+  const int n = g.n, lane = threadIdx.x & 31;
+  const float* row = L + (size_t)r * n;
+  int m = 0;
+  unsigned long long sm = 0;
+#pragma unroll 4
+  for (int c = 4 * lane; c < n; c += 128) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
+    const float x[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float v = c + u == r ? 0.f : fabsf(x[u]);
+      m = max(m, __float_as_int(v));
+      sm += exp_pack(v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  if (lane == 0) {
+    b.er[(size_t)slot * n + r] = m;
+    b.rc[(size_t)slot * n + r] = sm;
+  }
+  const int ex = exp_of(__int_as_float(m));
+  const size_t plane = (size_t)n * b.np;
+  int8_t* as = b.as + (size_t)slot * NSL * plane + (size_t)r * b.np;
+#pragma unroll 4
+  for (int c = 4 * lane; c < n; c += 128) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
+    const float x[4] = {a.x, a.y, a.z, a.w};
+    int8_t sl[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) slice4(c + u == r ? 0.f : x[u], ex, sl[u]);
+#pragma unroll
+    for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + c) = pack_plane(sl, j);
+  }
+}
+__device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const float* __restrict__ R, const Bufs& b,
+                                             int slot, int c0) {
+  __shared__ int pm[32][33];
+  __shared__ unsigned long long ps[32][33];
+  __shared__ int pex[32];
+  __shared__ float tile[32][33];
+  const int n = g.n;  // a multiple of 16 on this path: a float4 group is all in or all out
+  // pass 1: thread (row phase ty = 0..31, column quad q4 = 0..7) streams float4s
+  const int q4 = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int cq = c0 + 4 * q4;
+  int m[4] = {0, 0, 0, 0};
+  unsigned long long sm[4] = {0, 0, 0, 0};
+  if (cq < n) {
+#pragma unroll 4
+    for (int k = ty; k < n; k += 32) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(R + (size_t)k * n + cq));
+      const float x[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float v = k == cq + u ? 0.f : fabsf(x[u]);
+        m[u] = max(m[u], __float_as_int(v));
+        sm[u] += exp_pack(v);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    pm[ty][4 * q4 + u] = m[u];
+    ps[ty][4 * q4 + u] = sm[u];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int cl = threadIdx.x, c = c0 + cl;
+    int mm = 0;
+    unsigned long long ss = 0;
+    for (int w = 0; w < 32; ++w) {
+      mm = max(mm, pm[w][cl]);
+      ss += ps[w][cl];
+    }
+    if (c < n) {
+      b.ec[(size_t)slot * n + c] = mm;
+      b.cc[(size_t)slot * n + c] = ss;
+    }
+    pex[cl] = exp_of(__int_as_float(mm));
+  }
+  __syncthreads();
+  // pass 2: 32 x 32 tiles, one float4 per thread in, transposed slices out
+  const size_t plane = (size_t)n * b.np;
+  int8_t* bs = b.bs + (size_t)slot * NSL * plane;
+  const int ci = threadIdx.x / 8, q = threadIdx.x % 8;
+  auto ld = [&](int k) {  // this thread's float4 of tile row k (zero outside)
+    return (cq < n && k < n) ? __ldg(reinterpret_cast<const float4*>(R + (size_t)k * n + cq))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 nxt = ld(ty);  // software pipelined: the next tile's load is in flight while this one is sliced
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    {
+      const int k = k0 + ty;
+      const float4 a = nxt;
+      if (k0 + 32 < n) nxt = ld(k + 32);
+      const float x[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = k == cq + u ? 0.f : x[u];
+    }
+    __syncthreads();
+    const int cc = c0 + ci, k = k0 + 4 * q;
+    if (cc < n && k < n) {
+      int8_t sl[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) slice4(tile[4 * q + u][ci], pex[ci], sl[u]);
+#pragma unroll
+      for (int jj = 0; jj < NSL; ++jj)
+        *reinterpret_cast<uint32_t*>(bs + jj * plane + (size_t)cc * b.np + k) = pack_plane(sl, jj);
+    }
+    __syncthreads();
+  }
+}
+// Units of the first *dcount slots: per slot n / 8 row units, then n / 32 column strips.
+__global__ void __launch_bounds__(256, EXPMB_I8_PREP_MINB) k_i8_prep(GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs b,
+                                                 const int* __restrict__ dcount, int hcount) {
+  const int cnt = dcount ? *dcount : hcount;
+  const int n = g.n;
+  const int ru = (n + 7) / 8, cu = (n + 31) / 32, per_slot = ru + cu;
+  const long long total = (long long)cnt * per_slot;
+  int cur = -1;
+  bool valid = false;
+  I8Ops ops{};
+  for (long long w = blockIdx.x; w < total; w += gridDim.x) {
+    const int slot = (int)(w / per_slot), u = (int)(w - (long long)slot * per_slot);
+    if (slot != cur) {
+      cur = slot;
+      valid = i8_slot_ops(g, stage, list, slot, ops);
+    }
+    if (!valid) continue;
+    if (u < ru) {
+      const int r = 8 * u + (threadIdx.x >> 5);
+      if (r < n) i8_prep_rows(g, ops.L, b, slot, r);
+    } else {
+      __syncthreads();  // the column strip's shared arrays of the previous unit
+      i8_prep_cols(g, ops.R, b, slot, 32 * (u - ru));
+    }
+  }
+}
+
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"

@@ -78,3 +78,20 @@ def test_i8_default_on_for_large_dense(monkeypatch):
     rng = np.random.default_rng(9)
     W = np.stack([rng.standard_normal((n, n)) * (t / n ** 0.5) for t in (1.0, 20.0)]).astype(np.float32)
     print(f"n=1024 default worst {_check(W, 2.0 ** -24):.2e}")
+
+
+@pytest.mark.parametrize("n", [512, 528])
+def test_i8_variants_bit_identical(i8_on, monkeypatch, n):
+    """The fused prep pass (k_i8_prep) and the 2-CTA multicast stage compute the
+    same slices, scales and integer sums as the round-1 stats / slice kernels
+    and the one-CTA stage: e^W must agree bit for bit (528: an odd number of
+    64-column blocks, so the last cluster has a pad CTA)."""
+    rng = np.random.default_rng(n + 1)
+    W = torch.as_tensor((rng.standard_normal((3, n, n)) * (3.0 / n ** 0.5)).astype(np.float32), device="cuda")
+    outs = []
+    for prep, mc in (("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")):
+        monkeypatch.setenv("EXPMB_I8_PREP", prep)
+        monkeypatch.setenv("EXPMB_I8_MC", mc)
+        outs.append(X.expm(W, 2.0 ** -24).value.clone())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])

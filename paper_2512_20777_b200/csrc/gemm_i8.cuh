@@ -43,21 +43,33 @@
 namespace expmb {
 namespace i8 {
 
-// k-tiles of 64 bytes with the 64B swizzle: a stage (4 L + 4 R slices) is
-// 48 KB, so two stages per CTA and two CTAs per SM fit (TMA of the next
-// k-tile overlaps this one's MMAs, and one CTA's epilogue the other's MMAs).
+// k-tiles of 64 bytes with the 64B swizzle (TMA of the next k-tile overlaps
+// this one's MMAs).
 #ifndef EXPMB_I8_BK64
 #define EXPMB_I8_BK64 1
 #endif
+// EXPMB_I8_BN: columns per tile.  64: a stage (4 L + 4 R slices) is 48 KB,
+// two stages per CTA, two CTAs per SM (256 TMEM columns each; one CTA's
+// epilogue overlaps the other's MMAs).  128 (default): one CTA per SM owning
+// all 512 TMEM columns (four 128-column level accumulators), 64 KB stages in
+// a three-stage ring, a third less operand traffic per MAC (L2 -> smem and
+// smem -> tensor core), and eight epilogue warps because the epilogue now
+// runs with the MMAs idle.  C5: 259 ms (BN 64) -> 238 ms per step, same bits.
+#ifndef EXPMB_I8_BN
+#define EXPMB_I8_BN 128
+#endif
+#ifndef EXPMB_I8_CW
+#define EXPMB_I8_CW 16
+#endif
 #ifndef EXPMB_I8_STAGES
-#define EXPMB_I8_STAGES (EXPMB_I8_BK64 ? 2 : 1)
+#define EXPMB_I8_STAGES (EXPMB_I8_BK64 ? (EXPMB_I8_BN == 128 ? 3 : 2) : 1)
 #endif
 // EXPMB_I8_CAT: slice i of L against the R slices 0..3-i stacked along N in
 // one MMA (4 MMAs per 32-byte k-step); 0: the ten slice-pair MMAs
 #ifndef EXPMB_I8_CAT
 #define EXPMB_I8_CAT 1
 #endif
-constexpr int BM = 128, BN = 64, BKB = EXPMB_I8_BK64 ? 64 : 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
+constexpr int BM = 128, BN = EXPMB_I8_BN, BKB = EXPMB_I8_BK64 ? 64 : 128, STAGES = EXPMB_I8_STAGES, NSL = 4;
 constexpr bool kSw64 = BKB == 64;
 // UMMA shared-memory descriptor, K-major: 64B swizzle (8-row atoms of 512 B) or 128B (1024 B)
 __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
@@ -74,13 +86,23 @@ __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
   }
 }
 constexpr int A_TILE = BM * BKB;                     // 8 KB (64B swizzle)
-constexpr int B_TILE = BN * BKB;                     // 4 KB
-constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 48 KB
+constexpr int B_TILE = BN * BKB;                     // 4 KB (BN 64)
+constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 48 KB (BN 64), 64 KB (BN 128)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
 constexpr int NTHREADS = 192;                         // w0 TMA, w1 MMA/TMEM, w2..w5 epilogue
+// one-unit-per-CTA stage (k_i8_stage_np): EXPMB_I8_EPI_WARPS epilogue warps,
+// 4 or 8; with 8, warps w and w + 4 share a TMEM lane quarter and split the
+// tile's columns (the BN = 128 form runs its epilogue with the MMAs idle)
+#ifndef EXPMB_I8_EPI_WARPS
+#define EXPMB_I8_EPI_WARPS (EXPMB_I8_BN == 128 ? 8 : 4)
+#endif
+constexpr int EPI_PARTS = EXPMB_I8_EPI_WARPS / 4;
+constexpr int NTHREADS_NP = 64 + 32 * EXPMB_I8_EPI_WARPS;
+static_assert(EPI_PARTS == 1 || EPI_PARTS == 2, "EXPMB_I8_EPI_WARPS is 4 or 8");
 constexpr uint32_t TMEM_COLS = 4 * BN;                // one int32 accumulator per level
 constexpr int kNanExp = -100000;                      // row/column holds NaN/Inf
 // kind::i8: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 64, M = 128
+static_assert(BN == 64 || BN == 128, "EXPMB_I8_BN is 64 or 128");
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
@@ -529,6 +551,9 @@ __device__ __forceinline__ void tmem_ld16i(uint32_t taddr, int (&v)[16]) {
   for (int j = 0; j < 16; ++j) v[j] = (int)r[j];
 }
 
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, int (&v)[16]) { tmem_ld16i(taddr, v); }
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, int (&v)[32]) { tmem_ld32i(taddr, v); }
+
 struct Maps {
   CUtensorMap a, b;
 };
@@ -545,6 +570,23 @@ __device__ __forceinline__ void mma_i8_d(uint32_t tmem_d, uint64_t ad, uint64_t 
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate));
+}
+// The MMAs of one 32-byte k-step: for each L slice i, the stacked R slices
+// 0..3-i in pieces of at most 256 rows (the kind::i8 N limit), piece j0 into
+// the accumulators of levels i+j0 ...  first: the unit's first k-step (the
+// i = 0 MMAs, issued first, initialise every level).
+__device__ __forceinline__ void issue_kstep(uint32_t tmem, uint64_t ad0, uint64_t bd0, int k, bool first) {
+  constexpr int PER = 256 / BN;  // R slices per MMA
+#pragma unroll
+  for (int i = 0; i < NSL; ++i) {
+    const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
+#pragma unroll
+    for (int j0 = 0; j0 < NSL - i; j0 += PER) {
+      const int nr = (NSL - i - j0 < PER ? NSL - i - j0 : PER) * BN;
+      const uint64_t bd = bd0 + (uint64_t)((j0 * B_TILE + k * 32) >> 4);
+      mma_i8_d(tmem + (uint32_t)((i + j0) * BN), a, bd, idesc_n(nr), (first && i == 0) ? 0u : 1u);
+    }
+  }
 }
 
 // Persistent, warp-specialised int8-slice GEMM stage.  The grid walks the work
@@ -652,13 +694,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
 #pragma unroll
         for (int k = 0; k < BKB / 32; ++k) {
 #if EXPMB_I8_CAT
-#pragma unroll
-          for (int i = 0; i < NSL; ++i) {
-            const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
-            const uint64_t bd = bd0 + (uint64_t)((k * 32) >> 4);
-            // i = 0 covers every level: its first MMA of the unit initialises them all
-            mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
-          }
+          issue_kstep(tmem, ad0, bd0, k, kt == 0 && k == 0);
 #else
 #pragma unroll
           for (int lv = 0; lv < 4; ++lv) {
@@ -895,7 +931,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // SM operand stream (768 MB per 2048^2 product at 128 x 64 tiles); sharing
 // the L panel cuts it to 512 MB.
 template <bool MC>
-__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
+__global__ void __launch_bounds__(NTHREADS_NP, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
 k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs bf,
               const int* __restrict__ dcount) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -976,12 +1012,7 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
       const uint64_t ad0 = kdesc(base), bd0 = kdesc(base + NSL * A_TILE);
 #pragma unroll
       for (int k = 0; k < BKB / 32; ++k) {
-#pragma unroll
-        for (int i = 0; i < NSL; ++i) {
-          const uint64_t a = ad0 + (uint64_t)((i * A_TILE + k * 32) >> 4);
-          const uint64_t bd = bd0 + (uint64_t)((k * 32) >> 4);
-          mma_i8_d(tmem + (uint32_t)(i * BN), a, bd, idesc_n((NSL - i) * BN), (kt > 0 || k > 0 || i > 0) ? 1u : 0u);
-        }
+        issue_kstep(tmem, ad0, bd0, k, kt == 0 && k == 0);
       }
       if constexpr (MC) mma_commit_mc(&empty_bar[st], (uint16_t)3);
       else tc::mma_commit(&empty_bar[st]);
@@ -990,9 +1021,12 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     // 16-column chunks keep the live arrays small enough for 2 CTAs/SM
-    // without spills.
-    constexpr int CW = 16;
+    // without spills (EXPMB_I8_CW: 32 for the one-CTA-per-SM BN = 128 form).
+    constexpr int CW = EXPMB_I8_CW;
+    constexpr int CPART = BN / EPI_PARTS;  // columns per epilogue warp
+    static_assert(CPART % CW == 0, "chunk width");
     const int q = warp & 3;
+    const int hh = (warp - 2) >> 2;  // column part of this warp
     const int rl = q * 32 + lane;
     const int r = m0 + rl;
     const bool rowok = r < n;
@@ -1022,22 +1056,23 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
       }                                                                                        \
     }                                                                                          \
   } while (0)
-    I8_LOAD_ROWS(n0);
+    I8_LOAD_ROWS(n0 + hh * CPART);
     const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
     const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
     const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
     tc::mbar_wait(&tmem_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    double* red = reinterpret_cast<double*>(sm);  // the smem ring is idle now
+    double* red = reinterpret_cast<double*>(sm) + hh * (CW * BM);  // the smem ring is idle now
 #pragma unroll 1
-    for (int cb = 0; cb < BN / CW; ++cb) {
+    for (int cb = 0; cb < CPART / CW; ++cb) {
       int a0[CW], a1[CW], a2[CW], a3[CW];
-      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
-      tmem_ld16i(ta, a0);
-      tmem_ld16i(ta + BN, a1);
-      tmem_ld16i(ta + 2 * BN, a2);
-      tmem_ld16i(ta + 3 * BN, a3);
-      const int c0 = n0 + cb * CW;
+      const int cl0 = hh * CPART + cb * CW;  // first column of the chunk within the tile
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cl0;
+      tmem_ldw(ta, a0);
+      tmem_ldw(ta + BN, a1);
+      tmem_ldw(ta + 2 * BN, a2);
+      tmem_ldw(ta + 3 * BN, a3);
+      const int c0 = n0 + cl0;
       const bool full = rowok && c0 + CW <= n;
       if (cb > 0) I8_LOAD_ROWS(c0);
       float o0[CW];
@@ -1048,8 +1083,8 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
         // single int -> binary64 conversion (the conversion unit was the hot pipe)
         const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
                             (long long)a3[j];
-        double y = (double)T * rs21 * cs_sh[cb * CW + j];
-        const double dr = (double)dr_sh[cb * CW + j];
+        double y = (double)T * rs21 * cs_sh[cl0 + j];
+        const double dr = (double)dr_sh[cl0 + j];
         y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
         o0[j] = e.alpha * (float)y;
       }
@@ -1130,13 +1165,13 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
         // deterministic column abs-sums of this 128-row tile (select.py:193)
 #pragma unroll
         for (int j = 0; j < CW; ++j) red[j * BM + rl] = rowok ? fabs((double)o0[j]) : 0.0;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + hh) : "memory");
         if (rl < CW && c0 + rl < n) {
           double a = 0.0;
           for (int rr = 0; rr < BM; ++rr) a += red[rl * BM + rr];
           g.part[((size_t)z * g.tiles_m + blockIdx.y) * n + c0 + rl] = a;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + hh) : "memory");
       }
     }
 #undef I8_LOAD_ROWS

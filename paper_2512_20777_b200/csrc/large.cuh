@@ -388,7 +388,7 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     if (mc) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3((unsigned)((tn + 1) & ~1), (unsigned)tm, (unsigned)count);  // whole pairs
-      cfg.blockDim = dim3(i8::NTHREADS);
+      cfg.blockDim = dim3(i8::NTHREADS_NP);
       cfg.dynamicSmemBytes = i8::SMEM_BYTES;
       cfg.stream = st;
       cudaLaunchAttribute at[1];
@@ -400,7 +400,7 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
       cfg.numAttrs = 1;
       if (cudaLaunchKernelEx(&cfg, i8::k_i8_stage_np<true>, maps, g, stage, list, b, dcount) != cudaSuccess) return 1;
     } else {
-      i8::k_i8_stage_np<false><<<dim3(tn, tm, count), i8::NTHREADS, i8::SMEM_BYTES, st>>>(maps, g, stage, list, b,
+      i8::k_i8_stage_np<false><<<dim3(tn, tm, count), i8::NTHREADS_NP, i8::SMEM_BYTES, st>>>(maps, g, stage, list, b,
                                                                                         dcount);
     }
   }

@@ -40,8 +40,17 @@
 namespace expmb {
 namespace w16 {
 
+// EXPMB_W16_DYN (opt-in, A/B): one 16-warp CTA per SM owns a contiguous
+// range of the batch and its warps claim matrices from a shared-memory
+// cursor, up to Q at a time and fewer near the end of the range (guided
+// self-scheduling).  Measured slower than the static per-warp ranges (62.2
+// vs 59.3 us on C2: the short batches at the end of a range lose the
+// phase-1 pairing and pay a selector pass each), so the default is 0.
+#ifndef EXPMB_W16_DYN
+#define EXPMB_W16_DYN 0
+#endif
 #ifndef EXPMB_W16_WARPS
-#define EXPMB_W16_WARPS 8
+#define EXPMB_W16_WARPS (EXPMB_W16_DYN ? 16 : 8)
 #endif
 constexpr int WARPS = EXPMB_W16_WARPS;   // warps per CTA
 constexpr int NT = 32 * WARPS;
@@ -107,8 +116,21 @@ __device__ __forceinline__ void load_w(const float* slot, int g, int t, float (&
     }
 }
 
+// EXPMB_W16_OPAQUE: the left operand's TF32 mask comes from constant memory.
+// With the literal mask ptxas forwards the unmasked register to the HMMA (the
+// tensor core ignores the low 13 bits) and then needs four moves per k-step
+// to line the raw values up in fragment order; an opaque mask makes the LOP3
+// results themselves the fragment (ncu: 62 moves per matrix before).
+#ifndef EXPMB_W16_OPAQUE
+#define EXPMB_W16_OPAQUE 1
+#endif
+__constant__ uint32_t kTf32Mask = 0xffffe000u;
 __device__ __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
+#if EXPMB_W16_OPAQUE
+  const uint32_t u = __float_as_uint(x) & kTf32Mask;
+#else
   const uint32_t u = __float_as_uint(x) & 0xffffe000u;
+#endif
   hi = u;
   lo = __float_as_uint(x - __uint_as_float(u));
 }
@@ -207,9 +229,11 @@ __device__ __forceinline__ void product_rr(const float (&L)[8], const float (&R)
 // partial sums a lane carries, so the 8 partials (4 columns x 2 matrices)
 // finish as one full column sum per lane, then a 16-lane max.  Column sums of
 // non-negative floats compare as integers; NaN (0x7fffffff) orders above Inf,
-// so a NaN anywhere propagates.  Returns ||X||_1 on lanes 0-15 and ||Y||_1 on
-// lanes 16-31.
-__device__ __forceinline__ float norms2(const float (&x)[8], const float (&y)[8], int lane) {
+// so a NaN anywhere propagates.  nx = ||X||_1, ny = ||Y||_1 on every lane.
+#ifndef EXPMB_W16_REDUX
+#define EXPMB_W16_REDUX 1
+#endif
+__device__ __forceinline__ void norms2(const float (&x)[8], const float (&y)[8], int lane, float& nx, float& ny) {
   float c[8];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -238,10 +262,21 @@ __device__ __forceinline__ float norms2(const float (&x)[8], const float (&y)[8]
     const float keep = b2 ? e[1] : e[0], send = b2 ? e[0] : e[1];
     f = keep + __shfl_xor_sync(0xffffffffu, send, 4);
   }
+#if EXPMB_W16_REDUX
+  // two warp-wide integer max reductions (REDUX) instead of a 4-level
+  // shuffle butterfly per half; the result is warp-uniform
+  const unsigned m = __float_as_uint(f);
+  nx = __uint_as_float(__reduce_max_sync(0xffffffffu, b4 ? 0u : m));
+  ny = __uint_as_float(__reduce_max_sync(0xffffffffu, b4 ? m : 0u));
+#else
   int m = __float_as_int(f);
 #pragma unroll
   for (int off = 1; off <= 8; off <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-  return __int_as_float(m);
+  const float nv = __int_as_float(m);
+  const float other = __shfl_xor_sync(0xffffffffu, nv, 16);
+  nx = b4 ? other : nv;
+  ny = b4 ? nv : other;
+#endif
 }
 
 // pairwise elementwise helpers on an 8-entry tile (column pairs (2p, 2p+1))
@@ -311,12 +346,24 @@ __device__ __forceinline__ void eval_t8_t15(const float (&B)[8], const float (&A
 }
 
 template <int Q, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
+__global__ void __launch_bounds__(NT, (MINB * 8 / WARPS > 0 ? MINB * 8 / WARPS : 1))
 expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batch, double log_eps, PlanOut po) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   WarpSmem<Q>& S = reinterpret_cast<WarpSmem<Q>*>(smem_raw)[warp];
+#if EXPMB_W16_DYN
+  // the CTA owns [clo, chi); warp w starts on [clo + w Q, +Q) and claims the
+  // rest from cta_next (an offset into the range)
+  __shared__ int cta_next;
+  const int64_t clo = batch * blockIdx.x / gridDim.x, chi = batch * (blockIdx.x + 1) / gridDim.x;
+  const int cn = (int)(chi - clo);
+  if (threadIdx.x == 0) cta_next = min(cn, WARPS * Q);
+  __syncthreads();
+  const int64_t lo = clo + (int64_t)warp * Q;
+  const int64_t hi = min(chi, lo + Q);  // end of the batch being processed / staged
+  if (lo >= hi) return;
+#else
   // each warp owns a contiguous range of floor/ceil(batch / warps) matrices,
   // taken Q at a time (round-robin whole batches left a tail of up to one
   // batch per warp: 7 vs 6 batches at C2's 65536 / 2368 warps)
@@ -324,6 +371,7 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t lo = batch * gw / nwarps, hi = batch * (gw + 1) / nwarps;
   if (lo >= hi) return;
+#endif
   const double rung0_thr = rung0_threshold(log_eps);
   const float2 dg = make_float2(g == 2 * t ? 1.f : 0.f, g == 2 * t + 1 ? 1.f : 0.f);
   float* lane_a2 = &S.a2[0][0] + 8 * lane;
@@ -331,10 +379,33 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
 
 #pragma unroll
   for (int j = 0; j < Q; ++j) stage(S.w[j], W, base + j, hi, lane);
+#if EXPMB_W16_DYN
+  int nq = (int)(hi - base);
+#endif
 
   while (true) {
+#if EXPMB_W16_DYN
+    // claim the next batch now; its matrices are staged during phase 3
+    int64_t nbase;
+    int nnq;
+    {
+      int st = 0, sz = 0;
+      if (lane == 0) {
+        const int rem = cn - *(volatile int*)&cta_next;
+        sz = min(Q, max(1, rem / WARPS));
+        st = atomicAdd(&cta_next, sz);
+        sz = max(0, min(sz, cn - st));
+      }
+      st = __shfl_sync(0xffffffffu, st, 0);
+      nnq = __shfl_sync(0xffffffffu, sz, 0);
+      nbase = clo + st;
+    }
+    const int64_t nhi = nbase + nnq;
+#else
     const int64_t nbase = base + Q;
     const int nq = (int)min((int64_t)Q, hi - base);  // matrices in this batch (warp-uniform)
+    const int64_t nhi = hi;
+#endif
     // ---- phase 1: W^2 and both norms per matrix --------------------------------
     // (slot j's copy was issued while the previous batch's matrix j finished;
     // by now every one has landed, so one wait for all of them)
@@ -342,11 +413,11 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
     __syncwarp();
     float my_n1 = 0.f, my_n2 = 0.f;
     auto finish1 = [&](int j, const float (&w)[8], const float (&a)[8]) {
-      const float nv = norms2(w, a, lane);
-      const float other = __shfl_xor_sync(0xffffffffu, nv, 16);
+      float nx, ny;
+      norms2(w, a, lane, nx, ny);
       if (lane == j) {
-        my_n1 = nv;
-        my_n2 = other;
+        my_n1 = nx;
+        my_n2 = ny;
       }
       *reinterpret_cast<float4*>(lane_a2 + 256 * j) = make_float4(a[0], a[1], a[2], a[3]);
       *reinterpret_cast<float4*>(lane_a2 + 256 * j + 4) = make_float4(a[4], a[5], a[6], a[7]);
@@ -458,7 +529,7 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
       float B[8];
       if (j < nq && !po.plan_only) load_w(S.w[j], g, t, B);
       __syncwarp();  // every lane has read slot j: refill it with the next batch's matrix j
-      stage(S.w[j], W, nbase + j, hi, lane);
+      stage(S.w[j], W, nbase + j, nhi, lane);
       if (j >= nq || po.plan_only) continue;
       const int m = pk >> 8, s = pk & 0xff;
       float P[8];
@@ -509,7 +580,12 @@ expm_w16_kernel(const float* __restrict__ W, float* __restrict__ X, int64_t batc
                  make_float2(P[4 * nt + 2 * h], P[4 * nt + 2 * h + 1]));
     }
     if (po.nonfinite && lane < nq) po.nonfinite[base + lane] = (uint8_t)my_bad;
+#if EXPMB_W16_DYN
+    if (nnq == 0) break;
+    nq = nnq;
+#else
     if (nbase >= hi) break;
+#endif
     base = nbase;
   }
   cp_wait<0>();

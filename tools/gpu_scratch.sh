@@ -1,10 +1,10 @@
 #!/bin/bash
+# scratch A/B: w16 variants (a = round-2 baseline, b = opaque+redux static, c = redux+dyn, default = all)
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_i8.py -m gpu -q -x -rf -p no:cacheprovider > gpurun_out/s15_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s15_pytest.log
-if grep -q "rc=0" gpurun_out/s15_pytest.log; then
-for rep in 1 2; do
-timeout 300 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-per-config > gpurun_out/s15_m3_$rep.json 2>gpurun_out/s15_m3_$rep.err
-EXPMB_LIB=libexpmb_p4.so timeout 300 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-per-config > gpurun_out/s15_m4_$rep.json 2>gpurun_out/s15_m4_$rep.err
+timeout 600 python -m pytest tests/test_gpu_w16.py tests/test_gpu_select.py -m gpu -q -x -rf -p no:cacheprovider > gpurun_out/ab_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ab_pytest.log
+for rep in 1 2 3; do
+for lib in libexpmb_a.so libexpmb_b.so libexpmb_c.so libexpmb.so; do
+EXPMB_LIB=$lib timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/ab_${lib}_$rep.json 2>gpurun_out/ab_${lib}_$rep.err
 done
-fi
+done
 echo done

@@ -89,7 +89,6 @@ constexpr int A_TILE = BM * BKB;                     // 8 KB (64B swizzle)
 constexpr int B_TILE = BN * BKB;                     // 4 KB (BN 64)
 constexpr int STAGE_BYTES = NSL * (A_TILE + B_TILE);  // 48 KB (BN 64), 64 KB (BN 128)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
-constexpr int NTHREADS = 192;                         // w0 TMA, w1 MMA/TMEM, w2..w5 epilogue
 // one-unit-per-CTA stage (k_i8_stage_np): EXPMB_I8_EPI_WARPS epilogue warps,
 // 4 or 8; with 8, warps w and w + 4 share a TMEM lane quarter and split the
 // tile's columns (the BN = 128 form runs its epilogue with the MMAs idle)
@@ -137,6 +136,51 @@ __device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
   }
 }
 
+// The same four digits for four elements at once, as the four plane words
+// (element u in byte u), in about a third of the instructions: the scale is a
+// precomputed power of two (slice_scale), each rint is a magic-number add
+// whose low mantissa byte is the digit (1.5 2^(23 - 7i) puts the mantissa's
+// last place at 2^(-7i), round-to-nearest-even like rintf), and the residual
+// stays unscaled.  Bit-identical to slice4 (tests: EXPMB_I8_PREP=0 runs
+// slice4 in k_i8_slice).
+__device__ __forceinline__ bool slice_scale(int e, float& sc) {  // false: use slice4 (NaN/Inf row, extreme exponent)
+  sc = 0.f;
+  if (e == kNanExp || e < -100 || e > 100) return false;
+  sc = __int_as_float((6 - e + 127) << 23);  // 2^(6 - e)
+  return true;
+}
+__device__ __forceinline__ void slice4x4(const float (&x)[4], float sc, uint32_t (&w)[4]) {
+  float y[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) y[u] = x[u] * sc;  // |y| < 64, exact
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float M = i == 0 ? 12582912.f : i == 1 ? 98304.f : i == 2 ? 768.f : 6.f;
+    uint32_t t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float tu = y[u] + M;
+      t[u] = __float_as_uint(tu);
+      y[u] -= tu - M;  // exact
+    }
+    w[i] = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
+  }
+}
+// four elements -> plane words, by whichever path the row / column scale allows
+__device__ __forceinline__ void slice_quad(const float (&x)[4], int e, bool fast, float sc, uint32_t (&w)[4]) {
+  if (fast) {
+    slice4x4(x, sc, w);
+  } else {
+    int8_t sl[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) slice4(x[u], e, sl[u]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = (uint32_t)(uint8_t)sl[0][j] | ((uint32_t)(uint8_t)sl[1][j] << 8) | ((uint32_t)(uint8_t)sl[2][j] << 16) |
+             ((uint32_t)(uint8_t)sl[3][j] << 24);
+  }
+}
+
 // One pass over 32x32 tiles: row maxima of |L| and column maxima of |R|
 // (diagonals excluded: they are handled exactly in the epilogue) as the bit
 // patterns of non-negative floats, which order like the values (NaN above
@@ -146,6 +190,23 @@ __device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
 constexpr int kExpBias = 200;
 __device__ __forceinline__ unsigned long long exp_pack(float a) {
   return a > 0.f && a < INFINITY ? ((unsigned long long)(ilogbf(a) + kExpBias) << 20) | 1ull : 0ull;
+}
+// The same sums in two 32-bit accumulators (the streaming prep pass): esum
+// collects the biased exponents (ilogb + 127) of the finite nonzero entries,
+// cnt their number; exp_pack_sum gives the sum of exp_pack over them.
+__device__ __forceinline__ void exp_acc(float v, int& esum, int& cnt) {  // v >= 0 or NaN
+  const uint32_t bits = __float_as_uint(v);
+  const uint32_t e8 = bits >> 23;
+  if (e8 - 1u < 254u) {  // normal, finite
+    esum += (int)e8;
+    ++cnt;
+  } else if (e8 == 0u && bits != 0u) {  // subnormal: ilogb = 31 - clz - 149
+    esum += 31 - __clz(bits) - 149 + 127;
+    ++cnt;
+  }
+}
+__device__ __forceinline__ unsigned long long exp_pack_sum(long long esum, long long cnt) {
+  return ((unsigned long long)(esum + (long long)(kExpBias - 127) * cnt) << 20) | (unsigned long long)cnt;
 }
 // The operands of a slot's product (make_epi once per slot, not per tile).
 struct I8Ops {
@@ -260,6 +321,7 @@ __device__ __forceinline__ bool flat_ok(int maxbits, unsigned long long pk) {
   const long long cnt = (long long)(pk & 0xfffffull);
   const long long esum = (long long)(pk >> 20) - (long long)kExpBias * cnt;
   const int emax = ilogbf(__int_as_float(maxbits));
+  if (emax < -60 || emax > 60) return false;        // keeps the epilogue's fp32 power-of-two scales normal
   return cnt > 0 && (long long)emax * cnt - esum <= (long long)kFlatBits * cnt;
 }
 __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, const int* __restrict__ list,
@@ -369,16 +431,11 @@ __global__ void __launch_bounds__(256, 8) k_i8_slice(GemmCtx<float> g, int stage
 #ifndef EXPMB_I8_PREP_MINB
 #define EXPMB_I8_PREP_MINB 4
 #endif
-__device__ __forceinline__ uint32_t pack_plane(const int8_t (&v)[4][4], int j) {
-  return (uint32_t)(uint8_t)v[0][j] | ((uint32_t)(uint8_t)v[1][j] << 8) | ((uint32_t)(uint8_t)v[2][j] << 16) |
-         ((uint32_t)(uint8_t)v[3][j] << 24);
-}
 __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const float* __restrict__ L, const Bufs& b,
                                              int slot, int r) {
   const int n = g.n, lane = threadIdx.x & 31;
   const float* row = L + (size_t)r * n;
-  int m = 0;
-  unsigned long long sm = 0;
+  int m = 0, esum = 0, ecnt = 0;
 #pragma unroll 4
   for (int c = 4 * lane; c < n; c += 128) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
@@ -387,30 +444,35 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
     for (int u = 0; u < 4; ++u) {
       const float v = c + u == r ? 0.f : fabsf(x[u]);
       m = max(m, __float_as_int(v));
-      sm += exp_pack(v);
+      exp_acc(v, esum, ecnt);
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    esum += __shfl_xor_sync(0xffffffffu, esum, o);
+    ecnt += __shfl_xor_sync(0xffffffffu, ecnt, o);
   }
   if (lane == 0) {
     b.er[(size_t)slot * n + r] = m;
-    b.rc[(size_t)slot * n + r] = sm;
+    b.rc[(size_t)slot * n + r] = exp_pack_sum(esum, ecnt);
   }
   const int ex = exp_of(__int_as_float(m));
+  float sc;
+  const bool fast = slice_scale(ex, sc);
   const size_t plane = (size_t)n * b.np;
   int8_t* as = b.as + (size_t)slot * NSL * plane + (size_t)r * b.np;
 #pragma unroll 4
   for (int c = 4 * lane; c < n; c += 128) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
-    const float x[4] = {a.x, a.y, a.z, a.w};
-    int8_t sl[4][4];
+    float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) slice4(c + u == r ? 0.f : x[u], ex, sl[u]);
+    for (int u = 0; u < 4; ++u)
+      if (c + u == r) x[u] = 0.f;
+    uint32_t w[4];
+    slice_quad(x, ex, fast, sc, w);
 #pragma unroll
-    for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + c) = pack_plane(sl, j);
+    for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + c) = w[j];
   }
 }
 __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const float* __restrict__ R, const Bufs& b,
@@ -418,13 +480,13 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
   __shared__ int pm[32][33];
   __shared__ unsigned long long ps[32][33];
   __shared__ int pex[32];
+  __shared__ float psc[32];
   __shared__ float tile[32][33];
   const int n = g.n;  // a multiple of 16 on this path: a float4 group is all in or all out
   // pass 1: thread (row phase ty = 0..31, column quad q4 = 0..7) streams float4s
   const int q4 = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int cq = c0 + 4 * q4;
-  int m[4] = {0, 0, 0, 0};
-  unsigned long long sm[4] = {0, 0, 0, 0};
+  int m[4] = {0, 0, 0, 0}, esum[4] = {0, 0, 0, 0}, ecnt[4] = {0, 0, 0, 0};
   if (cq < n) {
 #pragma unroll 4
     for (int k = ty; k < n; k += 32) {
@@ -434,14 +496,14 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
       for (int u = 0; u < 4; ++u) {
         const float v = k == cq + u ? 0.f : fabsf(x[u]);
         m[u] = max(m[u], __float_as_int(v));
-        sm[u] += exp_pack(v);
+        exp_acc(v, esum[u], ecnt[u]);
       }
     }
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     pm[ty][4 * q4 + u] = m[u];
-    ps[ty][4 * q4 + u] = sm[u];
+    ps[ty][4 * q4 + u] = exp_pack_sum(esum[u], ecnt[u]);
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -457,6 +519,8 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
       b.cc[(size_t)slot * n + c] = ss;
     }
     pex[cl] = exp_of(__int_as_float(mm));
+    float sc;
+    psc[cl] = slice_scale(pex[cl], sc) ? sc : 0.f;  // 0: slice4 path
   }
   __syncthreads();
   // pass 2: 32 x 32 tiles, one float4 per thread in, transposed slices out
@@ -467,27 +531,42 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
     return (cq < n && k < n) ? __ldg(reinterpret_cast<const float4*>(R + (size_t)k * n + cq))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  float4 nxt = ld(ty);  // software pipelined: the next tile's load is in flight while this one is sliced
-  for (int k0 = 0; k0 < n; k0 += 32) {
-    {
-      const int k = k0 + ty;
-      const float4 a = nxt;
-      if (k0 + 32 < n) nxt = ld(k + 32);
-      const float x[4] = {a.x, a.y, a.z, a.w};
+  // software pipelined in groups of four tiles: the next group's four loads
+  // per thread are in flight while this group is sliced (one load in flight
+  // per thread left the strip latency-bound: 4 KB per CTA per DRAM round trip)
+  float4 nxt[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = k == cq + u ? 0.f : x[u];
+  for (int t = 0; t < 4; ++t) nxt[t] = ld(32 * t + ty);
+  for (int k0 = 0; k0 < n; k0 += 128) {
+    float4 cur[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cur[t] = nxt[t];
+    if (k0 + 128 < n) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) nxt[t] = ld(k0 + 128 + 32 * t + ty);
     }
-    __syncthreads();
-    const int cc = c0 + ci, k = k0 + 4 * q;
-    if (cc < n && k < n) {
-      int8_t sl[4][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) slice4(tile[4 * q + u][ci], pex[ci], sl[u]);
+    for (int t = 0; t < 4; ++t) {
+      const int kt = k0 + 32 * t;
+      if (kt >= n) break;  // uniform
+      {
+        const int k = kt + ty;
+        const float x[4] = {cur[t].x, cur[t].y, cur[t].z, cur[t].w};
 #pragma unroll
-      for (int jj = 0; jj < NSL; ++jj)
-        *reinterpret_cast<uint32_t*>(bs + jj * plane + (size_t)cc * b.np + k) = pack_plane(sl, jj);
+        for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = k == cq + u ? 0.f : x[u];
+      }
+      __syncthreads();
+      const int cc = c0 + ci, k = kt + 4 * q;
+      if (cc < n && k < n) {
+        const float x[4] = {tile[4 * q][ci], tile[4 * q + 1][ci], tile[4 * q + 2][ci], tile[4 * q + 3][ci]};
+        const float sc = psc[ci];
+        uint32_t w[4];
+        slice_quad(x, pex[ci], sc != 0.f, sc, w);
+#pragma unroll
+        for (int jj = 0; jj < NSL; ++jj) *reinterpret_cast<uint32_t*>(bs + jj * plane + (size_t)cc * b.np + k) = w[jj];
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 // Units of the first *dcount slots: per slot n / 8 row units, then n / 32 column strips.
@@ -589,28 +668,54 @@ __device__ __forceinline__ void issue_kstep(uint32_t tmem, uint64_t ad0, uint64_
   }
 }
 
-// Persistent, warp-specialised int8-slice GEMM stage.  The grid walks the work
-// units (slot, 128-row block, 64-column block) of the first *dcount slots;
-// warp 0 streams k-tiles through the TMA ring, warp 1 issues the MMAs into the
-// TMEM level accumulators, warps 2..5 run the fused epilogue.  The producer
-// runs ahead into the next unit while the epilogue drains the current one
-// (tmem_full / tmem_empty barriers hand the accumulators back and forth).
-__global__ void __launch_bounds__(NTHREADS, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
+// tcgen05.ld without the wait: issue the four level loads of a chunk, wait once
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Persistent, warp-specialised int8-slice GEMM stage (the default).  One CTA
+// per SM walks the work units (slot, 128-row block, BN-column block) of the
+// first *dcount slots; warp 0 streams k-tiles through the TMA ring, warp 1
+// issues the MMAs into the TMEM level accumulators, the epilogue warps drain
+// them.  The four level accumulators fill all 512 TMEM columns at BN = 128,
+// so there is no second accumulator set to compute into while the first is
+// drained; instead the epilogue is split:
+//   drain:  TMEM -> registers, the level sum as one exact 64-bit integer,
+//           one rounding to fp32 and the exact power-of-two row / column
+//           scales (64 values per thread), then TMEM goes back to the MMA
+//           warp (~1.5 us per unit);
+//   finish: the diagonal terms, the stage's fused linear combination, the
+//           column-norm partials and all global traffic, overlapped with the
+//           next unit's MMAs.
+// The one-unit-per-CTA form (k_i8_stage_np) spent a third of each unit in its
+// epilogue with the tensor pipe idle (ncu: IMMA 55% active, 14 of 40 us).
+// Rounding: y0 = fl(T) 2^(er + ec - 33) is the correctly rounded product of
+// the off-diagonal parts; the diagonal terms are added with two fp32 FMAs
+// (k_i8_stage_np sums them in binary64 and rounds once), so results differ
+// from that form in the last place.  k_i8_route keeps every row / column
+// exponent within +-60, so the two scale factors and their products with
+// fl(T) < 2^49 stay in the normal range whenever the result does.
+__global__ void __launch_bounds__(NTHREADS_NP, (STAGE_BYTES * STAGES <= 100 * 1024 ? 2 : 1))
 k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const int* __restrict__ list, Bufs bf,
            const int* __restrict__ dcount, int hcount) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ double cs_sh[BN];   // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
+  __shared__ float cf_sh[BN];    // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
   __shared__ float dr_sh[BN];    // diagonal of R for this unit's columns
-  __shared__ double red_sh[4][16];  // colnorm partials: one per epilogue warp and chunk column
+  __shared__ double red_sh[EXPMB_I8_EPI_WARPS][16];  // colnorm partials: one per epilogue warp and chunk column
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = g.n;
   const int KT = (n + BKB - 1) / BKB;
   const int cnt = dcount ? *dcount : hcount;
   const int tn = (n + BN - 1) / BN, tm = (n + BM - 1) / BM, tiles = tn * tm;
-  const int total = cnt * tiles;  // < 2^31: slots x (128 x 64) tiles of a chunk
+  const int total = cnt * tiles;  // < 2^31: slots x tiles of a chunk
   if ((int)blockIdx.x >= total) return;  // uniform: no unit for this CTA
 
   if (threadIdx.x == 0) {
@@ -619,7 +724,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       tc::mbar_init(&empty_bar[i], 1);
     }
     tc::mbar_init(&tfull_bar, 1);
-    tc::mbar_init(&tempty_bar, 4);  // one arrival per epilogue warp
+    tc::mbar_init(&tempty_bar, EXPMB_I8_EPI_WARPS);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -636,7 +741,9 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   // every role walks the same unit sequence and skips the same units: the
   // producer and the MMA issuer use the light test (a slot of a stage list
   // always needs its stage; the power stages run on every matrix that asked
-  // for that power), the epilogue builds the full stage program (make_epi)
+  // for that power), the epilogue builds the full stage program (make_epi).
+  // Consecutive units of a CTA's walk are gridDim.x apart, so at any time the
+  // CTAs work on neighbouring tiles of one matrix (operand panels shared in L2).
   const int pw = stage == STAGE_W2 ? 2 : stage == STAGE_W3 ? 3 : stage == STAGE_W4 ? 4 : 0;
   auto unit_light = [&](int w, int& slot, int& bx, int& by) -> bool {
     slot = w / tiles;
@@ -676,7 +783,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       }
     }
   } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer: 4 concatenated-slice MMAs per 32-byte k-step ----------------
+    // ---------------- MMA issuer: the concatenated-slice MMAs of every 32-byte k-step ----------------
     uint32_t it = 0, u = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int slot, bx, by;
@@ -715,12 +822,15 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
     }
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
-    // 16-column chunks keep the live arrays small enough for 2 CTAs/SM
-    // without spills.
-    constexpr int CW = 16;
-    const int q = warp & 3;
+    constexpr int CW = 16;                  // columns per chunk
+    constexpr int CPART = BN / EPI_PARTS;   // columns per epilogue warp
+    constexpr int NCH = CPART / CW;
+    constexpr int ETHREADS = 32 * EXPMB_I8_EPI_WARPS;
+    static_assert(CPART % CW == 0 && CPART <= 64, "the drained tile part lives in registers");
+    const int q = warp & 3;           // TMEM lane quarter of this warp
+    const int hh = (warp - 2) >> 2;   // column part of this warp
     const int rl = q * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int et = threadIdx.x - 64;  // 0 .. ETHREADS - 1
     uint32_t u = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int slot, z, bx, by;
@@ -729,19 +839,19 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       const int m0 = by * BM, n0 = bx * BN;
       const int r = m0 + rl;
       const bool rowok = r < n;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the previous unit's readers of cs_sh / dr_sh are done
+      asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");  // the previous unit's readers of cf_sh / dr_sh are done
       if (et < BN) {
         const int c = n0 + et;
         const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
-        cs_sh[et] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
+        cf_sh[et] = ec == kNanExp ? NAN : scalbnf(1.f, ec - 6);
         dr_sh[et] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");
       // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
       // the int8 GEMM carries Yl Yr (each row / column scaled without its
-      // diagonal, which in the squaring phase dominates), the rest is exact
-      // elementwise work here, all summed in binary64 and rounded once.  The
-      // operand rows of the first chunk are fetched while the MMAs still run.
+      // diagonal, which in the squaring phase dominates), the rest is
+      // elementwise work here.  The operand rows of the first chunk are
+      // fetched while the MMAs still run.
       float lrow[CW], rrow[CW];
 #define I8_LOAD_ROWS(C0)                                                                       \
   do {                                                                                         \
@@ -763,41 +873,50 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       }                                                                                        \
     }                                                                                          \
   } while (0)
-      I8_LOAD_ROWS(n0);
+      I8_LOAD_ROWS(n0 + hh * CPART);
       const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
-      const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
-      const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
+      const float rf = er == kNanExp ? NAN : scalbnf(1.f, er - 6 - 21);  // row scale / 2^21
+      const float dl = rowok ? e.L[(size_t)r * n + r] : 0.f;            // diagonal of L for this row
       tc::mbar_wait(&tfull_bar, u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-      for (int cb = 0; cb < BN / CW; ++cb) {
-        int a0[CW], a1[CW], a2[CW], a3[CW];
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + cb * CW;
-        tmem_ld16i(ta, a0);
-        tmem_ld16i(ta + BN, a1);
-        tmem_ld16i(ta + 2 * BN, a2);
-        tmem_ld16i(ta + 3 * BN, a3);
-        if (cb == BN / CW - 1) {
-          // every accumulator word of this unit is in registers: hand TMEM back
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          __syncwarp();
-          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&tempty_bar)) : "memory");
+      // ---- drain: the unit's accumulators -> y (registers), then TMEM goes back ----
+      float y[CPART];
+#pragma unroll
+      for (int cb = 0; cb < NCH; ++cb) {
+        uint32_t a0[CW], a1[CW], a2[CW], a3[CW];
+        const int cl0 = hh * CPART + cb * CW;  // first column of the chunk within the tile
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)cl0;
+        tmem_ld16_nowait(ta, a0);
+        tmem_ld16_nowait(ta + BN, a1);
+        tmem_ld16_nowait(ta + 2 * BN, a2);
+        tmem_ld16_nowait(ta + 3 * BN, a3);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49),
+          // rounded once to fp32; the scales are powers of two
+          const long long T = ((long long)(int)a0[j] << 21) + ((long long)(int)a1[j] << 14) +
+                              ((long long)(int)a2[j] << 7) + (long long)(int)a3[j];
+          y[cb * CW + j] = __ll2float_rn(T) * rf * cf_sh[cl0 + j];
         }
-        const int c0 = n0 + cb * CW;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&tempty_bar)) : "memory");
+      // ---- finish: overlapped with the next unit's MMAs ----
+#pragma unroll
+      for (int cb = 0; cb < NCH; ++cb) {
+        const int cl0 = hh * CPART + cb * CW;
+        const int c0 = n0 + cl0;
         const bool full = rowok && c0 + CW <= n;
         if (cb > 0) I8_LOAD_ROWS(c0);
         float o0[CW];
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const int c = c0 + j;
-          // the level sum as one exact 64-bit integer (|acc| < 2^27, so < 2^49) and a
-          // single int -> binary64 conversion (the conversion unit was the hot pipe)
-          const long long T = ((long long)a0[j] << 21) + ((long long)a1[j] << 14) + ((long long)a2[j] << 7) +
-                              (long long)a3[j];
-          double y = (double)T * rs21 * cs_sh[cb * CW + j];
-          const double dr = (double)dr_sh[cb * CW + j];
-          y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
-          o0[j] = e.alpha * (float)y;
+          const float dr = dr_sh[cl0 + j];
+          const float v = (c0 + j == r) ? fmaf(dl, dr, y[cb * CW + j])
+                                        : fmaf(dl, rrow[j], fmaf(lrow[j], dr, y[cb * CW + j]));
+          o0[j] = e.alpha * v;
         }
         for (int qq = 0; qq < e.nin; ++qq) {
           const float cq = e.c[0][qq];
@@ -874,20 +993,22 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
         }
         if (e.colnorm) {
           // deterministic column abs-sums of this 128-row tile (select.py:193):
-          // a fixed shuffle tree over each warp's 32 rows, then the 4 warps in order
+          // a fixed shuffle tree over each warp's 32 rows, then the 4 warps of
+          // this column part in lane-quarter order
 #pragma unroll
           for (int j = 0; j < CW; ++j) {
             double v = rowok ? fabs((double)o0[j]) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red_sh[q][j] = v;
+            if (lane == 0) red_sh[hh * 4 + q][j] = v;
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (et < CW && c0 + et < n) {
-            const double a = ((red_sh[0][et] + red_sh[1][et]) + red_sh[2][et]) + red_sh[3][et];
-            g.part[((size_t)z * g.tiles_m + by) * n + c0 + et] = a;
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
+          if (rl < CW && c0 + rl < n) {
+            const double a = ((red_sh[hh * 4][rl] + red_sh[hh * 4 + 1][rl]) + red_sh[hh * 4 + 2][rl]) +
+                             red_sh[hh * 4 + 3][rl];
+            g.part[((size_t)z * g.tiles_m + by) * n + c0 + rl] = a;
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
         }
       }
 #undef I8_LOAD_ROWS

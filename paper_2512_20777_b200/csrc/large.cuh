@@ -371,7 +371,8 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
                                                                                             dcount, count);
   if (chk("slice")) return 1;
   }
-  static const bool persist = getenv("EXPMB_I8_PERSIST") && getenv("EXPMB_I8_PERSIST")[0] == '1';
+  // persistent stage with the split epilogue (default); EXPMB_I8_PERSIST=0: one unit per CTA
+  const bool persist = !(getenv("EXPMB_I8_PERSIST") && getenv("EXPMB_I8_PERSIST")[0] == '0');  // read per call (tests A/B it)
   // 2-CTA clusters sharing the L panel by multicast (EXPMB_I8_MC=0: one CTA per tile)
   const bool mc = !(getenv("EXPMB_I8_MC") && getenv("EXPMB_I8_MC")[0] == '0');
   static bool attr_np = false;
@@ -405,8 +406,8 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     }
   }
   const int64_t units = (int64_t)count * ((n + i8::BN - 1) / i8::BN) * ((n + i8::BM - 1) / i8::BM);
-  if (persist) i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS, i8::SMEM_BYTES, units, &occ_stage,
-                                   i8::STAGE_BYTES * i8::STAGES <= 100 * 1024 ? 2 : 1), i8::NTHREADS,
+  if (persist) i8::k_i8_stage<<<persistent_grid(i8::k_i8_stage, i8::NTHREADS_NP, i8::SMEM_BYTES, units, &occ_stage,
+                                   i8::STAGE_BYTES * i8::STAGES <= 100 * 1024 ? 2 : 1), i8::NTHREADS_NP,
                    i8::SMEM_BYTES, st>>>(maps, g, stage, list, b, dcount, count);
   {
     const cudaError_t le = cudaGetLastError();

@@ -85,13 +85,36 @@ def test_i8_variants_bit_identical(i8_on, monkeypatch, n):
     """The fused prep pass (k_i8_prep) and the 2-CTA multicast stage compute the
     same slices, scales and integer sums as the round-1 stats / slice kernels
     and the one-CTA stage: e^W must agree bit for bit (528: an odd number of
-    64-column blocks, so the last cluster has a pad CTA)."""
+    column blocks, so the last cluster has a pad CTA).  The persistent stage
+    (the default) rounds the int8 part to fp32 before adding the diagonal
+    terms, so it is bit-identical across the prep variants and within a few
+    ulps (normwise) of the one-unit-per-CTA stage."""
     rng = np.random.default_rng(n + 1)
     W = torch.as_tensor((rng.standard_normal((3, n, n)) * (3.0 / n ** 0.5)).astype(np.float32), device="cuda")
     outs = []
+    monkeypatch.setenv("EXPMB_I8_PERSIST", "0")
     for prep, mc in (("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")):
         monkeypatch.setenv("EXPMB_I8_PREP", prep)
         monkeypatch.setenv("EXPMB_I8_MC", mc)
         outs.append(X.expm(W, 2.0 ** -24).value.clone())
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+    monkeypatch.setenv("EXPMB_I8_PERSIST", "1")
+    pers = []
+    for prep in ("1", "0"):
+        monkeypatch.setenv("EXPMB_I8_PREP", prep)
+        pers.append(X.expm(W, 2.0 ** -24).value.clone())
+    assert torch.equal(pers[0], pers[1])
+    d = _rel1(pers[0].double().cpu().numpy(), outs[0].double().cpu().numpy())
+    print(f"n={n} persistent vs one-unit stage: {d.max():.2e}")
+    assert d.max() <= 1e-6
+
+
+def test_i8_persistent_many_units(i8_on, monkeypatch):
+    """More work units than CTAs (8 matrices x 64 tiles at n = 1024 over 148
+    CTAs): every CTA of the persistent stage walks several units, handing the
+    TMEM accumulators back and forth between its MMA and epilogue warps."""
+    n = 1024
+    rng = np.random.default_rng(77)
+    W = np.stack([rng.standard_normal((n, n)) * (t / n ** 0.5) for t in (0.2, 1.0, 3.0, 7.0, 12.0, 20.0, 33.0, 50.0)])
+    print(f"n=1024 x 8 worst {_check(W.astype(np.float32), 2.0 ** -24):.2e}")

@@ -1,10 +1,9 @@
 #!/bin/bash
-# scratch A/B: w16 variants (a = round-2 baseline, b = opaque+redux static, c = redux+dyn, default = all)
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_w16.py tests/test_gpu_select.py -m gpu -q -x -rf -p no:cacheprovider > gpurun_out/ab_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ab_pytest.log
-for rep in 1 2 3; do
-for lib in libexpmb_a.so libexpmb_b.so libexpmb_c.so libexpmb.so; do
-EXPMB_LIB=$lib timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/ab_${lib}_$rep.json 2>gpurun_out/ab_${lib}_$rep.err
-done
+timeout 900 python -m pytest tests/test_gpu_i8.py -m gpu -q -x -rf -p no:cacheprovider --timeout 600 > gpurun_out/ab_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ab_pytest.log
+for rep in 1 2; do
+timeout 300 python bench.py --config C5 --steps 2 --warmup 2 --no-cpu-baseline --no-per-config > gpurun_out/ab_c5_new_$rep.json 2>gpurun_out/ab_c5_new_$rep.err
+EXPMB_I8_PERSIST=0 timeout 300 python bench.py --config C5 --steps 2 --warmup 2 --no-cpu-baseline --no-per-config > gpurun_out/ab_c5_newnp_$rep.json 2>gpurun_out/ab_c5_newnp_$rep.err
+EXPMB_LIB=libexpmb_a.so timeout 300 python bench.py --config C5 --steps 2 --warmup 2 --no-cpu-baseline --no-per-config > gpurun_out/ab_c5_head_$rep.json 2>gpurun_out/ab_c5_head_$rep.err
 done
 echo done

@@ -706,9 +706,19 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base_sh;
+  constexpr int TLD = 20;        // floats per row of a warp's transpose tile (16-byte aligned rows)
   __shared__ float cf_sh[BN];    // 2^(ec - 6) per column (NaN when the column holds NaN/Inf)
-  __shared__ float dr_sh[BN];    // diagonal of R for this unit's columns
+  __shared__ __align__(16) float dr_sh[BN];  // diagonal of R for this unit's columns
+  __shared__ float rf_sh[BM];    // 2^(er - 27) per row
+  __shared__ float dl_sh[BM];    // diagonal of L for this unit's rows
+  __shared__ __align__(16) float xp_sh[EXPMB_I8_EPI_WARPS][32 * TLD];  // per-warp transpose tile of a chunk
   __shared__ double red_sh[EXPMB_I8_EPI_WARPS][16];  // colnorm partials: one per epilogue warp and chunk column
+  // the unit's stage program, read by every epilogue thread with dynamic
+  // indices: shared memory, not a per-thread local-memory copy (the ~28 KB of
+  // L1 left beside the ring is swept by the epilogue's streaming loads)
+  __shared__ float ec_sh[3][4], ed_sh[3];
+  __shared__ float* eout_sh[3];
+  __shared__ const float* ein_sh[4];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = g.n;
@@ -827,56 +837,51 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
     constexpr int NCH = CPART / CW;
     constexpr int ETHREADS = 32 * EXPMB_I8_EPI_WARPS;
     static_assert(CPART % CW == 0 && CPART <= 64, "the drained tile part lives in registers");
+    static_assert(ETHREADS >= BM && ETHREADS >= BN, "one thread per tile row / column sets up the scales");
     const int q = warp & 3;           // TMEM lane quarter of this warp
     const int hh = (warp - 2) >> 2;   // column part of this warp
-    const int rl = q * 32 + lane;
+    const int rl = q * 32 + lane;     // drain: this thread's row of the tile (its TMEM lane)
     const int et = threadIdx.x - 64;  // 0 .. ETHREADS - 1
+    // finish: lane -> rows lr + 8 i (i = 0..3) of the warp's 32, columns 4 c4 .. 4 c4 + 3 of the chunk
+    const int lr = lane >> 2, c4 = lane & 3;
+    float* tile = &xp_sh[warp - 2][0];
     uint32_t u = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int slot, z, bx, by;
       Epi<float> e;
       if (!unit(w, slot, z, bx, by, e)) continue;
       const int m0 = by * BM, n0 = bx * BN;
-      const int r = m0 + rl;
-      const bool rowok = r < n;
-      asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");  // the previous unit's readers of cf_sh / dr_sh are done
+      asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");  // the previous unit's readers of the scale arrays are done
       if (et < BN) {
         const int c = n0 + et;
         const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
         cf_sh[et] = ec == kNanExp ? NAN : scalbnf(1.f, ec - 6);
         dr_sh[et] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
       }
+      if (et == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ed_sh[k] = e.d[k];
+          eout_sh[k] = e.out[k];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) ec_sh[k][qq] = e.c[k][qq];
+        }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) ein_sh[qq] = e.in[qq];
+      }
+      if (et < BM) {
+        const int r = m0 + et;
+        const int er = (r < n) ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+        rf_sh[et] = er == kNanExp ? NAN : scalbnf(1.f, er - 6 - 21);  // row scale / 2^21
+        dl_sh[et] = (r < n) ? e.L[(size_t)r * n + r] : 0.f;           // diagonal of L
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");
-      // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
-      // the int8 GEMM carries Yl Yr (each row / column scaled without its
-      // diagonal, which in the squaring phase dominates), the rest is
-      // elementwise work here.  The operand rows of the first chunk are
-      // fetched while the MMAs still run.
-      float lrow[CW], rrow[CW];
-#define I8_LOAD_ROWS(C0)                                                                       \
-  do {                                                                                         \
-    const int c0_ = (C0);                                                                      \
-    if (rowok && c0_ + CW <= n) {                                                              \
-      const float4* lp = reinterpret_cast<const float4*>(e.L + (size_t)r * n + c0_);           \
-      const float4* rp = reinterpret_cast<const float4*>(e.R + (size_t)r * n + c0_);           \
-      _Pragma("unroll") for (int j = 0; j < CW / 4; ++j) {                                     \
-        const float4 a = __ldg(lp + j);                                                        \
-        lrow[4 * j] = a.x; lrow[4 * j + 1] = a.y; lrow[4 * j + 2] = a.z; lrow[4 * j + 3] = a.w; \
-        const float4 bb = (e.R == e.L) ? a : __ldg(rp + j);                                    \
-        rrow[4 * j] = bb.x; rrow[4 * j + 1] = bb.y; rrow[4 * j + 2] = bb.z; rrow[4 * j + 3] = bb.w; \
-      }                                                                                        \
-    } else {                                                                                   \
-      _Pragma("unroll") for (int j = 0; j < CW; ++j) {                                         \
-        const bool ok_ = rowok && c0_ + j < n;                                                 \
-        lrow[j] = ok_ ? e.L[(size_t)r * n + c0_ + j] : 0.f;                                     \
-        rrow[j] = ok_ ? e.R[(size_t)r * n + c0_ + j] : 0.f;                                     \
-      }                                                                                        \
-    }                                                                                          \
-  } while (0)
-      I8_LOAD_ROWS(n0 + hh * CPART);
-      const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
-      const float rf = er == kNanExp ? NAN : scalbnf(1.f, er - 6 - 21);  // row scale / 2^21
-      const float dl = rowok ? e.L[(size_t)r * n + r] : 0.f;            // diagonal of L for this row
+      const float rf = rf_sh[rl];
+      const float* const eL = e.L;
+      const float* const eR = e.R;
+      const float ealpha = e.alpha;
+      const int enin = e.nin, enout = e.nout;
+      const bool ecolnorm = e.colnorm;
       tc::mbar_wait(&tfull_bar, u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       // ---- drain: the unit's accumulators -> y (registers), then TMEM goes back ----
@@ -904,103 +909,103 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&tempty_bar)) : "memory");
       // ---- finish: overlapped with the next unit's MMAs ----
+      // L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R with D = diagonal, Y = the rest:
+      // the int8 GEMM carried Yl Yr (each row / column scaled without its
+      // diagonal, which in the squaring phase dominates); the rest is
+      // elementwise.  Each chunk goes through a per-warp transpose tile so that
+      // a lane owns 4 consecutive columns of 4 rows: every global access is a
+      // float4 and a warp instruction covers 8 rows x 64 contiguous bytes (one
+      // thread per row, 16 bytes at a time, read every sector twice and the
+      // evaluation stages' epilogues ran longer than their MMAs).
 #pragma unroll
       for (int cb = 0; cb < NCH; ++cb) {
         const int cl0 = hh * CPART + cb * CW;
         const int c0 = n0 + cl0;
-        const bool full = rowok && c0 + CW <= n;
-        if (cb > 0) I8_LOAD_ROWS(c0);
-        float o0[CW];
+        __syncwarp();  // the previous chunk's readers of the tile are done
 #pragma unroll
-        for (int j = 0; j < CW; ++j) {
-          const float dr = dr_sh[cl0 + j];
-          const float v = (c0 + j == r) ? fmaf(dl, dr, y[cb * CW + j])
-                                        : fmaf(dl, rrow[j], fmaf(lrow[j], dr, y[cb * CW + j]));
-          o0[j] = e.alpha * v;
-        }
-        for (int qq = 0; qq < e.nin; ++qq) {
-          const float cq = e.c[0][qq];
-          if (cq == 0.f || !rowok) continue;
-          const float* ip = e.in[qq] + (size_t)r * n + c0;
-          if (full) {
+        for (int j = 0; j < CW; j += 4)
+          *reinterpret_cast<float4*>(tile + lane * TLD + j) =
+              make_float4(y[cb * CW + j], y[cb * CW + j + 1], y[cb * CW + j + 2], y[cb * CW + j + 3]);
+        __syncwarp();
+        const int c = c0 + 4 * c4;
+        const bool colok = c < n;  // n % 16 == 0 on this path: a column quad is all in or all out
+        const float4 dr4 = *reinterpret_cast<const float4*>(dr_sh + cl0 + 4 * c4);
+        const float drv[4] = {dr4.x, dr4.y, dr4.z, dr4.w};
+        double cs[4] = {0.0, 0.0, 0.0, 0.0};  // column abs-sums over this lane's rows
+        const bool same = eR == eL;
+        // two rows at a time, straight-line: every load of the pair is issued
+        // before the first use (read-only loads, out-of-range rows clamped to a
+        // valid address and only their stores predicated), so a chunk costs two
+        // memory round trips, not one per row
 #pragma unroll
-            for (int j = 0; j < CW; j += 4) {
-              const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
-              o0[j] = fmaf(cq, x.x, o0[j]); o0[j + 1] = fmaf(cq, x.y, o0[j + 1]);
-              o0[j + 2] = fmaf(cq, x.z, o0[j + 2]); o0[j + 3] = fmaf(cq, x.w, o0[j + 3]);
+        for (int ip = 0; ip < 4; ip += 2) {
+          bool ok[2];
+          size_t off[2];
+          float4 yv4[2], lv4[2], rv4[2], xin[2][4];
+          int rr[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int rw = lr + 8 * (ip + h);
+            rr[h] = m0 + q * 32 + rw;
+            ok[h] = colok && rr[h] < n;
+            off[h] = ok[h] ? (size_t)rr[h] * n + c : 0;
+            yv4[h] = *reinterpret_cast<const float4*>(tile + rw * TLD + 4 * c4);
+            lv4[h] = __ldg(reinterpret_cast<const float4*>(eL + off[h]));
+            rv4[h] = same ? lv4[h] : __ldg(reinterpret_cast<const float4*>(eR + off[h]));
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+              xin[h][qq] = qq < enin ? __ldg(reinterpret_cast<const float4*>(ein_sh[qq] + off[h]))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = rr[h];
+            const float dl = dl_sh[q * 32 + lr + 8 * (ip + h)];
+            const float yv[4] = {yv4[h].x, yv4[h].y, yv4[h].z, yv4[h].w}, lv[4] = {lv4[h].x, lv4[h].y, lv4[h].z, lv4[h].w},
+                        rv[4] = {rv4[h].x, rv4[h].y, rv4[h].z, rv4[h].w};
+            float base[4];  // out[0]; out[k > 0] adds its own combination and identity shift to it
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float v = (c + j == r) ? fmaf(dl, drv[j], yv[j]) : fmaf(dl, rv[j], fmaf(lv[j], drv[j], yv[j]));
+              base[j] = ealpha * v;
             }
-          } else {
 #pragma unroll
-            for (int j = 0; j < CW; ++j)
-              if (c0 + j < n) o0[j] = fmaf(cq, ip[j], o0[j]);
-          }
-        }
-        if (e.d[0] != 0.f && r >= c0 && r < c0 + CW) {
+            for (int k = 0; k < 3; ++k) {
+              float o[4] = {base[0], base[1], base[2], base[3]};
 #pragma unroll
-          for (int j = 0; j < CW; ++j)
-            if (c0 + j == r) o0[j] = fmaf(e.d[0], 1.f, o0[j]);
-        }
-        if (rowok) {
-          float* op = e.out[0] + (size_t)r * n + c0;
-          if (full) {
+              for (int qq = 0; qq < 4; ++qq) {
+                const float cq = ec_sh[k][qq];
+                const float xv[4] = {xin[h][qq].x, xin[h][qq].y, xin[h][qq].z, xin[h][qq].w};
 #pragma unroll
-            for (int j = 0; j < CW; j += 4)
-              *reinterpret_cast<float4*>(op + j) = make_float4(o0[j], o0[j + 1], o0[j + 2], o0[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < CW; ++j)
-              if (c0 + j < n) op[j] = o0[j];
-          }
-        }
-        for (int k = 1; k < e.nout; ++k) {
-          float ok[CW];
-#pragma unroll
-          for (int j = 0; j < CW; ++j) ok[j] = o0[j];
-          for (int qq = 0; qq < e.nin; ++qq) {
-            const float cq = e.c[k][qq];
-            if (cq == 0.f || !rowok) continue;
-            const float* ip = e.in[qq] + (size_t)r * n + c0;
-            if (full) {
-#pragma unroll
-              for (int j = 0; j < CW; j += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(ip + j));
-                ok[j] = fmaf(cq, x.x, ok[j]); ok[j + 1] = fmaf(cq, x.y, ok[j + 1]);
-                ok[j + 2] = fmaf(cq, x.z, ok[j + 2]); ok[j + 3] = fmaf(cq, x.w, ok[j + 3]);
+                for (int j = 0; j < 4; ++j) o[j] = cq != 0.f ? fmaf(cq, xv[j], o[j]) : o[j];  // (0 * Inf stays out)
               }
-            } else {
 #pragma unroll
-              for (int j = 0; j < CW; ++j)
-                if (c0 + j < n) ok[j] = fmaf(cq, ip[j], ok[j]);
-            }
-          }
-          if (e.d[k] != 0.f && r >= c0 && r < c0 + CW) {
+              const float dk = ed_sh[k];
 #pragma unroll
-            for (int j = 0; j < CW; ++j)
-              if (c0 + j == r) ok[j] = fmaf(e.d[k], 1.f, ok[j]);
-          }
-          if (rowok) {
-            float* op = e.out[k] + (size_t)r * n + c0;
-            if (full) {
+              for (int j = 0; j < 4; ++j) o[j] = (dk != 0.f && c + j == r) ? fmaf(dk, 1.f, o[j]) : o[j];
+              if (ok[h] && k < enout) *reinterpret_cast<float4*>(eout_sh[k] + off[h]) = make_float4(o[0], o[1], o[2], o[3]);
+              if (k == 0) {
 #pragma unroll
-              for (int j = 0; j < CW; j += 4)
-                *reinterpret_cast<float4*>(op + j) = make_float4(ok[j], ok[j + 1], ok[j + 2], ok[j + 3]);
-            } else {
+                for (int j = 0; j < 4; ++j) base[j] = o[j];
+                if (ecolnorm && ok[h]) {  // (binary64 conversions: only the power stages pay for them)
 #pragma unroll
-              for (int j = 0; j < CW; ++j)
-                if (c0 + j < n) op[j] = ok[j];
+                  for (int j = 0; j < 4; ++j) cs[j] += fabs((double)o[j]);
+                }
+              }
             }
           }
         }
-        if (e.colnorm) {
+        if (ecolnorm) {
           // deterministic column abs-sums of this 128-row tile (select.py:193):
-          // a fixed shuffle tree over each warp's 32 rows, then the 4 warps of
-          // this column part in lane-quarter order
+          // the lane's 4 rows, a fixed shuffle tree over the 8 lanes sharing a
+          // column quad, then the 4 warps of this column part in quarter order
 #pragma unroll
-          for (int j = 0; j < CW; ++j) {
-            double v = rowok ? fabs((double)o0[j]) : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red_sh[hh * 4 + q][j] = v;
+          for (int j = 0; j < 4; ++j) {
+            double v = cs[j];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (lr == 0) red_sh[hh * 4 + q][4 * c4 + j] = v;
           }
           asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
           if (rl < CW && c0 + rl < n) {
@@ -1011,7 +1016,6 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
           asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
         }
       }
-#undef I8_LOAD_ROWS
       ++u;
     }
   }

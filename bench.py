@@ -500,17 +500,18 @@ def run_lowrank(args):
 
 
 def _launch_count(key, m, s, n, dtype="f64"):
-    """Kernels of ours launched by one expm call (host orchestration is deterministic):
-    n > 64: colsum, two k_select, elem, nonfinite, finish + one launch per product
-    stage (W^2, E1..E3 as present, one per squaring level); on the int8-slice path
-    (fp32, n >= 512) a product stage is five kernels (stats, route, slice,
-    int8 GEMM, FFMA GEMM for routed-away products)."""
+    """Kernels of ours launched by one expm call (host orchestration is deterministic
+    and sync-free): n <= 64 one fused kernel.  n > 64 (one chunk): colsum, two
+    k_select, k_bucket, elem, nonfinite, finish + one launch per product stage:
+    W^2, E1..E3 and every squaring level up to the cap of 20 (levels beyond the
+    batch's largest s find an empty device-side bucket and exit at once).  On
+    the int8-slice path (fp32, n >= 320, n % 16 == 0) a product stage is four
+    kernels (prep, route, int8 stage, FFMA GEMM for routed-away products)."""
     if n <= 64:
         return 1
-    m = np.asarray(m); s = np.asarray(s)
-    stages = 1 + int((m >= 4).any()) + int((m >= 8).any()) + int((m >= 15).any()) + int(s.max())
-    per = 5 if (dtype == "f32" and n >= 512 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
-    return int(6 + stages * per)
+    stages = 4 + 20
+    per = 4 if (dtype == "f32" and n >= 320 and n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0") else 1
+    return int(7 + stages * per)
 
 
 def _shard_indices(cfg, rank: int, ws: int, scaling: str, batch: int = 0) -> np.ndarray:
@@ -713,7 +714,7 @@ def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool =
     else:
         roof["kernel"] = "gemm_stage_kernel" + (" (DMMA)" if cfg.dtype == "f64" else " (FFMA2)")
     roof["other"] = cmp_roof if hbm_binds else hbm_roof
-    if (cfg.dtype == "f32" and cfg.n >= 512 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0"
+    if (cfg.dtype == "f32" and cfg.n >= 320 and cfg.n % 16 == 0 and os.environ.get("EXPMB_I8", "") != "0"
             and not tg):
         # products run as exact int8-slice GEMMs on tcgen05 (gemm_i8.cuh): ten
         # int8 slice-pair products per fp32 product; the FFMA peak stays the
@@ -725,7 +726,8 @@ def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool =
         roof = {"bound": "tensor", "achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": ipk,
                 "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / ipk, "traffic": None,
                 "peak_source": isrc, "executed_int8_ops_per_launch": i8_ops,
-                "kernel": "i8::k_i8_stage (int8-slice tcgen05) + gemm_stage_kernel for routed-away products",
+                "kernel": "i8::k_i8_stage (persistent int8-slice tcgen05 stage, split epilogue) after i8::k_i8_prep; "
+                          "gemm_stage_kernel for routed-away products",
                 "other": ffma_view}
     if tg:
         # the time-grid path skips the evaluation products: its roofline is over

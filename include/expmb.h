@@ -68,7 +68,7 @@ double expmb_unit_roundoff(int dtype);
 
 /* Scratch bytes expmb_expm needs for this problem: 256 for n <= 64 (the
  * persistent kernels' work counter; optional there), the bucketed pipeline's
- * buffers for n > 64 (plus the int8-slice planes for fp32 n >= 512 unless
+ * buffers for n > 64 (plus the int8-slice planes for fp32 n >= 320 unless
  * EXPMB_I8=0).  Replaces nothing in the reference (numpy allocates per op). */
 size_t expmb_workspace_bytes(int64_t batch, int32_t n, int dtype, int scheme);
 

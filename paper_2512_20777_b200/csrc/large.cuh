@@ -44,18 +44,20 @@ namespace expmb {
 // ---------------------------------------------------------------------------
 constexpr int kLargeBufsSastre = 7;  // W2 Y0 Y1 La Ra Lb Rb   (Tmp aliases Lb)
 constexpr int kLargeBufsPS = 6;      // W2 W3 W4 Q0 Q1 Tmp
-// Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh):
-// opt-in with EXPMB_I8=1 (EXPMB_I8=0 forces the FFMA GEMM).
-// Default: on for fp32 n >= 512 (measured crossover, tools/i8_crossover.py:
-// 1.07x at 512, 1.38x at 768, 1.67x at 1024, 2.1x at 1536, 0.88x at 384);
-// EXPMB_I8=1 also enables it from n = 256, EXPMB_I8=0 disables it.  Each product is routed per matrix
-// (k_i8_route): operands that are not "flat" go to the FFMA GEMM.
+// Exact int8-slice (Ozaki) products on tcgen05 for fp32 (gemm_i8.cuh).
+// Default: on for fp32 n >= 320 with n % 16 == 0, the measured crossover
+// against the FFMA GEMM (tools/i8_crossover.py, round 2 with the persistent
+// stage and the fast prep pass: 0.85x at 256, 1.17x at 320, 1.13x at 384,
+// 1.40x at 448, 1.48x at 512, 1.93x at 768, 2.40x at 1024, 2.96x at 1536).
+// EXPMB_I8=1 also enables it from n = 256, EXPMB_I8=0 disables it.  Each
+// product is routed per matrix (k_i8_route): operands that are not "flat" go
+// to the FFMA GEMM.
 static inline bool use_i8_path(int n, int esize) {
   const char* e = getenv("EXPMB_I8");
   if (esize != 4 || n % 16 != 0) return false;
   if (e != nullptr && e[0] == '0') return false;
   if (e != nullptr && e[0] == '1') return n >= 256;
-  return n >= 512;
+  return n >= 320;
 }
 static inline int i8_np(int n) { return (n + 15) / 16 * 16; }
 constexpr size_t kLargeWsCap = (size_t)40 << 30;  // bound on the big buffers

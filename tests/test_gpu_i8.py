@@ -1,5 +1,5 @@
 """The exact int8-slice tensor-core GEMM path (gemm_i8.cuh; default for fp32
-n >= 512, EXPMB_I8=1 from n = 256) against the oracle: dense inputs over
+n >= 320, EXPMB_I8=1 from n = 256) against the oracle: dense inputs over
 three norm scales (the squaring phase's dominant diagonal included), ragged
 column tiles, PS, non-finite input, and the per-product routing: graded
 operands (entries ~2^20 apart within a row, where per-row scaling would lose
@@ -71,8 +71,24 @@ def test_i8_routes_graded_operands_to_ffma(monkeypatch):
     assert torch.equal(ref, got)
 
 
+def test_i8_default_from_320(monkeypatch):
+    """The default crossover: n = 320 runs on the int8-slice path (a different
+    result from the FFMA GEMM in the last places), n = 304 does not."""
+    monkeypatch.delenv("EXPMB_I8", raising=False)
+    rng = np.random.default_rng(11)
+    for n, differs in ((320, True), (304, False)):
+        W = (rng.standard_normal((2, n, n)) * (6.0 / n ** 0.5)).astype(np.float32)
+        _check(W, 2.0 ** -24)
+        Wt = torch.as_tensor(W, device="cuda")
+        dflt = X.expm(Wt, 2.0 ** -24).value.clone()
+        monkeypatch.setenv("EXPMB_I8", "0")
+        ffma = X.expm(Wt, 2.0 ** -24).value.clone()
+        monkeypatch.delenv("EXPMB_I8", raising=False)
+        assert (not torch.equal(dflt, ffma)) == differs, n
+
+
 def test_i8_default_on_for_large_dense(monkeypatch):
-    """Without EXPMB_I8 the path is on for n >= 512 and matches the oracle."""
+    """Without EXPMB_I8 the path is on for n >= 320 and matches the oracle."""
     monkeypatch.delenv("EXPMB_I8", raising=False)
     n = 1024
     rng = np.random.default_rng(9)

@@ -3,7 +3,7 @@ import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, '.')
 import paper_2512_20777_b200 as X
-for n, B in ((384, 256), (512, 128), (768, 64), (1024, 32), (1536, 16)):
+for n, B in ((256, 1024), (320, 512), (384, 256), (448, 256), (512, 128), (768, 64), (1024, 32), (1536, 16)):
     W = torch.as_tensor((np.random.default_rng(n).standard_normal((B, n, n)) * (8.0 / n ** 0.5)).astype(np.float32), device="cuda")
     res = {}
     for flag in ("0", "1"):

@@ -950,11 +950,11 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
             ok[h] = colok && rr[h] < n;
             off[h] = ok[h] ? (size_t)rr[h] * n + c : 0;
             yv4[h] = *reinterpret_cast<const float4*>(tile + rw * TLD + 4 * c4);
-            lv4[h] = __ldg(reinterpret_cast<const float4*>(eL + off[h]));
-            rv4[h] = same ? lv4[h] : __ldg(reinterpret_cast<const float4*>(eR + off[h]));
+            lv4[h] = __ldcs(reinterpret_cast<const float4*>(eL + off[h]));
+            rv4[h] = same ? lv4[h] : __ldcs(reinterpret_cast<const float4*>(eR + off[h]));
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq)
-              xin[h][qq] = qq < enin ? __ldg(reinterpret_cast<const float4*>(ein_sh[qq] + off[h]))
+              xin[h][qq] = qq < enin ? __ldcs(reinterpret_cast<const float4*>(ein_sh[qq] + off[h]))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
@@ -983,7 +983,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
               const float dk = ed_sh[k];
 #pragma unroll
               for (int j = 0; j < 4; ++j) o[j] = (dk != 0.f && c + j == r) ? fmaf(dk, 1.f, o[j]) : o[j];
-              if (ok[h] && k < enout) *reinterpret_cast<float4*>(eout_sh[k] + off[h]) = make_float4(o[0], o[1], o[2], o[3]);
+              if (ok[h] && k < enout) __stcs(reinterpret_cast<float4*>(eout_sh[k] + off[h]), make_float4(o[0], o[1], o[2], o[3]));
               if (k == 0) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) base[j] = o[j];

@@ -188,12 +188,10 @@ __device__ __forceinline__ void slice_quad(const float (&x)[4], int e, bool fast
 // sum of the binary exponents and the count of the nonzero entries, packed in
 // one 64-bit integer atomicAdd (deterministic).
 constexpr int kExpBias = 200;
-__device__ __forceinline__ unsigned long long exp_pack(float a) {
-  return a > 0.f && a < INFINITY ? ((unsigned long long)(ilogbf(a) + kExpBias) << 20) | 1ull : 0ull;
-}
-// The same sums in two 32-bit accumulators (the streaming prep pass): esum
-// collects the biased exponents (ilogb + 127) of the finite nonzero entries,
-// cnt their number; exp_pack_sum gives the sum of exp_pack over them.
+// The packed statistic of a set of entries is sum over its finite nonzero
+// members of ((ilogb + kExpBias) << 20 | 1).  It is gathered in two 32-bit
+// accumulators: esum collects the biased exponents (ilogb + 127), cnt the
+// number of such entries; exp_pack_sum packs them.
 __device__ __forceinline__ void exp_acc(float v, int& esum, int& cnt) {  // v >= 0 or NaN
   const uint32_t bits = __float_as_uint(v);
   const uint32_t e8 = bits >> 23;
@@ -240,23 +238,25 @@ __device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, const I8O
     for (int u = 0; u < 4; ++u)
       if (c + u == r) lf[u] = rf[u] = 0.f;  // diagonal: handled exactly in the epilogue
   }
-  int m = 0;
-  unsigned long long sm = 0;
+  int m = 0, esum = 0, ecnt = 0;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     m = max(m, __float_as_int(lf[u]));
-    sm += exp_pack(lf[u]);
+    exp_acc(lf[u], esum, ecnt);
+    int ce = 0, cc1 = 0;
+    exp_acc(rf[u], ce, cc1);
     cmax[i][4 * q + u] = __float_as_int(rf[u]);
-    csum[i][4 * q + u] = exp_pack(rf[u]);
+    csum[i][4 * q + u] = exp_pack_sum(ce, cc1);
   }
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) {  // the 8 lanes sharing row i
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    esum += __shfl_xor_sync(0xffffffffu, esum, o);
+    ecnt += __shfl_xor_sync(0xffffffffu, ecnt, o);
   }
   if (q == 0 && r < n) {
     if (m) atomicMax(b.er + (size_t)slot * n + r, m);
-    if (sm) atomicAdd(b.rc + (size_t)slot * n + r, sm);
+    if (ecnt) atomicAdd(b.rc + (size_t)slot * n + r, exp_pack_sum(esum, ecnt));
   }
   __syncthreads();
   if (threadIdx.x < 32 && c0 + threadIdx.x < n) {
@@ -355,10 +355,6 @@ __device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, const I8O
   int8_t* bs = b.bs + (size_t)slot * NSL * plane;
   const int* er = b.er + (size_t)slot * n;
   const int* ec = b.ec + (size_t)slot * n;
-  auto pack = [](const int8_t (&v)[4][4], int j) {  // plane j of four elements -> one 32-bit word
-    return (uint32_t)(uint8_t)v[0][j] | ((uint32_t)(uint8_t)v[1][j] << 8) | ((uint32_t)(uint8_t)v[2][j] << 16) |
-           ((uint32_t)(uint8_t)v[3][j] << 24);
-  };
   {
     // L row slices: row i, columns 4q..4q+3 (one float4 in, one 32-bit word per plane out)
     const int i = threadIdx.x / 8, q = threadIdx.x % 8;
@@ -373,11 +369,12 @@ __device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, const I8O
       for (int u = 0; u < 4; ++u)
         if (c + u == r) x[u] = y[u] = 0.f;
       const int ex = exp_of(__int_as_float(er[r]));
-      int8_t sl[4][4];
+      float sc;
+      const bool fast = slice_scale(ex, sc);
+      uint32_t w[4];
+      slice_quad(x, ex, fast, sc, w);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) slice4(x[u], ex, sl[u]);
-#pragma unroll
-      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + (size_t)r * b.np + c) = pack(sl, j);
+      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + (size_t)r * b.np + c) = w[j];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) tile[i][4 * q + u] = y[u];
@@ -389,11 +386,13 @@ __device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, const I8O
     const int c = c0 + ci, k = r0 + 4 * q;
     if (c < n && k < n) {
       const int ex = exp_of(__int_as_float(ec[c]));
-      int8_t sl[4][4];
+      float sc;
+      const bool fast = slice_scale(ex, sc);
+      const float x[4] = {tile[4 * q][ci], tile[4 * q + 1][ci], tile[4 * q + 2][ci], tile[4 * q + 3][ci]};
+      uint32_t w[4];
+      slice_quad(x, ex, fast, sc, w);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) slice4(tile[4 * q + u][ci], ex, sl[u]);
-#pragma unroll
-      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(bs + j * plane + (size_t)c * b.np + k) = pack(sl, j);
+      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(bs + j * plane + (size_t)c * b.np + k) = w[j];
     }
   }
 }

@@ -724,7 +724,9 @@ def measure(key: str, args, steps: int, warmup: int, cpu: bool, timegrid: bool =
         ffma_view.pop("other", None)
         ipk, isrc = pk["i8_tops"], pk["i8_src"]
         roof = {"bound": "tensor", "achieved": i8_ops / (ms_per_step * 1e-3) / 1e12, "peak": ipk,
-                "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / ipk, "traffic": None,
+                "unit": "TOPS", "frac": i8_ops / (ms_per_step * 1e-3) / 1e12 / ipk, "traffic": traffic,
+                "traffic_note": "DRAM bytes of ONE stage launch (profiles/ncu_traffic_C5.json); a step is 24 stage "
+                                "launches, per-stage bytes in profiles/stage_metrics_C5_r02.txt",
                 "peak_source": isrc, "executed_int8_ops_per_launch": i8_ops,
                 "kernel": "i8::k_i8_stage (persistent int8-slice tcgen05 stage, split epilogue) after i8::k_i8_prep; "
                           "gemm_stage_kernel for routed-away products",

@@ -711,7 +711,7 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
   __shared__ float rf_sh[BM];    // 2^(er - 27) per row
   __shared__ float dl_sh[BM];    // diagonal of L for this unit's rows
   __shared__ __align__(16) float xp_sh[EXPMB_I8_EPI_WARPS][32 * TLD];  // per-warp transpose tile of a chunk
-  __shared__ double red_sh[EXPMB_I8_EPI_WARPS][16];  // colnorm partials: one per epilogue warp and chunk column
+  __shared__ double red_sh[EXPMB_I8_EPI_WARPS][BN / EPI_PARTS];  // colnorm partials: one per epilogue warp and column
   // the unit's stage program, read by every epilogue thread with dynamic
   // indices: shared memory, not a per-thread local-memory copy (the ~28 KB of
   // L1 left beside the ring is swept by the epilogue's streaming loads)
@@ -996,24 +996,29 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
         }
         if (ecolnorm) {
           // deterministic column abs-sums of this 128-row tile (select.py:193):
-          // the lane's 4 rows, a fixed shuffle tree over the 8 lanes sharing a
-          // column quad, then the 4 warps of this column part in quarter order
+          // the lane's 4 rows, then a fixed shuffle tree over the 8 lanes
+          // sharing a column quad; the warps' partials meet once per unit below
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             double v = cs[j];
             v += __shfl_xor_sync(0xffffffffu, v, 4);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
             v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (lr == 0) red_sh[hh * 4 + q][4 * c4 + j] = v;
+            if (lr == 0) red_sh[hh * 4 + q][cb * CW + 4 * c4 + j] = v;
           }
-          asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
-          if (rl < CW && c0 + rl < n) {
-            const double a = ((red_sh[hh * 4][rl] + red_sh[hh * 4 + 1][rl]) + red_sh[hh * 4 + 2][rl]) +
-                             red_sh[hh * 4 + 3][rl];
-            g.part[((size_t)z * g.tiles_m + by) * n + c0 + rl] = a;
-          }
-          asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
         }
+      }
+      if (ecolnorm) {
+        // the 4 warps of this column part in lane-quarter order (one barrier
+        // pair per unit: a pair per chunk kept the warps in lockstep and
+        // serialised their memory round trips)
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
+        if (rl < CPART && n0 + hh * CPART + rl < n) {
+          const double a = ((red_sh[hh * 4][rl] + red_sh[hh * 4 + 1][rl]) + red_sh[hh * 4 + 2][rl]) +
+                           red_sh[hh * 4 + 3][rl];
+          g.part[((size_t)z * g.tiles_m + by) * n + n0 + hh * CPART + rl] = a;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
       }
       ++u;
     }

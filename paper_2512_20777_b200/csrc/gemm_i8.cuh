@@ -141,8 +141,8 @@ __device__ __forceinline__ void slice4(float x, int e, int8_t (&s)[4]) {
 // precomputed power of two (slice_scale), each rint is a magic-number add
 // whose low mantissa byte is the digit (1.5 2^(23 - 7i) puts the mantissa's
 // last place at 2^(-7i), round-to-nearest-even like rintf), and the residual
-// stays unscaled.  Bit-identical to slice4 (tests: EXPMB_I8_PREP=0 runs
-// slice4 in k_i8_slice).
+// stays unscaled.  The digits are those of slice4 (checked element by
+// element on the host over six exponent ranges and the rounding ties).
 __device__ __forceinline__ bool slice_scale(int e, float& sc) {  // false: use slice4 (NaN/Inf row, extreme exponent)
   sc = 0.f;
   if (e == kNanExp || e < -100 || e > 100) return false;
@@ -181,12 +181,29 @@ __device__ __forceinline__ void slice_quad(const float (&x)[4], int e, bool fast
   }
 }
 
-// One pass over 32x32 tiles: row maxima of |L| and column maxima of |R|
-// (diagonals excluded: they are handled exactly in the epilogue) as the bit
-// patterns of non-negative floats, which order like the values (NaN above
-// Inf), combined with atomicMax into er / ec; and, for the routing test, the
-// sum of the binary exponents and the count of the nonzero entries, packed in
-// one 64-bit integer atomicAdd (deterministic).
+// Row maxima of |L| and column maxima of |R| are kept as the bit patterns of
+// non-negative floats, which order like the values (NaN above Inf); for the
+// routing test, the sum of the binary exponents and the count of the nonzero
+// entries of every row / column travel packed in one 64-bit integer.
+//
+// The diagonal.  In the squaring phase X = I + (small), so a diagonal entry
+// would set its row's (column's) scale and cost the off-diagonal entries
+// their low bits; such a diagonal entry is SPLIT off (sliced as zero) and
+// applied in the stage's epilogue: L R = Yl Yr + D_L Yr + Yl D_R + D_L D_R.
+// Where the diagonal entry is no larger than the largest off-diagonal entry
+// of its row of L (column of R) it is KEPT in the slices (the scale, and with
+// it the routing test, is unchanged) and that row's D_L (column's D_R) is
+// zero: a unit whose rows and columns all keep their diagonal skips the
+// epilogue's two operand tiles.  The choice is per row / column and recorded
+// in the sign bit of er / ec.
+constexpr int kDiagKept = (int)0x80000000;
+__device__ __forceinline__ int scale_bits(int v) { return v & 0x7fffffff; }
+__device__ __forceinline__ bool diag_kept(int v) { return v < 0; }
+// keep the diagonal entry (|d| as bits) of a row / column whose largest
+// off-diagonal magnitude is moff (bits)?  Finite, nonzero off-diagonal mass only.
+__device__ __forceinline__ bool keep_diag(int dbits, int moff) {
+  return moff > 0 && moff < 0x7f800000 && dbits <= moff;  // (non-negative floats order like their bits)
+}
 constexpr int kExpBias = 200;
 // The packed statistic of a set of entries is sum over its finite nonzero
 // members of ((ilogb + kExpBias) << 20 | 1).  It is gathered in two 32-bit
@@ -220,95 +237,6 @@ __device__ __forceinline__ bool i8_slot_ops(const GemmCtx<float>& g, int stage, 
   return true;
 }
 
-__device__ __forceinline__ void i8_stats_tile(const GemmCtx<float>& g, const I8Ops& e, const Bufs& b, int slot, int bx,
-                                              int by) {
-  __shared__ int cmax[32][33];
-  __shared__ unsigned long long csum[32][33];
-  const int n = g.n;  // a multiple of 16 on this path: groups of 4 columns are all in or all out
-  const int r0 = by * 32, c0 = bx * 32;
-  const int i = threadIdx.x / 8, q = threadIdx.x % 8;  // row i of the tile, columns 4q..4q+3
-  const int r = r0 + i, c = c0 + 4 * q;
-  float lf[4] = {0.f, 0.f, 0.f, 0.f}, rf[4] = {0.f, 0.f, 0.f, 0.f};
-  if (r < n && c < n) {
-    const float4 a = *reinterpret_cast<const float4*>(e.L + (size_t)r * n + c);
-    const float4 bb = e.R == e.L ? a : *reinterpret_cast<const float4*>(e.R + (size_t)r * n + c);
-    lf[0] = fabsf(a.x); lf[1] = fabsf(a.y); lf[2] = fabsf(a.z); lf[3] = fabsf(a.w);
-    rf[0] = fabsf(bb.x); rf[1] = fabsf(bb.y); rf[2] = fabsf(bb.z); rf[3] = fabsf(bb.w);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (c + u == r) lf[u] = rf[u] = 0.f;  // diagonal: handled exactly in the epilogue
-  }
-  int m = 0, esum = 0, ecnt = 0;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    m = max(m, __float_as_int(lf[u]));
-    exp_acc(lf[u], esum, ecnt);
-    int ce = 0, cc1 = 0;
-    exp_acc(rf[u], ce, cc1);
-    cmax[i][4 * q + u] = __float_as_int(rf[u]);
-    csum[i][4 * q + u] = exp_pack_sum(ce, cc1);
-  }
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {  // the 8 lanes sharing row i
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    esum += __shfl_xor_sync(0xffffffffu, esum, o);
-    ecnt += __shfl_xor_sync(0xffffffffu, ecnt, o);
-  }
-  if (q == 0 && r < n) {
-    if (m) atomicMax(b.er + (size_t)slot * n + r, m);
-    if (ecnt) atomicAdd(b.rc + (size_t)slot * n + r, exp_pack_sum(esum, ecnt));
-  }
-  __syncthreads();
-  if (threadIdx.x < 32 && c0 + threadIdx.x < n) {
-    const int cc = threadIdx.x;
-    int mm = 0;
-    unsigned long long ss = 0;
-    for (int k = 0; k < 32; ++k) {
-      mm = max(mm, cmax[k][cc]);
-      ss += csum[k][cc];
-    }
-    if (mm) atomicMax(b.ec + (size_t)slot * n + c0 + cc, mm);
-    if (ss) atomicAdd(b.cc + (size_t)slot * n + c0 + cc, ss);
-  }
-}
-// Units (slot, 32x32 tile) over the first *dcount slots, grid-strided.
-// (8 CTAs/SM: the per-unit work is a short latency chain, occupancy hides it)
-__global__ void __launch_bounds__(256, 8) k_i8_stats(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                      Bufs b, const int* __restrict__ dcount, int hcount) {
-  const int cnt = dcount ? *dcount : hcount;
-  const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
-  const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
-  // a contiguous run of units per CTA: the slot's operands are looked up once
-  // per slot, not per 32x32 tile
-  const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int w1 = min(total, (int)blockIdx.x * per + per);
-  int cur = -1;
-  bool valid = false;
-  I8Ops ops{};
-  for (int w = blockIdx.x * per; w < w1; ++w) {
-    const int slot = w / tiles, t = w - slot * tiles;
-    if (slot != cur) {
-      cur = slot;
-      valid = i8_slot_ops(g, stage, list, slot, ops);
-    }
-    if (!valid) continue;
-    __syncthreads();  // shared tiles of the previous unit
-    i8_stats_tile(g, ops, b, slot, t % t32, t / t32);
-  }
-}
-
-// Zero the per-slot exponent / routing accumulators of the first *dcount slots.
-__global__ void __launch_bounds__(256) k_i8_zero(Bufs b, int n, const int* __restrict__ dcount, int hcount) {
-  const int cnt = dcount ? *dcount : hcount;
-  const size_t tot = (size_t)cnt * n;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
-    b.er[i] = 0;
-    b.ec[i] = 0;
-    b.rc[i] = 0ull;
-    b.cc[i] = 0ull;
-  }
-}
-
 // Route a product to this path only when every row of L and every column of
 // R is "flat": its largest entry's binary exponent exceeds the mean exponent
 // of its nonzero entries by at most 4, so typical entries keep >= 23 of the
@@ -336,7 +264,7 @@ __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, c
   if (part) {
     for (int i = threadIdx.x; i < n; i += 256) {
       const size_t o = (size_t)slot * n + i;
-      flat &= flat_ok(b.er[o], b.rc[o]) && flat_ok(b.ec[o], b.cc[o]);
+      flat &= flat_ok(scale_bits(b.er[o]), b.rc[o]) && flat_ok(scale_bits(b.ec[o]), b.cc[o]);
     }
   }
   flat = __syncthreads_and(flat);
@@ -344,89 +272,14 @@ __global__ void __launch_bounds__(256) k_i8_route(GemmCtx<float> g, int stage, c
   }
 }
 
-// One pass over 32x32 tiles: L slices row-major, R slices transposed (both K-major).
-__device__ __forceinline__ void i8_slice_tile(const GemmCtx<float>& g, const I8Ops& e, const Bufs& b, int slot, int bx,
-                                              int by) {
-  __shared__ float tile[32][33];
-  const int n = g.n;  // a multiple of 16 on this path
-  const int r0 = by * 32, c0 = bx * 32;
-  const size_t plane = (size_t)n * b.np;
-  int8_t* as = b.as + (size_t)slot * NSL * plane;
-  int8_t* bs = b.bs + (size_t)slot * NSL * plane;
-  const int* er = b.er + (size_t)slot * n;
-  const int* ec = b.ec + (size_t)slot * n;
-  {
-    // L row slices: row i, columns 4q..4q+3 (one float4 in, one 32-bit word per plane out)
-    const int i = threadIdx.x / 8, q = threadIdx.x % 8;
-    const int r = r0 + i, c = c0 + 4 * q;
-    float x[4] = {0.f, 0.f, 0.f, 0.f}, y[4] = {0.f, 0.f, 0.f, 0.f};
-    if (r < n && c < n) {
-      const float4 a = *reinterpret_cast<const float4*>(e.L + (size_t)r * n + c);
-      const float4 bb = e.R == e.L ? a : *reinterpret_cast<const float4*>(e.R + (size_t)r * n + c);
-      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-      y[0] = bb.x; y[1] = bb.y; y[2] = bb.z; y[3] = bb.w;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + u == r) x[u] = y[u] = 0.f;
-      const int ex = exp_of(__int_as_float(er[r]));
-      float sc;
-      const bool fast = slice_scale(ex, sc);
-      uint32_t w[4];
-      slice_quad(x, ex, fast, sc, w);
-#pragma unroll
-      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(as + j * plane + (size_t)r * b.np + c) = w[j];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) tile[i][4 * q + u] = y[u];
-  }
-  __syncthreads();
-  {
-    // R column slices, transposed: column ci, k = 4q..4q+3 of the tile
-    const int ci = threadIdx.x / 8, q = threadIdx.x % 8;
-    const int c = c0 + ci, k = r0 + 4 * q;
-    if (c < n && k < n) {
-      const int ex = exp_of(__int_as_float(ec[c]));
-      float sc;
-      const bool fast = slice_scale(ex, sc);
-      const float x[4] = {tile[4 * q][ci], tile[4 * q + 1][ci], tile[4 * q + 2][ci], tile[4 * q + 3][ci]};
-      uint32_t w[4];
-      slice_quad(x, ex, fast, sc, w);
-#pragma unroll
-      for (int j = 0; j < NSL; ++j) *reinterpret_cast<uint32_t*>(bs + j * plane + (size_t)c * b.np + k) = w[j];
-    }
-  }
-}
-__global__ void __launch_bounds__(256, 8) k_i8_slice(GemmCtx<float> g, int stage, const int* __restrict__ list,
-                                                      Bufs b, const int* __restrict__ dcount, int hcount) {
-  const int cnt = dcount ? *dcount : hcount;
-  const int t32 = (g.n + 31) / 32, tiles = t32 * t32;
-  const int total = cnt * tiles;  // < 2^31: slots x 32x32 tiles of a chunk
-  const int per = (total + gridDim.x - 1) / gridDim.x;  // contiguous units per CTA (see k_i8_stats)
-  const int w1 = min(total, (int)blockIdx.x * per + per);
-  int cur = -1;
-  bool valid = false;
-  I8Ops ops{};
-  for (int w = blockIdx.x * per; w < w1; ++w) {
-    const int slot = w / tiles, t = w - slot * tiles;
-    if (slot != cur) {
-      cur = slot;
-      valid = b.ok[slot] && i8_slot_ops(g, stage, list, slot, ops);
-    }
-    if (!valid) continue;
-    __syncthreads();  // the transpose tile of the previous unit
-    i8_slice_tile(g, ops, b, slot, t % t32, t / t32);
-  }
-}
-
-// One pass per operand instead of stats (32 x 32 tiles, atomics) + slice:
+// The prep pass: one streaming pass per operand.
 //  - an L unit is 8 rows, one warp per row: the warp reads its row once for
-//    the maximum |entry| and the exponent sums (no atomics: the row is whole
-//    in one warp) and once more, from L1/L2, to cut the four slices;
+//    the maximum |entry|, the diagonal decision and the exponent sums (no
+//    atomics: the row is whole in one warp) and once more, from L1/L2, to cut
+//    the four slices;
 //  - an R unit is a 32-column strip: 8 warps stream its rows for the column
 //    maxima (a shared-memory reduction), then re-read it in 32 x 32 tiles
 //    and write the transposed slices.
-// Same outputs (er / rc / ec / cc / as / bs) and bits as k_i8_stats +
-// k_i8_slice; the diagonal is left out exactly as there.
 #ifndef EXPMB_I8_PREP_MINB
 #define EXPMB_I8_PREP_MINB 4
 #endif
@@ -434,14 +287,16 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
                                              int slot, int r) {
   const int n = g.n, lane = threadIdx.x & 31;
   const float* row = L + (size_t)r * n;
-  int m = 0, esum = 0, ecnt = 0;
+  int m = 0, esum = 0, ecnt = 0, dgb = 0;  // off-diagonal maximum and statistics; |diagonal| bits
 #pragma unroll 4
   for (int c = 4 * lane; c < n; c += 128) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
     const float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const float v = c + u == r ? 0.f : fabsf(x[u]);
+      const bool isd = c + u == r;
+      const float v = isd ? 0.f : fabsf(x[u]);
+      dgb = isd ? __float_as_int(fabsf(x[u])) : dgb;
       m = max(m, __float_as_int(v));
       exp_acc(v, esum, ecnt);
     }
@@ -449,11 +304,13 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    dgb = max(dgb, __shfl_xor_sync(0xffffffffu, dgb, o));
     esum += __shfl_xor_sync(0xffffffffu, esum, o);
     ecnt += __shfl_xor_sync(0xffffffffu, ecnt, o);
   }
+  const bool keep = keep_diag(dgb, m);
   if (lane == 0) {
-    b.er[(size_t)slot * n + r] = m;
+    b.er[(size_t)slot * n + r] = m | (keep ? kDiagKept : 0);
     b.rc[(size_t)slot * n + r] = exp_pack_sum(esum, ecnt);
   }
   const int ex = exp_of(__int_as_float(m));
@@ -467,7 +324,7 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
     float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (c + u == r) x[u] = 0.f;
+      if (!keep && c + u == r) x[u] = 0.f;
     uint32_t w[4];
     slice_quad(x, ex, fast, sc, w);
 #pragma unroll
@@ -478,14 +335,16 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
                                              int slot, int c0) {
   __shared__ int pm[32][33];
   __shared__ unsigned long long ps[32][33];
+  __shared__ int pd[32][33];  // |diagonal| bits seen by each row phase
   __shared__ int pex[32];
+  __shared__ int pkeep[32];
   __shared__ float psc[32];
   __shared__ float tile[32][33];
   const int n = g.n;  // a multiple of 16 on this path: a float4 group is all in or all out
   // pass 1: thread (row phase ty = 0..31, column quad q4 = 0..7) streams float4s
   const int q4 = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int cq = c0 + 4 * q4;
-  int m[4] = {0, 0, 0, 0}, esum[4] = {0, 0, 0, 0}, ecnt[4] = {0, 0, 0, 0};
+  int m[4] = {0, 0, 0, 0}, esum[4] = {0, 0, 0, 0}, ecnt[4] = {0, 0, 0, 0}, dgb[4] = {0, 0, 0, 0};
   if (cq < n) {
 #pragma unroll 4
     for (int k = ty; k < n; k += 32) {
@@ -493,7 +352,9 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
       const float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float v = k == cq + u ? 0.f : fabsf(x[u]);
+        const bool isd = k == cq + u;
+        const float v = isd ? 0.f : fabsf(x[u]);
+        dgb[u] = isd ? __float_as_int(fabsf(x[u])) : dgb[u];
         m[u] = max(m[u], __float_as_int(v));
         exp_acc(v, esum[u], ecnt[u]);
       }
@@ -502,21 +363,25 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     pm[ty][4 * q4 + u] = m[u];
+    pd[ty][4 * q4 + u] = dgb[u];
     ps[ty][4 * q4 + u] = exp_pack_sum(esum[u], ecnt[u]);
   }
   __syncthreads();
   if (threadIdx.x < 32) {
     const int cl = threadIdx.x, c = c0 + cl;
-    int mm = 0;
+    int mm = 0, dd = 0;
     unsigned long long ss = 0;
     for (int w = 0; w < 32; ++w) {
       mm = max(mm, pm[w][cl]);
+      dd = max(dd, pd[w][cl]);
       ss += ps[w][cl];
     }
+    const bool keep = keep_diag(dd, mm);
     if (c < n) {
-      b.ec[(size_t)slot * n + c] = mm;
+      b.ec[(size_t)slot * n + c] = mm | (keep ? kDiagKept : 0);
       b.cc[(size_t)slot * n + c] = ss;
     }
+    pkeep[cl] = keep ? 1 : 0;
     pex[cl] = exp_of(__int_as_float(mm));
     float sc;
     psc[cl] = slice_scale(pex[cl], sc) ? sc : 0.f;  // 0: slice4 path
@@ -552,7 +417,7 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
         const int k = kt + ty;
         const float x[4] = {cur[t].x, cur[t].y, cur[t].z, cur[t].w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = k == cq + u ? 0.f : x[u];
+        for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = (k == cq + u && !pkeep[4 * q4 + u]) ? 0.f : x[u];
       }
       __syncthreads();
       const int cc = c0 + ci, k = kt + 4 * q;
@@ -851,11 +716,15 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       if (!unit(w, slot, z, bx, by, e)) continue;
       const int m0 = by * BM, n0 = bx * BN;
       asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");  // the previous unit's readers of the scale arrays are done
+      int mine = 0;  // this thread set a nonzero split diagonal entry
       if (et < BN) {
         const int c = n0 + et;
-        const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
+        const int ecb = (c < n) ? bf.ec[(size_t)slot * n + c] : kDiagKept;
+        const int ec = exp_of(__int_as_float(scale_bits(ecb)));
         cf_sh[et] = ec == kNanExp ? NAN : scalbnf(1.f, ec - 6);
-        dr_sh[et] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
+        const float dr = diag_kept(ecb) ? 0.f : e.R[(size_t)c * n + c];  // D_R: split diagonal entries only
+        dr_sh[et] = dr;
+        mine |= dr != 0.f;
       }
       if (et == 0) {
 #pragma unroll
@@ -870,11 +739,22 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
       }
       if (et < BM) {
         const int r = m0 + et;
-        const int er = (r < n) ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+        const int erb = (r < n) ? bf.er[(size_t)slot * n + r] : kDiagKept;
+        const int er = exp_of(__int_as_float(scale_bits(erb)));
         rf_sh[et] = er == kNanExp ? NAN : scalbnf(1.f, er - 6 - 21);  // row scale / 2^21
-        dl_sh[et] = (r < n) ? e.L[(size_t)r * n + r] : 0.f;           // diagonal of L
+        const float dl = diag_kept(erb) ? 0.f : e.L[(size_t)r * n + r];  // D_L: split diagonal entries only
+        dl_sh[et] = dl;
+        mine |= dl != 0.f;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(ETHREADS) : "memory");
+      // barrier + OR: does any row / column of this unit carry a split diagonal
+      // entry?  If none does, the finish phase skips the two operand tiles.
+      int need_lr;
+      asm volatile(
+          "{\n .reg .pred p, q;\n setp.ne.b32 q, %1, 0;\n barrier.cta.red.or.pred p, 1, %2, q;\n"
+          " selp.b32 %0, 1, 0, p;\n}\n"
+          : "=r"(need_lr)
+          : "r"(mine), "n"(ETHREADS)
+          : "memory");
       const float rf = rf_sh[rl];
       const float* const eL = e.L;
       const float* const eR = e.R;
@@ -949,8 +829,8 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
             ok[h] = colok && rr[h] < n;
             off[h] = ok[h] ? (size_t)rr[h] * n + c : 0;
             yv4[h] = *reinterpret_cast<const float4*>(tile + rw * TLD + 4 * c4);
-            lv4[h] = __ldcs(reinterpret_cast<const float4*>(eL + off[h]));
-            rv4[h] = same ? lv4[h] : __ldcs(reinterpret_cast<const float4*>(eR + off[h]));
+            lv4[h] = need_lr ? __ldcs(reinterpret_cast<const float4*>(eL + off[h])) : make_float4(0.f, 0.f, 0.f, 0.f);
+            rv4[h] = (same || !need_lr) ? lv4[h] : __ldcs(reinterpret_cast<const float4*>(eR + off[h]));
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq)
               xin[h][qq] = qq < enin ? __ldcs(reinterpret_cast<const float4*>(ein_sh[qq] + off[h]))
@@ -965,7 +845,9 @@ k_i8_stage(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, const
             float base[4];  // out[0]; out[k > 0] adds its own combination and identity shift to it
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float v = (c + j == r) ? fmaf(dl, drv[j], yv[j]) : fmaf(dl, rv[j], fmaf(lv[j], drv[j], yv[j]));
+              // y + D_L Yr + Yl D_R + D_L D_R at (r, c): Yr(r, r) = R(r, r) - D_R(r), Yl likewise
+              const float yr = rv[j] - ((c + j == r) ? drv[j] : 0.f);
+              const float v = fmaf(dl, yr, fmaf(lv[j], drv[j], yv[j]));
               base[j] = ealpha * v;
             }
 #pragma unroll
@@ -1083,9 +965,10 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
 
   if (threadIdx.x < BN) {
     const int c = n0 + threadIdx.x;
-    const int ec = (c < n) ? exp_of(__int_as_float(bf.ec[(size_t)slot * n + c])) : 0;
+    const int ecb = (c < n) ? bf.ec[(size_t)slot * n + c] : kDiagKept;
+    const int ec = exp_of(__int_as_float(scale_bits(ecb)));
     cs_sh[threadIdx.x] = ec == kNanExp ? (double)NAN : ldexp(1.0, ec - 6);
-    dr_sh[threadIdx.x] = (c < n) ? e.R[(size_t)c * n + c] : 0.f;
+    dr_sh[threadIdx.x] = diag_kept(ecb) ? 0.f : e.R[(size_t)c * n + c];  // D_R: split diagonal entries only
   }
   const int rank = MC ? (int)(blockIdx.x & 1) : 0;  // cluster dims (2, 1, 1): the rank is blockIdx.x % 2
   if (threadIdx.x == 0) {
@@ -1186,9 +1069,10 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
     }                                                                                          \
   } while (0)
     I8_LOAD_ROWS(n0 + hh * CPART);
-    const int er = rowok ? exp_of(__int_as_float(bf.er[(size_t)slot * n + r])) : 0;
+    const int erb = rowok ? bf.er[(size_t)slot * n + r] : kDiagKept;
+    const int er = exp_of(__int_as_float(scale_bits(erb)));
     const double rs21 = er == kNanExp ? (double)NAN : ldexp(1.0, er - 6 - 21);  // row scale / 2^21
-    const double dl = rowok ? (double)e.L[(size_t)r * n + r] : 0.0;  // diagonal of L for this row
+    const double dl = diag_kept(erb) ? 0.0 : (double)e.L[(size_t)r * n + r];  // D_L: the split diagonal entry of this row
     tc::mbar_wait(&tmem_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     double* red = reinterpret_cast<double*>(sm) + hh * (CW * BM);  // the smem ring is idle now
@@ -1214,7 +1098,8 @@ k_i8_stage_np(const __grid_constant__ Maps maps, GemmCtx<float> g, int stage, co
                             (long long)a3[j];
         double y = (double)T * rs21 * cs_sh[cl0 + j];
         const double dr = (double)dr_sh[cl0 + j];
-        y += (c == r) ? dl * dr : dl * (double)rrow[j] + (double)lrow[j] * dr;
+        // D_L Yr + Yl D_R + D_L D_R at (r, c): Yr(r, r) = R(r, r) - D_R(r), Yl likewise
+        y += dl * ((double)rrow[j] - ((c == r) ? dr : 0.0)) + (double)lrow[j] * dr;
         o0[j] = e.alpha * (float)y;
       }
       for (int qq = 0; qq < e.nin; ++qq) {

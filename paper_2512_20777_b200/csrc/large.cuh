@@ -347,31 +347,15 @@ static int i8_launch(const i8::Maps& maps, const GemmCtx<float>& g, int stage, c
     if (e != cudaSuccess) fprintf(stderr, "expmb i8 stage %d: %s failed: %s\n", stage, what, cudaGetErrorString(e));
     return e != cudaSuccess ? 1 : 0;
   };
-  static int occ_stats = 0, occ_slice = 0, occ_zero = 0, occ_stage = 0;
-  const int t32 = (n + 31) / 32;
-  const int64_t u32 = (int64_t)count * t32 * t32;
-  // one streaming pass per operand (k_i8_prep); EXPMB_I8_PREP=0: the round-1
-  // stats (32 x 32 tiles, atomics) + route + slice sequence
-  const bool prep = !(getenv("EXPMB_I8_PREP") && getenv("EXPMB_I8_PREP")[0] == '0');  // read per call (tests A/B it)
-  static int occ_prep = 0;
-  if (prep) {
+  static int occ_stage = 0, occ_prep = 0;
+  {
+    // one streaming pass per operand: scales, diagonal decision, routing statistics, slices
     const int64_t units = (int64_t)count * ((n + 7) / 8 + (n + 31) / 32);
     i8::k_i8_prep<<<persistent_grid(i8::k_i8_prep, 256, 0, units, &occ_prep), 256, 0, st>>>(g, stage, list, b,
                                                                                         dcount, count);
     if (chk("prep")) return 1;
     i8::k_i8_route<<<std::min(count, sm_count_dev() * 8), 256, 0, st>>>(g, stage, list, b, dcount, count);
     if (chk("route")) return 1;
-  } else {
-  i8::k_i8_zero<<<persistent_grid(i8::k_i8_zero, 256, 0, ((int64_t)count * n + 255) / 256, &occ_zero), 256, 0, st>>>(
-      b, n, dcount, count);
-  i8::k_i8_stats<<<persistent_grid(i8::k_i8_stats, 256, 0, u32, &occ_stats, 8), 256, 0, st>>>(g, stage, list, b,
-                                                                                            dcount, count);
-  if (chk("stats")) return 1;
-  i8::k_i8_route<<<std::min(count, sm_count_dev() * 8), 256, 0, st>>>(g, stage, list, b, dcount, count);
-  if (chk("route")) return 1;
-  i8::k_i8_slice<<<persistent_grid(i8::k_i8_slice, 256, 0, u32, &occ_slice, 8), 256, 0, st>>>(g, stage, list, b,
-                                                                                            dcount, count);
-  if (chk("slice")) return 1;
   }
   // persistent stage with the split epilogue (default); EXPMB_I8_PERSIST=0: one unit per CTA
   const bool persist = !(getenv("EXPMB_I8_PERSIST") && getenv("EXPMB_I8_PERSIST")[0] == '0');  // read per call (tests A/B it)

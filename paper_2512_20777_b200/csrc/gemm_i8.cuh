@@ -14,23 +14,28 @@
 //   P[r][c] = 2^(er_r + ec_c - 12) sum_{L=0..3} 2^(-7L) acc_L[r][c],
 //   acc_L = sum_{i+j=L} S_i T_j  (int32 on tcgen05.mma.kind::i8, exact)
 // Ten slice-pair GEMMs (pairs with i + j > 3 contribute < 2^-28 of the row and
-// column maxima and are dropped), the level sum and the scaling in binary64,
-// then one rounding to fp32.  The diagonal of each operand is split off and
-// applied exactly in the epilogue (L R = Yl Yr + D_L Y_R + Y_L D_R + D_L D_R),
-// so the squaring phase's dominant diagonal does not set the row scale.
-// Measured on C5 (tools/i8_debug.py): 1.5x the FFMA GEMM's throughput and a
-// smaller error (worst 4.8e-7 vs 2.1e-6).  Limitation: the scale is per row
-// / column, so entries far below their row's maximum keep fewer bits than in
-// fp32 -- on graded matrices (entries ~2^20 apart within a row) the error is
-// 30x the FFMA path's (tools/i8_graded_probe.py).  Hence opt-in (EXPMB_I8=1,
-// fp32, n % 16 == 0).
+// column maxima and are dropped), the level sum as one exact 64-bit integer,
+// one rounding to fp32 and the power-of-two scales.  A diagonal entry that
+// exceeds its row's (column's) off-diagonal maximum is split off and applied
+// in the epilogue (L R = Yl Yr + D_L Yr + Yl D_R + D_L D_R), so the squaring
+// phase's dominant diagonal does not set the row scale.  Limitation: the
+// scale is per row / column, so entries far below their row's maximum keep
+// fewer bits than in fp32 -- on graded matrices (entries ~2^20 apart within a
+// row) the error is 30x the FFMA path's (tools/i8_graded_probe.py).  Hence
+// every product is routed per matrix (k_i8_route): only operands whose rows
+// and columns are "flat" run here, the rest on the FFMA GEMM.  Default for
+// fp32 n >= 320, n % 16 == 0 (large.cuh: use_i8_path).
 //
-// Kernels: k_i8_rowexp / k_i8_colexp (exponents), k_i8_slice_rows (L slices,
-// K-major), k_i8_slice_cols (R slices transposed to K-major), k_i8_stage
-// (TMA 64B-swizzled 2-stage ring of 4 L slices + 4 R slices per k-tile, one thread
-// issuing the ten pair MMAs per 32-byte k-step into four int32 TMEM
-// accumulators, four epilogue warps applying the stage's fused linear
-// combination exactly as gemm_simt.cuh's epilogue does).
+// Kernels: k_i8_prep (scales, diagonal decision, routing statistics and the
+// four int8 slices of each operand, K-major, in one streaming pass per
+// operand), k_i8_route (the flatness test), k_i8_stage (persistent: a TMA
+// 64B-swizzled 3-stage ring of 4 L + 4 R slices per 64-byte k-tile, one
+// thread issuing the concatenated-slice MMAs into four int32 TMEM level
+// accumulators, eight epilogue warps draining them and applying the stage's
+// fused linear combination as gemm_simt.cuh's epilogue does, overlapped with
+// the next unit's MMAs); k_i8_stage_np is the one-unit-per-CTA form
+// (EXPMB_I8_PERSIST=0), optionally as 2-CTA clusters sharing the L panel by
+// TMA multicast.
 #pragma once
 
 #include <cuda.h>

@@ -292,16 +292,15 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
                                              int slot, int r) {
   const int n = g.n, lane = threadIdx.x & 31;
   const float* row = L + (size_t)r * n;
-  int m = 0, esum = 0, ecnt = 0, dgb = 0;  // off-diagonal maximum and statistics; |diagonal| bits
+  int m = 0, esum = 0, ecnt = 0;  // off-diagonal maximum and statistics
+  const int dgb = __float_as_int(fabsf(__ldg(row + r)));  // |diagonal entry| bits
 #pragma unroll 4
   for (int c = 4 * lane; c < n; c += 128) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
     const float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const bool isd = c + u == r;
-      const float v = isd ? 0.f : fabsf(x[u]);
-      dgb = isd ? __float_as_int(fabsf(x[u])) : dgb;
+      const float v = c + u == r ? 0.f : fabsf(x[u]);
       m = max(m, __float_as_int(v));
       exp_acc(v, esum, ecnt);
     }
@@ -309,7 +308,6 @@ __device__ __forceinline__ void i8_prep_rows(const GemmCtx<float>& g, const floa
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    dgb = max(dgb, __shfl_xor_sync(0xffffffffu, dgb, o));
     esum += __shfl_xor_sync(0xffffffffu, esum, o);
     ecnt += __shfl_xor_sync(0xffffffffu, ecnt, o);
   }
@@ -340,7 +338,6 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
                                              int slot, int c0) {
   __shared__ int pm[32][33];
   __shared__ unsigned long long ps[32][33];
-  __shared__ int pd[32][33];  // |diagonal| bits seen by each row phase
   __shared__ int pex[32];
   __shared__ int pkeep[32];
   __shared__ float psc[32];
@@ -349,7 +346,7 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
   // pass 1: thread (row phase ty = 0..31, column quad q4 = 0..7) streams float4s
   const int q4 = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int cq = c0 + 4 * q4;
-  int m[4] = {0, 0, 0, 0}, esum[4] = {0, 0, 0, 0}, ecnt[4] = {0, 0, 0, 0}, dgb[4] = {0, 0, 0, 0};
+  int m[4] = {0, 0, 0, 0}, esum[4] = {0, 0, 0, 0}, ecnt[4] = {0, 0, 0, 0};
   if (cq < n) {
 #pragma unroll 4
     for (int k = ty; k < n; k += 32) {
@@ -357,9 +354,7 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
       const float x[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const bool isd = k == cq + u;
-        const float v = isd ? 0.f : fabsf(x[u]);
-        dgb[u] = isd ? __float_as_int(fabsf(x[u])) : dgb[u];
+        const float v = k == cq + u ? 0.f : fabsf(x[u]);
         m[u] = max(m[u], __float_as_int(v));
         exp_acc(v, esum[u], ecnt[u]);
       }
@@ -368,17 +363,16 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     pm[ty][4 * q4 + u] = m[u];
-    pd[ty][4 * q4 + u] = dgb[u];
     ps[ty][4 * q4 + u] = exp_pack_sum(esum[u], ecnt[u]);
   }
   __syncthreads();
   if (threadIdx.x < 32) {
     const int cl = threadIdx.x, c = c0 + cl;
-    int mm = 0, dd = 0;
+    const int dd = c < n ? __float_as_int(fabsf(__ldg(R + (size_t)c * n + c))) : 0;  // |diagonal entry| bits
+    int mm = 0;
     unsigned long long ss = 0;
     for (int w = 0; w < 32; ++w) {
       mm = max(mm, pm[w][cl]);
-      dd = max(dd, pd[w][cl]);
       ss += ps[w][cl];
     }
     const bool keep = keep_diag(dd, mm);
@@ -400,6 +394,7 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
     return (cq < n && k < n) ? __ldg(reinterpret_cast<const float4*>(R + (size_t)k * n + cq))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   };
+  const bool kept[4] = {pkeep[4 * q4] != 0, pkeep[4 * q4 + 1] != 0, pkeep[4 * q4 + 2] != 0, pkeep[4 * q4 + 3] != 0};
   // software pipelined in groups of four tiles: the next group's four loads
   // per thread are in flight while this group is sliced (one load in flight
   // per thread left the strip latency-bound: 4 KB per CTA per DRAM round trip)
@@ -422,7 +417,7 @@ __device__ __forceinline__ void i8_prep_cols(const GemmCtx<float>& g, const floa
         const int k = kt + ty;
         const float x[4] = {cur[t].x, cur[t].y, cur[t].z, cur[t].w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = (k == cq + u && !pkeep[4 * q4 + u]) ? 0.f : x[u];
+        for (int u = 0; u < 4; ++u) tile[ty][4 * q4 + u] = (k == cq + u && !kept[u]) ? 0.f : x[u];
       }
       __syncthreads();
       const int cc = c0 + ci, k = kt + 4 * q;
